@@ -1,0 +1,343 @@
+#!/usr/bin/env python3
+"""Benchmark: ODE system-windows integrated per second on B200 (FP64).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl bode|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+Workload (BASELINE.json configs[1]): RKCK on the Pleiades problem (N = 28),
+2^22 systems per GPU with the reference's perturbed initial conditions
+(perturbInitialConditions(pleiades_ic, 0.01, seed 42), problems.cpp:171-191).
+A "step" is one outer window of 0.1 time units over all systems (a restart,
+batch_driver.hpp:36-39); K = 10 steps is the paper's [0, 1] protocol
+(PAPER.md:652). value = systems x windows / device time (max over ranks),
+inputs resident in HBM; e2e = the same metric through the host-pointer C ABI
+(bode_int_driver) with pinned host buffers, H2D + D2H inside every step.
+The y array (940 MB) exceeds L2 (126 MB), so no L2 flush is needed.
+
+Multi-GPU: systems are independent, so each rank integrates its own 2^22
+systems with no collective on the data path (weak scaling); torch.distributed
+only provides the barrier and the max-over-ranks of the device time.
+
+Roofline: the path is FP64-compute bound (AI ~74 flop/B for RKCK-Pleiades);
+achieved = algorithmic flops (SURVEY.md 8d formulas on the per-system
+counters the kernel emits) / kernel time; peak = this device's DFMA
+throughput measured in the same run (MEASURED_PEAKS.json has no FP64 entry).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "tests"))
+
+METRIC = "ODE systems integrated/sec (RKCK, RKC) at 1/2/4/8 B200 vs CPU ref, %FP64 roof"
+UNIT = "system-windows/s"
+F_RHS = {"pleiades": 420, "heat": None, "expdecay": 1, "harmonic": 0}
+
+
+def algorithmic_flops(problem: str, solver: str, dim: int, stats: np.ndarray, windows: int) -> float:
+    """RKCK F = rhs*F_rhs + (acc+rej)*58*N;
+    RKC F = rhs*F_rhs + N*(10*S + 6*I + 7*C + 8) per window, I = rhs - 2 - S."""
+    f_rhs = (4 * dim - 2) if problem == "heat" else F_RHS[problem]
+    rhs = float(stats["rhs_evals"].sum())
+    if solver == "rkck":
+        att = float(stats["steps_accepted"].sum() + stats["steps_rejected"].sum())
+        return rhs * f_rhs + att * 58 * dim
+    S = float(stats["stages_total"].sum())
+    C = float(stats["spec_rad_evals"].sum())
+    n_sys = stats.size
+    I = rhs - 2.0 * windows * n_sys - S
+    return rhs * f_rhs + dim * (10 * S + 6 * I + 7 * C + 8.0 * windows * n_sys)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_rate(problem, solver, base, mag, seed, num, windows, g=None):
+    """The reference CPU path (oracle/_ref = unmodified reference sources;
+    fallback: the oracle restatement) on all host threads."""
+    from golden_cases import perturb
+    from oracle_lib import Oracle, RefLib, ref_available
+    from paper_1611_02274_b200 import _abi as A
+    prob = A.make_problem(problem, base.size)
+    solv = A.SOLVER_NAMES[solver]
+    y0 = perturb(base, mag, seed, num)
+    cores = os.cpu_count()
+    if ref_available():
+        lib, kind = RefLib(), "reference"
+        run = lambda y, t0, t1: lib.lib.ref_integrate_batch(
+            ctypes.byref(prob), solv, t0, t1, num, A.dptr(y), A.dptr(g),
+            ctypes.byref(A.default_tol()), None, cores)
+    else:
+        lib, kind = Oracle(), "port"
+        run = lambda y, t0, t1: lib.lib.orc_integrate_batch(
+            ctypes.byref(prob), solv, t0, t1, num, A.dptr(y), A.dptr(g),
+            ctypes.byref(A.default_tol()), None, cores)
+    y = y0.copy()
+    run(y, 0.0, 0.1)  # warm-up window
+    y = y0.copy()
+    t = time.perf_counter()
+    for k in range(windows):
+        t0 = 0.0 + k * 0.1
+        rc = run(y, t0, 0.0 + (k + 1) * 0.1)
+        assert rc == 0
+    dt = time.perf_counter() - t
+    return num * windows / dt, cores, kind, dt
+
+
+def run_reference_arm(args):
+    from golden_cases import PLEIADES_IC
+    rate, cores, kind, dt = cpu_reference_rate("pleiades", "rkck", PLEIADES_IC, 0.01, 42,
+                                               args.cpu_sample, args.warmup + args.steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / (args.warmup + args.steps) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "RKCK Pleiades, perturb 0.01 seed 42, eps 1e-10",
+                   "systems_sampled": args.cpu_sample, "window": 0.1},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{args.cpu_sample} systems x {args.warmup + args.steps} windows"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warmup, stream):
+    """K windows on HBM-resident state; per-launch CUDA events on `stream`."""
+    num = y0.size // dim
+    yd = torch.from_numpy(y0).to("cuda")
+    gd = torch.from_numpy(g0).to("cuda") if g0 is not None else None
+    st = torch.zeros(num * 8, dtype=torch.int64, device="cuda")
+    tol = A.default_tol()
+    prob = P.OdeProblem(A.PROBLEM_NAMES[problem], dim, 0 if g0 is None else 1)
+    gp = gd.data_ptr() if gd is not None else 0
+
+    def window(k, merge):
+        t0 = 0.0 + (k % 10) * 0.1
+        P.int_driver_device(prob, solver, arith, t0, 0.0 + (k % 10 + 1) * 0.1, num, gp,
+                            yd.data_ptr(), tol, st.data_ptr(), merge, stream.cuda_stream)
+
+    with torch.cuda.stream(stream):
+        for k in range(warmup):
+            window(k, False)
+        yd.copy_(torch.from_numpy(y0))
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        n0 = P.lib().bode_launch_count()
+        ev[0].record(stream)
+        for k in range(steps):
+            window(k, k > 0)
+            ev[k + 1].record(stream)
+        torch.cuda.synchronize()
+    launches = P.lib().bode_launch_count() - n0
+    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)]
+    stats = st.cpu().numpy().view(A.STATS_DTYPE).copy()
+    return sum(per) / 1e3, per, stats, launches, yd
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="bode", choices=["bode", "reference"])
+    ap.add_argument("--num", type=int, default=1 << 22, help="systems per GPU")
+    ap.add_argument("--arith", default="fast", choices=["fast", "exact"])
+    ap.add_argument("--rkc-num", type=int, default=1 << 20)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 15)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference_arm(args)
+        return
+
+    import torch
+    import paper_1611_02274_b200 as P
+    from paper_1611_02274_b200 import _abi as A
+    from golden_cases import PLEIADES_IC, heat_ic, perturb
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    L = P.lib()
+    stream = torch.cuda.Stream()
+
+    peak = ctypes.c_double()
+    psec = ctypes.c_double()
+    P.api.check(L.bode_selftest_fp64_peak(ctypes.byref(peak), ctypes.byref(psec)))
+
+    # ---- headline: RKCK Pleiades, per-rank shard of args.num systems ----
+    num = args.num
+    y0 = perturb(PLEIADES_IC, 0.01, 42 + rank, num)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        secs, per, stats, launches, _ = measure_device(P, A, torch, "pleiades", "rkck",
+                                                       args.arith, 28, y0, None, args.steps,
+                                                       args.warmup, stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+        tt = torch.tensor([secs], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        secs = float(tt.item())
+    value = world * num * args.steps / secs
+    flops = algorithmic_flops("pleiades", "rkck", 28, stats, args.steps)
+    achieved = flops / sum(p / 1e3 for p in per)
+
+    # ---- e2e through the host-pointer C ABI (pinned buffers, H2D+D2H every window) ----
+    e2e = None
+    if not args.no_e2e:
+        yh = torch.from_numpy(y0.copy()).pin_memory()
+        sth = torch.zeros(num * 8, dtype=torch.int64).pin_memory()
+        yp = ctypes.cast(yh.data_ptr(), ctypes.POINTER(ctypes.c_double))
+        prob = A.make_problem(A.PLEIADES)
+        tol = A.default_tol()
+        ar = A.ARITH_NAMES[args.arith]
+        P.api.check(L.bode_int_driver(ctypes.byref(prob), 0, ar, 0.0, 0.1, num, None, yp,
+                                      ctypes.byref(tol), ctypes.c_void_p(sth.data_ptr()), 1))
+        yh.copy_(torch.from_numpy(y0))
+        if dist:
+            dist.barrier()
+        t = time.perf_counter()
+        for k in range(args.steps):
+            P.api.check(L.bode_int_driver(ctypes.byref(prob), 0, ar, 0.0 + (k % 10) * 0.1,
+                                          0.0 + (k % 10 + 1) * 0.1, num, None, yp,
+                                          ctypes.byref(tol), ctypes.c_void_p(sth.data_ptr()), 1))
+        e2e_s = time.perf_counter() - t
+        if dist:
+            tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        e2e = {"value": world * num * args.steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": num * 28 * 8, "d2h_bytes_per_step": num * (28 * 8 + 64),
+               "ms_per_step": e2e_s / args.steps * 1e3, "pinned_host": True}
+
+    # ---- secondary: RKC heat64 (config 3) on this GPU ----
+    rkc = None
+    if args.rkc_num > 0:
+        yh0 = perturb(heat_ic(64), 0.01, 42 + rank, args.rkc_num)
+        s2, per2, st2, l2, _ = measure_device(P, A, torch, "heat", "rkc", "exact", 64, yh0, None,
+                                              min(args.steps, 10), 1, stream)
+        f2 = algorithmic_flops("heat", "rkc", 64, st2, min(args.steps, 10))
+        rkc = {"workload": f"RKC heat n=64, {args.rkc_num} systems, exact arithmetic",
+               "value": args.rkc_num * min(args.steps, 10) / s2, "unit": UNIT,
+               "ms_per_step": s2 / min(args.steps, 10) * 1e3,
+               "achieved_tflops": f2 / s2 / 1e12, "frac_of_fp64_peak": f2 / s2 / peak.value,
+               "flop_per_system_window": f2 / (args.rkc_num * min(args.steps, 10))}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if not args.no_cpu:
+        rate, cores, kind, dt = cpu_reference_rate("pleiades", "rkck", PLEIADES_IC, 0.01, 42,
+                                                   args.cpu_sample, 10)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": f"{args.cpu_sample} Pleiades systems x 10 windows ([0,1]), all host "
+                         f"threads, {dt:.2f} s"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"RKCK Pleiades (N=28), {num} systems per GPU, perturb 0.01 "
+                               f"seed 42+rank, eps 1e-10, window 0.1 (restart)",
+                   "arith": args.arith, "systems_per_gpu": num, "window": 0.1,
+                   "l2": "state (num*28*8 B) exceeds the 126 MB L2; no flush needed",
+                   "parallelism": f"dp{world} (independent shards, no collective)"},
+        "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak.value / 1e12,
+                     "unit": "TFLOP/s", "frac": achieved / peak.value, "traffic": None,
+                     "peak_source": "DFMA microbenchmark on this device in this run "
+                                    "(MEASURED_PEAKS.json has no FP64 entry); nominal 37.2",
+                     "flop_per_system_window": flops / (num * args.steps),
+                     "kernel_ms_per_launch": sum(per) / len(per)},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clk.summary(), "rkc_heat64": rkc,
+        "work_per_system_window": {
+            "attempts": float((stats["steps_accepted"] + stats["steps_rejected"]).sum()) / (num * args.steps),
+            "rhs_evals": float(stats["rhs_evals"].sum()) / (num * args.steps)},
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,40 @@
+// dispatch.h -- compiled-kernel registry shared by kernels.cu and host.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace bode {
+
+constexpr int kMaxBlock = 256;
+
+struct DevTol {  // bode_tol_t, by value in the kernel parameters
+    double eps, abs_tol, rel_tol, uround, tiny, safety, p1, errcon, pgrow, pshrnk,
+        h_min_floor, kappa;
+};
+
+struct DevStats {  // bode_stats_t, per system (AoS, 64 bytes)
+    long long steps_accepted, steps_rejected, rhs_evals, spec_rad_evals, stages_total;
+    double h_min_seen, h_max_seen;
+    int underflow, reserved;
+};
+static_assert(sizeof(DevStats) == 64, "DevStats must match bode_stats_t");
+
+template <class P, int L>
+constexpr int C_of() { return P::N / L; }
+
+using LaunchFn = void (*)(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                          const double* g, double* y, DevStats* st, long long num, double t,
+                          double tEnd, DevTol tol, int merge);
+
+struct KernelEntry {
+    int kind, dim, param_dim, solver, arith;
+    int lanes;            // lanes per system (L)
+    int smem_per_thread;  // dynamic shared memory bytes per thread
+    int default_block;
+    const void* fn;
+    LaunchFn launch;
+};
+
+const KernelEntry* kernel_table(int* count);
+
+}  // namespace bode

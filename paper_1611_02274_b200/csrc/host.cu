@@ -1,0 +1,500 @@
+// host.cu -- C-ABI implementation (include/bode.h): argument validation with
+// the reference's error semantics, device buffers, multi-GPU sharding,
+// H2D/compute/D2H pipelining and the device-resident outer loop.
+//
+// Reference behaviour mirrored here:
+//   integrateBatch validation order  batch_driver.cpp:42-50
+//   ToleranceSettings::validate      ode_problem.hpp:46-53
+//   contiguous static partition      batch_driver.cpp:68-73 (here: across GPUs)
+//   outerLoop window schedule        batch_driver.cpp:99-105
+//   per-system stats merge           batch_driver.cpp:109-110, ode_problem.hpp:72-80
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/bode.h"
+#include "dispatch.h"
+
+namespace {
+
+using bode::DevStats;
+using bode::DevTol;
+using bode::KernelEntry;
+
+thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
+std::atomic<int> g_block_override{0};
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define BODE_CUDA(call)                                                                   \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(BODE_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+const double kPleiadesIC[28] = {
+    // data/pleiades_ic.txt (FNV-1a 0x5583feb418028048, problems.hpp:29):
+    // x1..x7, y1..y7, x'1..x'7, y'1..y'7
+    3.0,  3.0, -1.0, -3.0, 2.0, -2.0, 2.0,  3.0,  -3.0, 2.0, 0.0,  0.0,   -4.0, 4.0,
+    0.0,  0.0, 0.0,  0.0,  0.0, 1.75, -1.5, 0.0,  0.0,  0.0, -1.25, 1.0, 0.0,  0.0};
+
+DevTol to_dev(const bode_tol_t* t) {
+    DevTol d;
+    d.eps = t->eps;
+    d.abs_tol = t->abs_tol;
+    d.rel_tol = t->rel_tol;
+    d.uround = t->uround;
+    d.tiny = t->tiny;
+    d.safety = t->safety;
+    d.p1 = t->p1;
+    d.errcon = t->errcon;
+    d.pgrow = t->pgrow;
+    d.pshrnk = t->pshrnk;
+    d.h_min_floor = t->h_min_floor;
+    d.kappa = t->kappa;
+    return d;
+}
+
+const KernelEntry* find_entry(const bode_problem_t* p, int solver, int arith) {
+    int n = 0;
+    const KernelEntry* tab = bode::kernel_table(&n);
+    for (int i = 0; i < n; ++i) {
+        const KernelEntry& e = tab[i];
+        if (e.kind == p->kind && e.dim == p->dim && e.param_dim == p->param_dim &&
+            e.solver == solver && e.arith == arith)
+            return &e;
+    }
+    return nullptr;
+}
+
+int check_problem_shape(const bode_problem_t* p) {
+    if (p == nullptr) return fail(BODE_E_INVALID_SHAPE, "problem is NULL");
+    if (p->dim < 1) return fail(BODE_E_INVALID_SHAPE, "problem dim must be positive");
+    if (p->param_dim < 0) return fail(BODE_E_INVALID_SHAPE, "negative param_dim");
+    if (p->kind == BODE_PROBLEM_HEAT && p->dim < 2)
+        return fail(BODE_E_INVALID_SHAPE, "heatEquation: need at least two interior points");
+    return BODE_OK;
+}
+
+// Common validation of integrateBatch (batch_driver.cpp:42-50).
+int validate_call(const bode_problem_t* p, int solver, int arith, double t, double t_end,
+                  int64_t num, const void* g, const void* y, const bode_tol_t* tol,
+                  const KernelEntry** entry) {
+    if (!(t_end > t)) return fail(BODE_E_INVALID_INTERVAL, "integrateBatch: tNext must exceed t");
+    int rc = check_problem_shape(p);
+    if (rc) return rc;
+    if (num < 1) return fail(BODE_E_INVALID_SHAPE, "numSystems must be positive");
+    if (y == nullptr) return fail(BODE_E_INVALID_SHAPE, "state array is NULL");
+    if (p->param_dim > 0 && g == nullptr)
+        return fail(BODE_E_INVALID_SHAPE, "parameter array is NULL but param_dim > 0");
+    if (tol == nullptr) return fail(BODE_E_INVALID_SHAPE, "tolerance settings are NULL");
+    rc = bode_tol_validate(tol);
+    if (rc) return rc;
+    if (solver != BODE_SOLVER_RKCK && solver != BODE_SOLVER_RKC)
+        return fail(BODE_E_INVALID_SHAPE, "unknown solver");
+    if (arith != BODE_ARITH_EXACT && arith != BODE_ARITH_FAST)
+        return fail(BODE_E_INVALID_SHAPE, "unknown arithmetic policy");
+    *entry = find_entry(p, solver, arith);
+    if (*entry == nullptr)
+        return fail(BODE_E_UNSUPPORTED, "no device kernel compiled for this problem/dim/solver");
+    return BODE_OK;
+}
+
+int block_for(const KernelEntry* e) {
+    int b = g_block_override.load();
+    if (b <= 0) b = e->default_block;
+    return b;
+}
+
+// Launch one window over `num` systems resident on the current device.
+int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double* y,
+                  DevStats* st, long long num, double t, double tEnd, const DevTol& tol,
+                  int merge) {
+    const int block = block_for(e);
+    const long long threads = num * e->lanes;
+    const long long grid = (threads + block - 1) / block;
+    const size_t smem = (size_t)e->smem_per_thread * block;
+    if (smem > 48 * 1024) {
+        // per-device attribute; idempotent and cheap, so set it on every launch
+        BODE_CUDA(cudaFuncSetAttribute(e->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    }
+    e->launch(e->fn, dim3((unsigned)grid), dim3(block), smem, s, g, y, st, num, t, tEnd, tol,
+              merge);
+    g_launches.fetch_add(1);
+    BODE_CUDA(cudaGetLastError());
+    return BODE_OK;
+}
+
+// Per-device buffers reused across calls (no cudaMalloc on the hot path once warm).
+struct DeviceBuffers {
+    std::mutex m;
+    double* y = nullptr;
+    double* g = nullptr;
+    DevStats* st = nullptr;
+    size_t y_cap = 0, g_cap = 0, st_cap = 0;
+    cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+};
+
+DeviceBuffers g_dev[64];
+
+template <class T>
+int ensure(T** p, size_t* cap, size_t count) {
+    if (count <= *cap) return BODE_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    BODE_CUDA(cudaMalloc((void**)p, std::max<size_t>(count, 1) * sizeof(T)));
+    *cap = count;
+    return BODE_OK;
+}
+
+bool host_pinned(const void* ptr) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+struct Shard {
+    int device;
+    int64_t begin, count;
+};
+
+std::vector<Shard> make_shards(int64_t num, int gpus) {
+    std::vector<Shard> v;
+    const int64_t base = num / gpus, rem = num % gpus;
+    int64_t b = 0;
+    for (int d = 0; d < gpus; ++d) {
+        const int64_t len = base + (d < rem ? 1 : 0);
+        if (len > 0) v.push_back({d, b, len});
+        b += len;
+    }
+    return v;
+}
+
+int check_devices(int gpus) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        return fail(BODE_E_NO_DEVICE, "no CUDA device available (there is no CPU fallback)");
+    }
+    if (gpus < 1) return fail(BODE_E_INVALID_SHAPE, "num_gpus must be positive");
+    if (gpus > n) return fail(BODE_E_NO_DEVICE, "num_gpus exceeds the visible device count");
+    return BODE_OK;
+}
+
+// One shard of a host-pointer window: pipelined H2D -> kernel -> D2H in chunks
+// over up to three streams, so copies in both directions overlap compute.
+int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard& sh,
+                     int64_t num, const double* g, double* y, bode_stats_t* stats, double t,
+                     double tEnd, const DevTol& tol) {
+    BODE_CUDA(cudaSetDevice(sh.device));
+    DeviceBuffers& B = g_dev[sh.device];
+    std::lock_guard<std::mutex> lock(B.m);
+    const int N = p->dim, P = p->param_dim;
+    int rc = ensure(&B.y, &B.y_cap, (size_t)sh.count * N);
+    if (rc) return rc;
+    if (P > 0 && (rc = ensure(&B.g, &B.g_cap, (size_t)sh.count * P))) return rc;
+    if (stats && (rc = ensure(&B.st, &B.st_cap, (size_t)sh.count))) return rc;
+    for (auto& s : B.streams)
+        if (!s) BODE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+
+    const bool pinned = host_pinned(y);
+    const int64_t min_chunk = 1 << 16;
+    int nchunks = pinned ? (int)std::min<int64_t>(8, std::max<int64_t>(1, sh.count / min_chunk)) : 1;
+    const int64_t cbase = sh.count / nchunks, crem = sh.count % nchunks;
+    int64_t off = 0;
+    for (int k = 0; k < nchunks; ++k) {
+        const int64_t nk = cbase + (k < crem ? 1 : 0);
+        cudaStream_t s = B.streams[k % 3];
+        double* dy = B.y + off * N;
+        double* dg = P > 0 ? B.g + off * P : nullptr;
+        DevStats* dst = stats ? B.st + off : nullptr;
+        const int64_t src = sh.begin + off;
+        BODE_CUDA(cudaMemcpy2DAsync(dy, nk * sizeof(double), y + src, num * sizeof(double),
+                                    nk * sizeof(double), N, cudaMemcpyHostToDevice, s));
+        if (P > 0)
+            BODE_CUDA(cudaMemcpy2DAsync(dg, nk * sizeof(double), g + src, num * sizeof(double),
+                                        nk * sizeof(double), P, cudaMemcpyHostToDevice, s));
+        rc = launch_window(e, s, dg, dy, dst, nk, t, tEnd, tol, 0);
+        if (rc) return rc;
+        BODE_CUDA(cudaMemcpy2DAsync(y + src, num * sizeof(double), dy, nk * sizeof(double),
+                                    nk * sizeof(double), N, cudaMemcpyDeviceToHost, s));
+        if (stats)
+            BODE_CUDA(cudaMemcpyAsync(stats + src, dst, nk * sizeof(DevStats),
+                                      cudaMemcpyDeviceToHost, s));
+        off += nk;
+    }
+    for (auto& s : B.streams) BODE_CUDA(cudaStreamSynchronize(s));
+    return BODE_OK;
+}
+
+template <class F>
+int for_each_shard(const std::vector<Shard>& shards, F&& f) {
+    if (shards.size() == 1) return f(shards[0]);
+    std::vector<int> rcs(shards.size(), BODE_OK);
+    std::vector<std::string> msgs(shards.size());
+    std::vector<std::thread> pool;
+    for (size_t i = 0; i < shards.size(); ++i)
+        pool.emplace_back([&, i] {
+            rcs[i] = f(shards[i]);
+            if (rcs[i]) msgs[i] = g_last_error;
+        });
+    for (auto& th : pool) th.join();
+    for (size_t i = 0; i < shards.size(); ++i)
+        if (rcs[i]) return fail(rcs[i], msgs[i]);
+    return BODE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bode_version(void) { return "bode 0.1.0 (sm_100a, FP64)"; }
+const char* bode_last_error(void) { return g_last_error.c_str(); }
+
+int bode_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+void bode_tol_default(bode_tol_t* t) {  // ode_problem.hpp:33-44
+    t->eps = 1.0e-10;
+    t->abs_tol = 1.0e-10;
+    t->rel_tol = 1.0e-6;
+    t->uround = 2.22e-16;
+    t->tiny = 1.0e-30;
+    t->safety = 0.9;
+    t->p1 = 0.1;
+    t->errcon = 1.89e-4;
+    t->pgrow = -0.2;
+    t->pshrnk = -0.25;
+    t->h_min_floor = 1.0e-20;
+    t->kappa = 2.0 / 13.0;
+}
+
+int bode_tol_validate(const bode_tol_t* t) {  // ode_problem.hpp:46-53
+    if (t == nullptr) return fail(BODE_E_INVALID_SHAPE, "tolerance settings are NULL");
+    if (!(t->eps > 0.0 && t->abs_tol > 0.0 && t->rel_tol > 0.0))
+        return fail(BODE_E_INVALID_SHAPE, "ToleranceSettings: eps/absTol/relTol must be positive");
+    if (!(t->safety > 0.0 && t->safety < 1.0) || !(t->p1 > 0.0 && t->p1 < 1.0))
+        return fail(BODE_E_INVALID_SHAPE, "ToleranceSettings: safety and p1 must lie in (0, 1)");
+    if (!(t->uround > 0.0 && t->tiny > 0.0 && t->h_min_floor > 0.0 && t->kappa >= 0.0))
+        return fail(BODE_E_INVALID_SHAPE, "ToleranceSettings: bad auxiliary constants");
+    return BODE_OK;
+}
+
+int bode_problem_init(bode_problem_t* p, int32_t kind, int32_t dim) {
+    if (p == nullptr) return fail(BODE_E_INVALID_SHAPE, "problem is NULL");
+    p->kind = kind;
+    p->reserved = 0;
+    switch (kind) {
+        case BODE_PROBLEM_PLEIADES: p->dim = 28; p->param_dim = 0; break;
+        case BODE_PROBLEM_HEAT:
+            if (dim < 2) return fail(BODE_E_INVALID_SHAPE, "heatEquation: need at least two interior points");
+            p->dim = dim; p->param_dim = 0; break;
+        case BODE_PROBLEM_EXPDECAY: p->dim = 1; p->param_dim = 1; break;
+        case BODE_PROBLEM_HARMONIC: p->dim = 2; p->param_dim = 0; break;
+        case BODE_PROBLEM_RICCATI:
+        case BODE_PROBLEM_SINT: p->dim = 1; p->param_dim = 0; break;
+        case BODE_PROBLEM_DIAG:
+            if (dim < 1) return fail(BODE_E_INVALID_SHAPE, "dim must be positive");
+            p->dim = dim; p->param_dim = dim; break;
+        case BODE_PROBLEM_ZERO:
+        case BODE_PROBLEM_CONST:
+            if (dim < 1) return fail(BODE_E_INVALID_SHAPE, "dim must be positive");
+            p->dim = dim; p->param_dim = 0; break;
+        default: return fail(BODE_E_INVALID_SHAPE, "unknown problem kind");
+    }
+    return BODE_OK;
+}
+
+int bode_problem_supported(const bode_problem_t* p, int32_t solver, int32_t arith) {
+    return (p && find_entry(p, solver, arith)) ? 1 : 0;
+}
+
+int64_t bode_num_windows(double t0, double t_end, double h_outer) {
+    const double ratio = (t_end - t0) / h_outer;  // batch_driver.cpp:99-100
+    const long n = static_cast<long>(std::ceil(ratio - 1e-9));
+    return std::max(1L, n);
+}
+
+double bode_window_end(double t0, double t_end, double h_outer, int64_t k) {
+    const int64_t n = bode_num_windows(t0, t_end, h_outer);  // batch_driver.cpp:105
+    return (k == n) ? t_end : t0 + static_cast<double>(k) * h_outer;
+}
+
+int bode_set_block_size(int32_t threads) {
+    if (threads != 0 && (threads < 32 || threads > bode::kMaxBlock || threads % 32 != 0))
+        return fail(BODE_E_INVALID_SHAPE, "block size must be 0 or a multiple of 32 in [32, 256]");
+    g_block_override.store(threads);
+    return BODE_OK;
+}
+
+int64_t bode_launch_count(void) { return g_launches.load(); }
+
+int bode_int_driver_device(const bode_problem_t* p, int32_t solver, int32_t arith, double t,
+                           double t_end, int64_t num, const double* g_dev, double* y_dev,
+                           const bode_tol_t* tol, bode_stats_t* stats_dev, int32_t merge_stats,
+                           void* stream) {
+    const KernelEntry* e = nullptr;
+    int rc = validate_call(p, solver, arith, t, t_end, num, g_dev, y_dev, tol, &e);
+    if (rc) return rc;
+    if ((rc = check_devices(1))) return rc;
+    return launch_window(e, (cudaStream_t)stream, g_dev, y_dev, (DevStats*)stats_dev, num, t,
+                         t_end, to_dev(tol), merge_stats ? 1 : 0);
+}
+
+int bode_int_driver(const bode_problem_t* p, int32_t solver, int32_t arith, double t,
+                    double t_end, int64_t num, const double* g, double* y, const bode_tol_t* tol,
+                    bode_stats_t* stats, int32_t num_gpus) {
+    const KernelEntry* e = nullptr;
+    int rc = validate_call(p, solver, arith, t, t_end, num, g, y, tol, &e);
+    if (rc) return rc;
+    if ((rc = check_devices(num_gpus))) return rc;
+    const DevTol dt = to_dev(tol);
+    const auto shards = make_shards(num, num_gpus);
+    return for_each_shard(shards, [&](const Shard& sh) {
+        return run_shard_window(e, p, sh, num, g, y, stats, t, t_end, dt);
+    });
+}
+
+int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, double t0,
+                    double t_end, double h_outer, int64_t num, const double* g, double* y,
+                    const bode_tol_t* tol, bode_stats_t* stats, int32_t num_gpus,
+                    bode_sink_fn sink, void* user, int32_t* outer_steps) {
+    if (!(t_end > t0)) return fail(BODE_E_INVALID_INTERVAL, "outerLoop: tEnd must exceed t0");
+    if (!(h_outer > 0.0)) return fail(BODE_E_INVALID_INTERVAL, "outerLoop: hOuter must be positive");
+    const KernelEntry* e = nullptr;
+    int rc = validate_call(p, solver, arith, t0, t_end, num, g, y, tol, &e);
+    if (rc) return rc;
+    if ((rc = check_devices(num_gpus))) return rc;
+    const DevTol dt = to_dev(tol);
+    const auto shards = make_shards(num, num_gpus);
+    const int N = p->dim, P = p->param_dim;
+    const int64_t nwin = bode_num_windows(t0, t_end, h_outer);
+
+    // upload each shard once; y stays resident across windows
+    rc = for_each_shard(shards, [&](const Shard& sh) {
+        BODE_CUDA(cudaSetDevice(sh.device));
+        DeviceBuffers& B = g_dev[sh.device];
+        std::lock_guard<std::mutex> lock(B.m);
+        int r = ensure(&B.y, &B.y_cap, (size_t)sh.count * N);
+        if (r) return r;
+        if (P > 0 && (r = ensure(&B.g, &B.g_cap, (size_t)sh.count * P))) return r;
+        if ((r = ensure(&B.st, &B.st_cap, (size_t)sh.count))) return r;
+        if (!B.streams[0]) BODE_CUDA(cudaStreamCreateWithFlags(&B.streams[0], cudaStreamNonBlocking));
+        cudaStream_t s = B.streams[0];
+        BODE_CUDA(cudaMemcpy2DAsync(B.y, sh.count * sizeof(double), y + sh.begin,
+                                    num * sizeof(double), sh.count * sizeof(double), N,
+                                    cudaMemcpyHostToDevice, s));
+        if (P > 0)
+            BODE_CUDA(cudaMemcpy2DAsync(B.g, sh.count * sizeof(double), g + sh.begin,
+                                        num * sizeof(double), sh.count * sizeof(double), P,
+                                        cudaMemcpyHostToDevice, s));
+        BODE_CUDA(cudaStreamSynchronize(s));
+        return BODE_OK;
+    });
+    if (rc) return rc;
+
+    double t = t0;
+    for (int64_t k = 1; k <= nwin; ++k) {
+        const double tk = (k == nwin) ? t_end : t0 + static_cast<double>(k) * h_outer;
+        const bool snap = sink != nullptr || k == nwin;
+        rc = for_each_shard(shards, [&](const Shard& sh) {
+            BODE_CUDA(cudaSetDevice(sh.device));
+            DeviceBuffers& B = g_dev[sh.device];
+            std::lock_guard<std::mutex> lock(B.m);
+            cudaStream_t s = B.streams[0];
+            int r = launch_window(e, s, P > 0 ? B.g : nullptr, B.y, B.st, sh.count, t, tk, dt,
+                                  k > 1 ? 1 : 0);
+            if (r) return r;
+            if (snap)
+                BODE_CUDA(cudaMemcpy2DAsync(y + sh.begin, num * sizeof(double), B.y,
+                                            sh.count * sizeof(double), sh.count * sizeof(double),
+                                            N, cudaMemcpyDeviceToHost, s));
+            if (k == nwin && stats)
+                BODE_CUDA(cudaMemcpyAsync(stats + sh.begin, B.st, sh.count * sizeof(DevStats),
+                                          cudaMemcpyDeviceToHost, s));
+            BODE_CUDA(cudaStreamSynchronize(s));
+            return BODE_OK;
+        });
+        if (rc) return rc;
+        if (sink) sink(tk, y, num, N, user);
+        t = tk;
+    }
+    if (outer_steps) *outer_steps = (int32_t)nwin;
+    return BODE_OK;
+}
+
+// ---- synthetic inputs (problems.cpp:158-191) ----
+uint64_t bode_splitmix64_at(uint64_t seed, uint64_t k) {
+    uint64_t z = seed + (k + 1) * 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+double bode_unit_symmetric_at(uint64_t seed, uint64_t k) {
+    const double u01 = static_cast<double>(bode_splitmix64_at(seed, k) >> 11) * 0x1.0p-53;
+    return 2.0 * u01 - 1.0;
+}
+
+int bode_perturb_initial_conditions(const double* base, int32_t dim, double magnitude,
+                                    uint64_t seed, int64_t count, double* out) {
+    if (count < 1) return fail(BODE_E_INVALID_SHAPE, "perturbInitialConditions: count must be positive");
+    if (dim < 1 || base == nullptr) return fail(BODE_E_INVALID_SHAPE, "perturbInitialConditions: empty base state");
+    if (!(magnitude >= 0.0 && magnitude <= 0.1))
+        return fail(BODE_E_INVALID_SHAPE, "perturbInitialConditions: magnitude outside [0, 0.1]");
+    const unsigned hw = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+    const int64_t workers = std::min<int64_t>(hw, std::max<int64_t>(1, count / 65536));
+    auto body = [&](int64_t lo, int64_t hi) {
+        for (int64_t i = lo; i < hi; ++i)
+            for (int j = 0; j < dim; ++j) {
+                const uint64_t k = static_cast<uint64_t>(i) * static_cast<uint64_t>(dim) + j;
+                const double u = bode_unit_symmetric_at(seed, k);
+                out[i + count * j] = base[j] * (1.0 + u * magnitude);
+            }
+    };
+    if (workers <= 1) {
+        body(0, count);
+    } else {
+        std::vector<std::thread> pool;
+        for (int64_t w = 0; w < workers; ++w)
+            pool.emplace_back(body, count * w / workers, count * (w + 1) / workers);
+        for (auto& th : pool) th.join();
+    }
+    return BODE_OK;
+}
+
+void bode_pleiades_ic(double out[28]) { std::memcpy(out, kPleiadesIC, sizeof(kPleiadesIC)); }
+
+void bode_heat_initial_condition(int32_t n, double* u) {  // problems.cpp:124-132
+    const double dx = 1.0 / (n + 1);
+    for (int i = 0; i < n; ++i) {
+        const double x = (i + 1) * dx;
+        u[i] = 4.0 * x * (1.0 - x);
+    }
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// kernels.cu -- the intDriver kernels for sm_100a and
+// their dispatch table.
+//
+// One lane group (L lanes) integrates one system over one window [t, tEnd]:
+// coalesced SoA load of y[i + num*j] (batch.hpp:15-29), the
+// fused solver (rkck.cuh / rkc.cuh), SoA store, per-system stats (AoS).
+// All arithmetic is FP64 on the CUDA cores; nothing here is a contraction,
+// so there are no tensor cores on this path.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "dispatch.h"
+#include "rkc.cuh"
+
+namespace bode {
+
+template <class P, class R, int L, int SOLVER, bool KSMEM>
+__global__ void __launch_bounds__(kMaxBlock)
+    integrate_kernel(const double* __restrict__ g_soa, double* __restrict__ y_soa,
+                     DevStats* __restrict__ stats, long long num, double t, double tEnd,
+                     DevTol tol, int merge) {
+    constexpr int C = P::N / L;
+    constexpr int PP = P::P > 0 ? P::P : 1;
+    const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long sys = gt / L;
+    if (sys >= num) return;  // whole lane groups retire together
+    Group<L> G;
+    R y[C];
+    R g[PP];
+#pragma unroll
+    for (int c = 0; c < C; ++c) y[c] = R(y_soa[sys + num * (long long)(G.lane * C + c)]);
+#pragma unroll
+    for (int p = 0; p < PP; ++p) g[p] = R(P::P > 0 ? g_soa[sys + num * (long long)p] : 0.0);
+    DevStats st;
+    if constexpr (SOLVER == 0)
+        rkck_system<P, R, L, KSMEM>(G, t, tEnd, y, g, tol, st);
+    else
+        rkc_system<P, R, L>(G, t, tEnd, y, g, tol, st);
+#pragma unroll
+    for (int c = 0; c < C; ++c) y_soa[sys + num * (long long)(G.lane * C + c)] = val(y[c]);
+    if (stats != nullptr && G.lane == 0) {
+        if (merge) {
+            DevStats o = stats[sys];
+            stats_merge(o, st);
+            stats[sys] = o;
+        } else {
+            stats[sys] = st;
+        }
+    }
+}
+
+// ---- dispatch table ----
+template <class P, class R, int L, int SOLVER, bool KSMEM>
+static KernelEntry make_entry(int kind, int arith) {
+    KernelEntry e;
+    e.kind = kind;
+    e.dim = P::N;
+    e.param_dim = P::P;
+    e.solver = SOLVER;
+    e.arith = arith;
+    e.lanes = L;
+    e.smem_per_thread = KSMEM ? 4 * C_of<P, L>() * (int)sizeof(double) : 0;
+    e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM>;
+    e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                  const double* g, double* y, DevStats* st, long long num, double t,
+                  double tEnd, DevTol tol, int merge) {
+        auto k = (void (*)(const double*, double*, DevStats*, long long, double, double, DevTol,
+                           int))fn;
+        k<<<grid, block, smem, s>>>(g, y, st, num, t, tEnd, tol, merge);
+    };
+    e.default_block = KSMEM ? 128 : 128;
+    return e;
+}
+
+#define BODE_BOTH_ARITH(P, L, SOLVER, KSMEM, KIND)                           \
+    make_entry<P, xd, L, SOLVER, KSMEM>(KIND, 0),                            \
+        make_entry<P, double, L, SOLVER, KSMEM>(KIND, 1)
+
+const KernelEntry* kernel_table(int* count) {
+    static const KernelEntry table[] = {
+        // RKCK (nonstiff): Pleiades stages in shared memory, small systems in registers
+        BODE_BOTH_ARITH(Pleiades, 1, 0, true, 0),
+        BODE_BOTH_ARITH(ExpDecay, 1, 0, false, 2),
+        BODE_BOTH_ARITH(Harmonic, 1, 0, false, 3),
+        BODE_BOTH_ARITH(Zero<2>, 1, 0, false, 4),
+        BODE_BOTH_ARITH(Riccati, 1, 0, false, 5),
+        BODE_BOTH_ARITH(Diag<3>, 1, 0, false, 6),
+        BODE_BOTH_ARITH(Const<1>, 1, 0, false, 7),
+        BODE_BOTH_ARITH(SinT, 1, 0, false, 8),
+        BODE_BOTH_ARITH(Heat<8>, 1, 0, false, 1),
+        // RKC (moderately stiff)
+        BODE_BOTH_ARITH(Heat<64>, 4, 1, false, 1),
+        BODE_BOTH_ARITH(Heat<32>, 4, 1, false, 1),
+        BODE_BOTH_ARITH(Heat<16>, 2, 1, false, 1),
+        BODE_BOTH_ARITH(Heat<8>, 1, 1, false, 1),
+        BODE_BOTH_ARITH(ExpDecay, 1, 1, false, 2),
+        BODE_BOTH_ARITH(Harmonic, 1, 1, false, 3),
+        BODE_BOTH_ARITH(Zero<2>, 1, 1, false, 4),
+        BODE_BOTH_ARITH(Diag<3>, 1, 1, false, 6),
+        BODE_BOTH_ARITH(Const<1>, 1, 1, false, 7),
+    };
+    *count = (int)(sizeof(table) / sizeof(table[0]));
+    return table;
+}
+
+}  // namespace bode

@@ -1,0 +1,241 @@
+// problems.cuh -- fused device right-hand sides (the paper's user dydt,
+// PAPER.md:370, :416), one per reference problem (proj/src/problems.cpp).
+//
+// A system is owned by a group of L consecutive lanes; lane l holds the C =
+// N/L components [l*C, (l+1)*C) of every state-length vector in registers.
+// rhs() computes the lane's slice of dy/dt; problems whose RHS couples
+// components across lanes (the heat stencil) exchange halos with warp
+// shuffles. Expression shapes and accumulation orders follow the reference
+// exactly, so with R = xd the result is bitwise the reference's.
+#pragma once
+
+#include "arith.cuh"
+
+namespace bode {
+
+// Lane group of L lanes (L divides 32) inside a warp.
+template <int L>
+struct Group {
+    int lane;       // 0..L-1
+    unsigned mask;  // the group's lanes in the warp
+    __device__ __forceinline__ Group() {
+        const int wl = threadIdx.x & 31;
+        lane = wl & (L - 1);
+        mask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (wl & ~(L - 1)));
+    }
+    // value held by group lane `src`
+    __device__ __forceinline__ double from(double v, int src) const {
+        return __shfl_sync(mask, v, src, L);
+    }
+    __device__ __forceinline__ double from_prev(double v) const {  // lane-1
+        return __shfl_up_sync(mask, v, 1, L);
+    }
+    __device__ __forceinline__ double from_next(double v) const {  // lane+1
+        return __shfl_down_sync(mask, v, 1, L);
+    }
+    __device__ __forceinline__ double max_all(double v) const {  // fmax over lanes
+#pragma unroll
+        for (int o = L / 2; o > 0; o /= 2) v = fmax(v, __shfl_xor_sync(mask, v, o, L));
+        return v;
+    }
+    __device__ __forceinline__ bool any(bool b) const {
+        return (__ballot_sync(mask, b) & mask) != 0u;
+    }
+};
+
+template <>
+struct Group<1> {
+    int lane = 0;
+    unsigned mask = 0u;
+    __device__ __forceinline__ Group() {}
+    __device__ __forceinline__ double from(double v, int) const { return v; }
+    __device__ __forceinline__ double from_prev(double v) const { return v; }
+    __device__ __forceinline__ double from_next(double v) const { return v; }
+    __device__ __forceinline__ double max_all(double v) const { return v; }
+    __device__ __forceinline__ bool any(bool b) const { return b; }
+};
+
+template <class R, int L>
+__device__ __forceinline__ R grp_from(const Group<L>& G, R v, int src) {
+    return R(G.from(val(v), src));
+}
+
+// Sequential sum in global component order: lane 0 sums its C terms, hands
+// the partial to lane 1, ... exactly the reference's `sum += term` loop
+// (rkc.cpp:122-127, spectral_radius.cpp:11-13). Result valid on every lane.
+template <class R, int L, int C>
+__device__ __forceinline__ R seq_sum(const Group<L>& G, const R (&terms)[C], R init) {
+    if constexpr (L == 1) {
+        R s = init;
+#pragma unroll
+        for (int c = 0; c < C; ++c) s = s + terms[c];
+        return s;
+    } else {
+        R s = init;
+#pragma unroll 1
+        for (int k = 0; k < L; ++k) {
+            if (G.lane == k) {
+#pragma unroll
+                for (int c = 0; c < C; ++c) s = s + terms[c];
+            }
+            s = R(G.from(val(s), k));
+        }
+        return s;
+    }
+}
+
+// -------------------------------------------------------------------------
+// Pleiades (problems.cpp:9-37): N = 28, masses m_i = i + 1, pairs i<j with
+// i outer, j inner; action/reaction share one distance evaluation.
+struct Pleiades {
+    static constexpr int N = 28, P = 0;
+    static constexpr const char* name = "pleiades";
+    template <class R, int L>
+    __device__ __forceinline__ static void rhs(const Group<L>&, R, const R (&w)[N],
+                                               const R*, R (&out)[N]) {
+        static_assert(L == 1, "Pleiades couples all components: one lane per system");
+#pragma unroll
+        for (int i = 0; i < 14; ++i) out[i] = w[14 + i];
+#pragma unroll
+        for (int i = 14; i < 28; ++i) out[i] = R(0.0);
+#pragma unroll
+        for (int i = 0; i < 7; ++i) {
+#pragma unroll
+            for (int j = i + 1; j < 7; ++j) {
+                const R dx = w[j] - w[i];
+                const R dy = w[7 + j] - w[7 + i];
+                const R r2 = dx * dx + dy * dy;
+                const double mi = double(i + 1);
+                const double mj = double(j + 1);
+                if constexpr (is_exact<R>::value) {
+                    const R invR3 = R(1.0) / (r2 * sqrt_(r2));
+                    out[14 + i] += R(mj) * dx * invR3;
+                    out[21 + i] += R(mj) * dy * invR3;
+                    out[14 + j] -= R(mi) * dx * invR3;
+                    out[21 + j] -= R(mi) * dy * invR3;
+                } else {
+                    const double rs = rsqrt(val(r2));
+                    const double invR3 = rs * rs * rs;
+                    const double ax = val(dx) * invR3;
+                    const double ay = val(dy) * invR3;
+                    out[14 + i] += mj * ax;
+                    out[21 + i] += mj * ay;
+                    out[14 + j] -= mi * ax;
+                    out[21 + j] -= mi * ay;
+                }
+            }
+        }
+    }
+};
+
+// Heat equation, method of lines (problems.cpp:94-115): N = n interior
+// points, (u[i-1] - 2 u[i] + u[i+1]) / dx^2 with zero Dirichlet boundaries.
+template <int NN>
+struct Heat {
+    static constexpr int N = NN, P = 0;
+    static constexpr const char* name = "heat";
+    template <class R, int L>
+    __device__ __forceinline__ static void rhs(const Group<L>& G, R, const R (&u)[N / L],
+                                               const R*, R (&out)[N / L]) {
+        constexpr int C = N / L;
+        const double dx = 1.0 / (NN + 1);
+        const double inv = 1.0 / (dx * dx);
+        // halo values from the neighbouring lanes (unused at the boundaries)
+        const R left = R(G.from_prev(val(u[C - 1])));
+        const R right = R(G.from_next(val(u[0])));
+        const bool first = G.lane == 0, last = G.lane == L - 1;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const R um = (c > 0) ? u[c - 1] : left;
+            const R up = (c < C - 1) ? u[c + 1] : right;
+            if (c == 0 && first)
+                out[c] = (R(-2.0) * u[c] + up) * R(inv);
+            else if (c == C - 1 && last)
+                out[c] = (um - R(2.0) * u[c]) * R(inv);
+            else
+                out[c] = (um - R(2.0) * u[c] + up) * R(inv);
+        }
+    }
+};
+
+// dy/dt = -g0 y (problems.cpp:134-144)
+struct ExpDecay {
+    static constexpr int N = 1, P = 1;
+    static constexpr const char* name = "expdecay";
+    template <class R, int L>
+    __device__ __forceinline__ static void rhs(const Group<L>&, R, const R (&y)[1],
+                                               const R* g, R (&out)[1]) {
+        out[0] = -g[0] * y[0];
+    }
+};
+
+// (q, p)' = (p, -q) (problems.cpp:146-156)
+struct Harmonic {
+    static constexpr int N = 2, P = 0;
+    static constexpr const char* name = "harmonic";
+    template <class R, int L>
+    __device__ __forceinline__ static void rhs(const Group<L>&, R, const R (&y)[2],
+                                               const R*, R (&out)[2]) {
+        out[0] = y[1];
+        out[1] = -y[0];
+    }
+};
+
+// Calibration problems of the reference test suites.
+template <int NN>
+struct Zero {  // test_batch.cpp:248-256
+    static constexpr int N = NN, P = 0;
+    static constexpr const char* name = "zero";
+    template <class R, int L>
+    __device__ __forceinline__ static void rhs(const Group<L>&, R, const R (&)[N / L],
+                                               const R*, R (&out)[N / L]) {
+#pragma unroll
+        for (int c = 0; c < N / L; ++c) out[c] = R(0.0);
+    }
+};
+
+struct Riccati {  // y' = y^2 (test_rkck.cpp:28)
+    static constexpr int N = 1, P = 0;
+    static constexpr const char* name = "riccati";
+    template <class R, int L>
+    __device__ __forceinline__ static void rhs(const Group<L>&, R, const R (&y)[1],
+                                               const R*, R (&out)[1]) {
+        out[0] = y[0] * y[0];
+    }
+};
+
+template <int NN>
+struct Diag {  // y_i' = g_i y_i (test_specrad.cpp:16-24)
+    static constexpr int N = NN, P = NN;
+    static constexpr const char* name = "diag";
+    template <class R, int L>
+    __device__ __forceinline__ static void rhs(const Group<L>& G, R, const R (&y)[N / L],
+                                               const R* g, R (&out)[N / L]) {
+#pragma unroll
+        for (int c = 0; c < N / L; ++c) out[c] = g[G.lane * (N / L) + c] * y[c];
+    }
+};
+
+template <int NN>
+struct Const {  // y' = 1 (test_rkck.cpp:26)
+    static constexpr int N = NN, P = 0;
+    static constexpr const char* name = "const";
+    template <class R, int L>
+    __device__ __forceinline__ static void rhs(const Group<L>&, R, const R (&)[N / L],
+                                               const R*, R (&out)[N / L]) {
+#pragma unroll
+        for (int c = 0; c < N / L; ++c) out[c] = R(1.0);
+    }
+};
+
+struct SinT {  // y' = sin(t) y (test_rkck.cpp:220-230)
+    static constexpr int N = 1, P = 0;
+    static constexpr const char* name = "sint";
+    template <class R, int L>
+    __device__ __forceinline__ static void rhs(const Group<L>&, R t, const R (&y)[1],
+                                               const R*, R (&out)[1]) {
+        out[0] = sin_(t) * y[0];
+    }
+};
+
+}  // namespace bode

@@ -1,0 +1,210 @@
+// rkck.cuh -- adaptive Runge-Kutta-Cash-Karp integration of one system per
+// lane group, entirely on chip.
+//
+// Follows proj/src/rkck.cpp: tableau (:8-27), step (:34-78), errorNorm
+// (:88-98), adjustStep (:100-113) and driver (:115-159). The step, its
+// embedded error estimate, the scaled max-norm and the controller are fused:
+// yErr is never materialised, it is folded into the norm component by
+// component, and yNext is formed in place only once the step is accepted.
+//
+// Storage: y and f0 live in registers. The stage derivatives k2..k5 live in
+// registers for small systems or in shared memory for large ones (KSMEM),
+// laid out [stage][component][thread] so a warp touches 32 consecutive
+// doubles (conflict-free). k6 stays in the RHS output registers.
+#pragma once
+
+#include "dispatch.h"
+#include "problems.cuh"
+
+namespace bode {
+
+__device__ __forceinline__ void stats_init(DevStats& s) {
+    s.steps_accepted = s.steps_rejected = s.rhs_evals = s.spec_rad_evals = s.stages_total = 0;
+    s.h_min_seen = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+    s.h_max_seen = 0.0;
+    s.underflow = 0;
+    s.reserved = 0;
+}
+
+// IntegrationStats::recordAcceptedStep (ode_problem.hpp:66-70)
+__device__ __forceinline__ void stats_accept(DevStats& s, double h) {
+    ++s.steps_accepted;
+    s.h_min_seen = fmin(s.h_min_seen, h);
+    s.h_max_seen = fmax(s.h_max_seen, h);
+}
+
+// IntegrationStats::merge (ode_problem.hpp:72-80)
+__device__ __forceinline__ void stats_merge(DevStats& a, const DevStats& b) {
+    a.steps_accepted += b.steps_accepted;
+    a.steps_rejected += b.steps_rejected;
+    a.rhs_evals += b.rhs_evals;
+    a.spec_rad_evals += b.spec_rad_evals;
+    a.stages_total += b.stages_total;
+    a.h_min_seen = fmin(a.h_min_seen, b.h_min_seen);
+    a.h_max_seen = fmax(a.h_max_seen, b.h_max_seen);
+    a.underflow = a.underflow || b.underflow;
+}
+
+// Cash-Karp tableau (rkck.cpp:8-27), evaluated as the same double quotients.
+namespace ck {
+constexpr double a2 = 1.0 / 5.0, a3 = 3.0 / 10.0, a4 = 3.0 / 5.0, a5 = 1.0, a6 = 7.0 / 8.0;
+constexpr double b21 = 1.0 / 5.0;
+constexpr double b31 = 3.0 / 40.0, b32 = 9.0 / 40.0;
+constexpr double b41 = 3.0 / 10.0, b42 = -9.0 / 10.0, b43 = 6.0 / 5.0;
+constexpr double b51 = -11.0 / 54.0, b52 = 5.0 / 2.0, b53 = -70.0 / 27.0, b54 = 35.0 / 27.0;
+constexpr double b61 = 1631.0 / 55296.0, b62 = 175.0 / 512.0, b63 = 575.0 / 13824.0,
+                 b64 = 44275.0 / 110592.0, b65 = 253.0 / 4096.0;
+constexpr double c1 = 37.0 / 378.0, c3 = 250.0 / 621.0, c4 = 125.0 / 594.0, c5 = 0.0,
+                 c6 = 512.0 / 1771.0;
+constexpr double s1 = 2825.0 / 27648.0, s3 = 18575.0 / 48384.0, s4 = 13525.0 / 55296.0,
+                 s5 = 277.0 / 14336.0, s6 = 1.0 / 4.0;
+// d = c - c* (rkck.cpp:68-72); both operands are exact double constants and
+// the subtraction is a single IEEE rounding, folded at compile time.
+constexpr double d1 = c1 - s1, d3 = c3 - s3, d4 = c4 - s4, d5 = c5 - s5, d6 = c6 - s6;
+}  // namespace ck
+
+// Stage-derivative store for k2..k5 (slot 0..3).
+template <class R, int C, bool SMEM>
+struct KStore;
+
+template <class R, int C>
+struct KStore<R, C, false> {
+    R k[4][C];
+    __device__ __forceinline__ R get(int m, int c) const { return k[m][c]; }
+    __device__ __forceinline__ void set(int m, int c, R v) { k[m][c] = v; }
+};
+
+template <class R, int C>
+struct KStore<R, C, true> {
+    double* base;  // dynamic shared memory, [slot][c][blockDim.x]
+    int stride;
+    __device__ __forceinline__ KStore() {
+        extern __shared__ double bode_smem[];
+        base = bode_smem + threadIdx.x;
+        stride = blockDim.x;
+    }
+    __device__ __forceinline__ R get(int m, int c) const { return R(base[(m * C + c) * stride]); }
+    __device__ __forceinline__ void set(int m, int c, R v) { base[(m * C + c) * stride] = val(v); }
+};
+
+// adjustStep (rkck.cpp:100-113)
+template <class R>
+__device__ __forceinline__ bool rkck_adjust(R h, R err, bool nanFlag, R hMin, R hMax,
+                                            const DevTol& tol, R& hNew) {
+    if (err > R(1.0) || !isfinite_(err) || nanFlag) {
+        hNew = (!isfinite_(err) || nanFlag)
+                   ? R(tol.p1) * h
+                   : fmax_(R(tol.safety) * h * pow_(err, R(tol.pshrnk)), R(tol.p1) * h);
+        return false;
+    }
+    R hn = (err > R(tol.errcon)) ? R(tol.safety) * h * pow_(err, R(tol.pgrow)) : R(5.0) * h;
+    hNew = fmax_(hMin, fmin_(hMax, hn));
+    return true;
+}
+
+// One system (this lane's slice) from t to tEnd: rkck::driver (rkck.cpp:115-159).
+// y is updated in place; returns the window's stats.
+template <class P, class R, int L, bool KSMEM>
+__device__ __forceinline__ void rkck_system(const Group<L>& G, double t_in, double tEnd_in,
+                                            R (&y)[P::N / L], const R* g, const DevTol& tol,
+                                            DevStats& st) {
+    constexpr int C = P::N / L;
+    using namespace ck;
+    stats_init(st);
+    const R tEnd(tEnd_in);
+    R t(t_in);
+    const R hMax = fabs_(tEnd - t);
+    const R hMin(tol.h_min_floor);
+    R h = R(0.5) * fabs_(tEnd - t);
+    const R uround(tol.uround), eps(tol.eps), tiny(tol.tiny);
+
+    R f0[C];
+    KStore<R, C, KSMEM> K;
+    bool haveF = false;
+
+#pragma unroll 1
+    while (tEnd - t > uround * fabs_(tEnd)) {
+        h = fmin_(tEnd - t, h);
+        R arg[C], out[C];
+        if (!haveF) {  // rejected retries reuse f(t, y) (rkck.cpp:133-137)
+            P::template rhs<R, L>(G, t, y, g, f0);
+            ++st.rhs_evals;
+            haveF = true;
+        }
+        // ---- rkck::step (rkck.cpp:42-64): five stage evaluations ----
+        // stage 2: y + h*b21*f0
+#pragma unroll
+        for (int c = 0; c < C; ++c) arg[c] = y[c] + h * R(b21) * f0[c];
+        P::template rhs<R, L>(G, t + R(a2) * h, arg, g, out);
+#pragma unroll
+        for (int c = 0; c < C; ++c) K.set(0, c, out[c]);
+        // stage 3
+#pragma unroll
+        for (int c = 0; c < C; ++c) arg[c] = y[c] + h * (R(b31) * f0[c] + R(b32) * K.get(0, c));
+        P::template rhs<R, L>(G, t + R(a3) * h, arg, g, out);
+#pragma unroll
+        for (int c = 0; c < C; ++c) K.set(1, c, out[c]);
+        // stage 4
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            arg[c] = y[c] + h * (R(b41) * f0[c] + R(b42) * K.get(0, c) + R(b43) * K.get(1, c));
+        P::template rhs<R, L>(G, t + R(a4) * h, arg, g, out);
+#pragma unroll
+        for (int c = 0; c < C; ++c) K.set(2, c, out[c]);
+        // stage 5
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            arg[c] = y[c] + h * (R(b51) * f0[c] + R(b52) * K.get(0, c) + R(b53) * K.get(1, c) +
+                                 R(b54) * K.get(2, c));
+        P::template rhs<R, L>(G, t + R(a5) * h, arg, g, out);
+#pragma unroll
+        for (int c = 0; c < C; ++c) K.set(3, c, out[c]);
+        // stage 6
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            arg[c] = y[c] + h * (R(b61) * f0[c] + R(b62) * K.get(0, c) + R(b63) * K.get(1, c) +
+                                 R(b64) * K.get(2, c) + R(b65) * K.get(3, c));
+        P::template rhs<R, L>(G, t + R(a6) * h, arg, g, out);  // out = k6
+        st.rhs_evals += 5;
+        st.stages_total += 6;
+
+        // ---- yErr folded into errorNorm (rkck.cpp:75-76, :88-98) ----
+        R err(0.0);
+        bool nanFlag = false;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const R yErr = h * (R(d1) * f0[c] + R(d3) * K.get(1, c) + R(d4) * K.get(2, c) +
+                                R(d5) * K.get(3, c) + R(d6) * out[c]);
+            if (!isfinite_(yErr)) nanFlag = true;
+            err = fmax_(err, fabs_(yErr / (fabs_(y[c]) + fabs_(h * f0[c]) + tiny)));
+        }
+        if constexpr (L > 1) {
+            err = R(G.max_all(val(err)));
+            nanFlag = G.any(nanFlag);
+        }
+        err = err / eps;
+
+        R hNew;
+        const bool accepted = rkck_adjust(h, err, nanFlag, hMin, hMax, tol, hNew);
+        if (accepted) {
+            t += h;
+            stats_accept(st, val(h));
+            // yNext (rkck.cpp:74), written over y once the step is accepted
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+                y[c] = y[c] + h * (R(c1) * f0[c] + R(c3) * K.get(1, c) + R(c4) * K.get(2, c) +
+                                   R(c6) * out[c]);
+            haveF = false;
+            h = hNew;
+        } else {
+            ++st.steps_rejected;
+            if (hNew < R(tol.h_min_floor)) {  // freeze at the last accepted state
+                st.underflow = 1;
+                break;
+            }
+            h = hNew;
+        }
+    }
+}
+
+}  // namespace bode

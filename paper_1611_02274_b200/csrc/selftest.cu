@@ -1,0 +1,95 @@
+// selftest.cu -- diagnostics exported through the C ABI (bode_selftest_*).
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/bode.h"
+#include "arith.cuh"
+
+namespace {
+
+__global__ void cbrt_kernel(const double* __restrict__ x, double* __restrict__ out, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = bode::glibc_cbrt(x[i]);
+}
+
+}  // namespace
+
+extern "C" int bode_selftest_cbrt(const double* x, double* out, int64_t n) {
+    if (n < 1 || x == nullptr || out == nullptr) return BODE_E_INVALID_SHAPE;
+    int dev = 0;
+    if (cudaGetDeviceCount(&dev) != cudaSuccess || dev < 1) {
+        cudaGetLastError();
+        return BODE_E_NO_DEVICE;
+    }
+    double *dx = nullptr, *dy = nullptr;
+    if (cudaMalloc(&dx, n * sizeof(double)) != cudaSuccess) return BODE_E_CUDA;
+    if (cudaMalloc(&dy, n * sizeof(double)) != cudaSuccess) {
+        cudaFree(dx);
+        return BODE_E_CUDA;
+    }
+    cudaMemcpy(dx, x, n * sizeof(double), cudaMemcpyHostToDevice);
+    cbrt_kernel<<<(unsigned)((n + 255) / 256), 256>>>(dx, dy, n);
+    cudaError_t e = cudaMemcpy(out, dy, n * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(dx);
+    cudaFree(dy);
+    return e == cudaSuccess ? BODE_OK : BODE_E_CUDA;
+}
+
+namespace {
+
+// 8 independent DFMA chains per thread keep the FP64 pipe saturated
+// regardless of its latency; values stay bounded (x <- x*a + b, |a| < 1).
+__global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters, double a, double b) {
+    double x0 = threadIdx.x * 1e-3, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+    double x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+#pragma unroll 1
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+            x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+        }
+    }
+    const double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+    if (s == 12345.678) out[blockIdx.x] = s;  // keep the chains live
+}
+
+}  // namespace
+
+// Measured FP64 FMA throughput of the current device: flop/s (2 per DFMA).
+extern "C" int bode_selftest_fp64_peak(double* flops_per_s, double* seconds) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        return BODE_E_NO_DEVICE;
+    }
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double* out = nullptr;
+    if (cudaMalloc(&out, 65536 * sizeof(double)) != cudaSuccess) return BODE_E_CUDA;
+    const int blocks = sms * 8, threads = 256, iters = 2048;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    dfma_peak_kernel<<<blocks, threads>>>(out, 64, 0.999, 1e-3);  // warm-up
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        dfma_peak_kernel<<<blocks, threads>>>(out, iters, 0.999, 1e-3);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = ms < best ? ms : best;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (cudaGetLastError() != cudaSuccess) return BODE_E_CUDA;
+    const double flops = 2.0 * 8 * 16 * (double)iters * blocks * threads;
+    *seconds = best * 1e-3;
+    *flops_per_s = flops / (*seconds);
+    return BODE_OK;
+}

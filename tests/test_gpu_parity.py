@@ -1,0 +1,200 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference.
+
+Bars (BASELINE.json north_star):
+  * EXACT policy: RKC bitwise (states and every counter); RKCK per-system
+    max-norm relative error <= 1e-13 = 1e-3*eps with identical accepted /
+    rejected / RHS counts (device pow is libdevice, not glibc: ulp-level only
+    in the step-size controller, measured bitwise on >99% of systems).
+  * FAST policy (FMA, rsqrt): RKCK <= 1e-13 with identical counts; RKC is
+    reported against the exact run with a looser bound, since RKC step
+    selection is chaotic at the ulp level.
+Per-system relative error: max_j |dy_j| / max_j |y_j^ref| (acceptance.cpp:142-147).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import paper_1611_02274_b200 as B
+from paper_1611_02274_b200 import _abi as A
+from golden_cases import CASES, build_inputs, perturb, PLEIADES_IC, heat_ic
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+COUNTS = ("steps_accepted", "steps_rejected", "rhs_evals", "spec_rad_evals", "underflow")
+
+
+def sysrel(y, yref, num, dim):
+    a = y.reshape(dim, num)
+    b = yref.reshape(dim, num)
+    return np.max(np.abs(a - b), axis=0) / np.maximum(np.max(np.abs(b), axis=0), 1e-300)
+
+
+def problem_of(p: A.Problem) -> B.OdeProblem:
+    return B.OdeProblem(p.kind, p.dim, p.param_dim)
+
+
+def run_gpu(prob, solver, y0, g, arith, t0=0.0, t1=1.0, hout=0.1, gpus=1):
+    num = y0.size // prob.dim
+    batch = B.BatchStates(num, prob.dim, prob.param_dim, y0.copy(),
+                          g.copy() if g is not None else np.zeros(0))
+    r = B.outer_loop(problem_of(prob), batch, t0, t1, hout, solver=solver, arith=arith, gpus=gpus)
+    assert r.outer_steps == B.lib().bode_num_windows(t0, t1, hout)
+    return r.states.values, r.stats
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_exact_matches_golden(gpu, name):
+    gold = dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+    prob, solver, y0, g = build_inputs(CASES[name])
+    y, st = run_gpu(prob, solver, y0, g, "exact")
+    for k in COUNTS:
+        assert np.array_equal(st[k], gold[k]), k
+    num = y0.size // prob.dim
+    if solver == A.SOLVER_RKC:
+        assert np.array_equal(y.view(np.uint64), gold["y"].view(np.uint64))
+        assert np.array_equal(st["h_min_seen"], gold["h_min_seen"])
+    else:
+        err = sysrel(y, gold["y"], num, prob.dim)
+        assert err.max() <= 1e-13, err.max()
+        bitwise = np.mean(np.all((y == gold["y"]).reshape(prob.dim, num), axis=0))
+        assert bitwise >= 0.99, bitwise
+
+
+@pytest.mark.parametrize("name", ["cfg1_pleiades_rkck_s42", "cfg1_pleiades_rkck_s20140609"])
+def test_fast_rkck_within_bar(gpu, name):
+    gold = dict(np.load(os.path.join(GOLDEN, name + ".npz")))
+    prob, solver, y0, g = build_inputs(CASES[name])
+    y, st = run_gpu(prob, solver, y0, g, "fast")
+    err = sysrel(y, gold["y"], y0.size // 28, 28)
+    assert err.max() <= 1e-13, err.max()
+    for k in ("steps_accepted", "steps_rejected", "rhs_evals"):
+        assert np.array_equal(st[k], gold[k]), k
+
+
+def test_fast_rkc_close_to_exact(gpu):
+    prob, solver, y0, g = build_inputs(CASES["cfg3_heat64_rkc_s42"])
+    ye, _ = run_gpu(prob, solver, y0, g, "exact")
+    yf, _ = run_gpu(prob, solver, y0, g, "fast")
+    err = sysrel(yf, ye, y0.size // 64, 64)
+    assert err.max() <= 1e-4, err.max()  # O(relTol): a different, equally valid step sequence
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_pleiades_large_vs_oracle(gpu, oracle, arith):
+    """2^16 systems, perturbation 0.1 (divergence stress)."""
+    num = 1 << 16
+    prob = A.make_problem(A.PLEIADES)
+    y0 = perturb(PLEIADES_IC, 0.1, 42, num)
+    y, st = run_gpu(prob, A.SOLVER_RKCK, y0, None, arith)
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKCK, 0.0, 1.0, 0.1, y0)
+    err = sysrel(y, yo, num, 28)
+    assert err.max() <= 1e-13, err.max()
+    for k in ("steps_accepted", "steps_rejected", "rhs_evals", "underflow"):
+        assert np.array_equal(st[k], so[k]), k
+
+
+def test_heat64_exact_bitwise_vs_oracle(gpu, oracle):
+    num = 4096
+    prob = A.make_problem(A.HEAT, 64)
+    y0 = perturb(heat_ic(64), 0.01, 1234, num)
+    y, st = run_gpu(prob, A.SOLVER_RKC, y0, None, "exact")
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKC, 0.0, 1.0, 0.1, y0)
+    assert np.array_equal(y.view(np.uint64), yo.view(np.uint64))
+    for k in COUNTS + ("stages_total",):
+        assert np.array_equal(st[k], so[k]), k
+
+
+@pytest.mark.parametrize("n", [8, 16, 32])
+def test_heat_other_sizes_exact(gpu, oracle, n):
+    num = 1024
+    prob = A.make_problem(A.HEAT, n)
+    y0 = perturb(heat_ic(n), 0.01, 5, num)
+    y, st = run_gpu(prob, A.SOLVER_RKC, y0, None, "exact")
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKC, 0.0, 1.0, 0.1, y0)
+    assert np.array_equal(y.view(np.uint64), yo.view(np.uint64))
+    for k in COUNTS + ("stages_total",):
+        assert np.array_equal(st[k], so[k]), k
+
+
+def test_stiffness_varied_exact_bitwise(gpu, oracle):
+    """Config 4 at 2^16 systems: g0 log-uniform in [1, 1e4]."""
+    num = 1 << 16
+    case = dict(CASES["cfg4_expdecay_rkc_stiff"])
+    prob, solver, y0, g = build_inputs(case, num)
+    y, st = run_gpu(prob, solver, y0, g, "exact")
+    rc, yo, so, _ = oracle.outer_loop(prob, solver, 0.0, 1.0, 0.1, y0, g)
+    assert np.array_equal(y.view(np.uint64), yo.view(np.uint64))
+    for k in COUNTS + ("stages_total",):
+        assert np.array_equal(st[k], so[k]), k
+
+
+def test_stride_sample_at_2_20(gpu, oracle):
+    """Full-size property check: 2^20 Pleiades on the GPU, every 64th system
+    re-integrated by the oracle (systems are independent, batch_driver.hpp:16-21)."""
+    num = 1 << 20
+    prob = A.make_problem(A.PLEIADES)
+    y0 = perturb(PLEIADES_IC, 0.01, 42, num)
+    y, st = run_gpu(prob, A.SOLVER_RKCK, y0, None, "exact")
+    idx = np.arange(0, num, 64)
+    sub = np.ascontiguousarray(y0.reshape(28, num)[:, idx]).reshape(-1)
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKCK, 0.0, 1.0, 0.1, sub)
+    got = np.ascontiguousarray(y.reshape(28, num)[:, idx]).reshape(-1)
+    err = sysrel(got, yo, idx.size, 28)
+    assert err.max() <= 1e-13
+    assert np.array_equal(st["steps_accepted"][idx], so["steps_accepted"])
+    assert np.array_equal(st["steps_rejected"][idx], so["steps_rejected"])
+
+
+@pytest.mark.parametrize("solver", ["rkck", "rkc"])
+def test_block_size_invariance(gpu, solver):
+    """Results are bitwise independent of the launch shape (test_batch.cpp:127-142)."""
+    if solver == "rkck":
+        prob, y0, g = A.make_problem(A.PLEIADES), perturb(PLEIADES_IC, 0.01, 3, 3000), None
+    else:
+        prob, y0, g = A.make_problem(A.HEAT, 64), perturb(heat_ic(64), 0.01, 3, 1000), None
+    L = B.lib()
+    outs = []
+    try:
+        for bs in (64, 128, 256):
+            assert L.bode_set_block_size(bs) == 0
+            outs.append(run_gpu(prob, solver, y0, g, "exact")[0])
+    finally:
+        L.bode_set_block_size(0)
+    assert all(np.array_equal(o.view(np.uint64), outs[0].view(np.uint64)) for o in outs[1:])
+
+
+def test_outer_loop_equals_windowed_int_driver(gpu):
+    """Device-resident outerLoop == 10 host-pointer integrateBatch windows."""
+    prob = B.problems.heat_equation(64)
+    b = B.problems.perturb_initial_conditions(heat_ic(64), 0.01, 11, 777)
+    r = B.outer_loop(prob, b, 0.0, 1.0, 0.1, solver="rkc")
+    cur = b
+    acc = np.zeros(777, dtype=np.int64)
+    for k in range(1, 11):
+        t0 = 0.0 if k == 1 else 0.0 + (k - 1) * 0.1
+        t1 = 1.0 if k == 10 else 0.0 + k * 0.1
+        w = B.integrate_batch(prob, cur, t0, t1, solver="rkc")
+        cur = w.states
+        acc += w.stats["steps_accepted"]
+    assert np.array_equal(cur.values.view(np.uint64), r.states.values.view(np.uint64))
+    assert np.array_equal(acc, r.stats["steps_accepted"])
+
+
+def test_device_pointer_entry_with_torch(gpu):
+    import torch
+    prob = A.make_problem(A.PLEIADES)
+    num = 5000
+    y0 = perturb(PLEIADES_IC, 0.01, 8, num)
+    yd = torch.from_numpy(y0.copy()).cuda()
+    st = torch.zeros(num * 8, dtype=torch.int64, device="cuda")
+    tol = A.default_tol()
+    s = torch.cuda.current_stream()
+    B.int_driver_device(problem_of(prob), "rkck", "exact", 0.0, 0.1, num, 0, yd.data_ptr(), tol,
+                        st.data_ptr(), False, s.cuda_stream)
+    torch.cuda.synchronize()
+    host = B.integrate_batch(problem_of(prob), B.BatchStates(num, 28, 0, y0.copy(), np.zeros(0)),
+                             0.0, 0.1)
+    assert np.array_equal(yd.cpu().numpy().view(np.uint64), host.states.values.view(np.uint64))
