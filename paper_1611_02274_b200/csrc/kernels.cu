@@ -12,6 +12,7 @@
 
 #include "dispatch.h"
 #include "rkc.cuh"
+#include "rkck_nystrom.cuh"
 
 namespace bode {
 
@@ -33,7 +34,9 @@ __global__ void __launch_bounds__(kMaxBlock)
 #pragma unroll
     for (int p = 0; p < PP; ++p) g[p] = R(P::P > 0 ? g_soa[sys + num * (long long)p] : 0.0);
     DevStats st;
-    if constexpr (SOLVER == 0)
+    if constexpr (SOLVER == 0 && is_second_order<P>::value)
+        rkck_nystrom_system<P, R>(t, tEnd, y, tol, st);
+    else if constexpr (SOLVER == 0)
         rkck_system<P, R, L, KSMEM>(G, t, tEnd, y, g, tol, st);
     else
         rkc_system<P, R, L>(G, t, tEnd, y, g, tol, st);
@@ -60,7 +63,7 @@ static KernelEntry make_entry(int kind, int arith) {
     e.solver = SOLVER;
     e.arith = arith;
     e.lanes = L;
-    e.smem_per_thread = KSMEM ? 4 * C_of<P, L>() * (int)sizeof(double) : 0;
+    e.smem_per_thread = KSMEM ? kSmemStride<C_of<P, L>()>() * (int)sizeof(double) : 0;
     e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM>;
     e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                   const double* g, double* y, DevStats* st, long long num, double t,

@@ -90,14 +90,12 @@ __device__ __forceinline__ R seq_sum(const Group<L>& G, const R (&terms)[C], R i
 struct Pleiades {
     static constexpr int N = 28, P = 0;
     static constexpr const char* name = "pleiades";
-    template <class R, int L>
-    __device__ __forceinline__ static void rhs(const Group<L>&, R, const R (&w)[N],
-                                               const R*, R (&out)[N]) {
-        static_assert(L == 1, "Pleiades couples all components: one lane per system");
+    // Accelerations a(q) for positions q = (x_1..x_7, y_1..y_7): the out[14..27]
+    // half of the reference RHS, accumulated in the reference's order.
+    template <class R>
+    __device__ __forceinline__ static void accel(const R* w, R* a) {
 #pragma unroll
-        for (int i = 0; i < 14; ++i) out[i] = w[14 + i];
-#pragma unroll
-        for (int i = 14; i < 28; ++i) out[i] = R(0.0);
+        for (int i = 0; i < 14; ++i) a[i] = R(0.0);
 #pragma unroll
         for (int i = 0; i < 7; ++i) {
 #pragma unroll
@@ -109,22 +107,30 @@ struct Pleiades {
                 const double mj = double(j + 1);
                 if constexpr (is_exact<R>::value) {
                     const R invR3 = R(1.0) / (r2 * sqrt_(r2));
-                    out[14 + i] += R(mj) * dx * invR3;
-                    out[21 + i] += R(mj) * dy * invR3;
-                    out[14 + j] -= R(mi) * dx * invR3;
-                    out[21 + j] -= R(mi) * dy * invR3;
+                    a[i] += R(mj) * dx * invR3;
+                    a[7 + i] += R(mj) * dy * invR3;
+                    a[j] -= R(mi) * dx * invR3;
+                    a[7 + j] -= R(mi) * dy * invR3;
                 } else {
-                    const double rs = rsqrt(val(r2));
+                    const double rs = rsqrt_fast(val(r2));
                     const double invR3 = rs * rs * rs;
                     const double ax = val(dx) * invR3;
                     const double ay = val(dy) * invR3;
-                    out[14 + i] += mj * ax;
-                    out[21 + i] += mj * ay;
-                    out[14 + j] -= mi * ax;
-                    out[21 + j] -= mi * ay;
+                    a[i] += mj * ax;
+                    a[7 + i] += mj * ay;
+                    a[j] -= mi * ax;
+                    a[7 + j] -= mi * ay;
                 }
             }
         }
+    }
+    template <class R, int L>
+    __device__ __forceinline__ static void rhs(const Group<L>&, R, const R (&w)[N],
+                                               const R*, R (&out)[N]) {
+        static_assert(L == 1, "Pleiades couples all components: one lane per system");
+#pragma unroll
+        for (int i = 0; i < 14; ++i) out[i] = w[14 + i];
+        accel<R>(w, out + 14);
     }
 };
 

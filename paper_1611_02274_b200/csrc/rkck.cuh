@@ -9,8 +9,8 @@
 //
 // Storage: y and f0 live in registers. The stage derivatives k2..k5 live in
 // registers for small systems or in shared memory for large ones (KSMEM),
-// laid out [stage][component][thread] so a warp touches 32 consecutive
-// doubles (conflict-free). k6 stays in the RHS output registers.
+// one odd-length row per thread (conflict-free, immediate-offset addressing).
+// k6 stays in the RHS output registers.
 #pragma once
 
 #include "dispatch.h"
@@ -63,6 +63,12 @@ constexpr double s1 = 2825.0 / 27648.0, s3 = 18575.0 / 48384.0, s4 = 13525.0 / 5
 constexpr double d1 = c1 - s1, d3 = c3 - s3, d4 = c4 - s4, d5 = c5 - s5, d6 = c6 - s6;
 }  // namespace ck
 
+// Shared-memory row length per thread for 4 stage slots of C doubles: rounded
+// up to an odd number of doubles so the 64-bit accesses of a half-warp hit 16
+// distinct bank pairs (conflict-free) while every address is base + immediate.
+template <int C>
+__host__ __device__ constexpr int kSmemStride() { return (4 * C) | 1; }
+
 // Stage-derivative store for k2..k5 (slot 0..3).
 template <class R, int C, bool SMEM>
 struct KStore;
@@ -76,15 +82,13 @@ struct KStore<R, C, false> {
 
 template <class R, int C>
 struct KStore<R, C, true> {
-    double* base;  // dynamic shared memory, [slot][c][blockDim.x]
-    int stride;
+    double* base;  // dynamic shared memory: one row of kSmemStride<C>() doubles per thread
     __device__ __forceinline__ KStore() {
         extern __shared__ double bode_smem[];
-        base = bode_smem + threadIdx.x;
-        stride = blockDim.x;
+        base = bode_smem + threadIdx.x * kSmemStride<C>();
     }
-    __device__ __forceinline__ R get(int m, int c) const { return R(base[(m * C + c) * stride]); }
-    __device__ __forceinline__ void set(int m, int c, R v) { base[(m * C + c) * stride] = val(v); }
+    __device__ __forceinline__ R get(int m, int c) const { return R(base[m * C + c]); }
+    __device__ __forceinline__ void set(int m, int c, R v) { base[m * C + c] = val(v); }
 };
 
 // adjustStep (rkck.cpp:100-113)

@@ -1,0 +1,203 @@
+// rkck_nystrom.cuh -- RKCK for second-order systems y = (q, v), dq/dt = v,
+// dv/dt = a(q) (the Pleiades problem, problems.cpp:13-35).
+//
+// This is rkck::step / errorNorm / adjustStep / driver (rkck.cpp:34-159)
+// evaluated on the same operands in the same order, but stored in Nystrom
+// form: for such an RHS the first half of every stage derivative is a copy
+// of the second half of its stage argument (problems.cpp:17,
+// out[i] = w[14 + i]), so
+//   f0      = (v, A0)            -- only A0 = a(q) is stored, v aliases y
+//   k_j     = (V_j, A_j)         -- V_j = v + h * sum_m b_jm A_m
+//   arg_j   = (Q_j, V_j)         -- Q_j = q + h * sum_m b_jm V_m  (V_1 = v)
+// Every double that enters an operation is bitwise the one the reference
+// uses, so with R = xd the result is bitwise rkck::driver's (up to the
+// device pow in the controller, see arith.cuh).
+//
+// Register/shared-memory plan (one system per thread, SURVEY.md 7.4 hard
+// part 1): q, v, A0 in registers (3 x M doubles); k2..k5 in shared memory,
+// one odd-length row per thread (conflict-free, immediate offsets); stages
+// 3..6 run as one rolled loop (one inlined acceleration, bounded live ranges);
+// k6 reuses k2's slot (c2 = c*2 = 0, so k2 is dead once arg6 is formed); the
+// error norm is folded into the step and costs one division (arith.cuh
+// QuotMax); the fast policy is free of out-of-line calls.
+#pragma once
+
+#include "rkck.cuh"
+
+namespace bode {
+
+template <class P>
+struct is_second_order {
+    static constexpr bool value = false;
+};
+template <>
+struct is_second_order<Pleiades> {
+    static constexpr bool value = true;
+};
+
+#define BODE_FENCE() asm volatile("" ::: "memory")
+
+// b_j1..b_j5 for stages 3..6 (rkck.cpp:15-19), read uniformly by the warp
+__constant__ double c_ck_b[4][5] = {
+    {3.0 / 40.0, 9.0 / 40.0, 0.0, 0.0, 0.0},
+    {3.0 / 10.0, -9.0 / 10.0, 6.0 / 5.0, 0.0, 0.0},
+    {-11.0 / 54.0, 5.0 / 2.0, -70.0 / 27.0, 35.0 / 27.0, 0.0},
+    {1631.0 / 55296.0, 175.0 / 512.0, 575.0 / 13824.0, 44275.0 / 110592.0, 253.0 / 4096.0}};
+
+template <class P, class R>
+__device__ __forceinline__ void rkck_nystrom_system(double t_in, double tEnd_in,
+                                                    R (&y)[P::N], const DevTol& tol,
+                                                    DevStats& st) {
+    constexpr int M = P::N / 2;
+    using namespace ck;
+    stats_init(st);
+    extern __shared__ double bode_smem[];
+    double* const ks = bode_smem + threadIdx.x * kSmemStride<P::N>();
+    // slot m holds k_{m+2} (slot 0 holds k6 after stage 6): V at [0, M), A at [M, 2M)
+    auto kget = [&](int m, int c) -> R { return R(ks[m * P::N + c]); };
+    auto kset = [&](int m, int c, R v) { ks[m * P::N + c] = val(v); };
+
+    R* const q = y;      // y[0..M)
+    R* const v = y + M;  // y[M..2M)
+    const R tEnd(tEnd_in);
+    R t(t_in);
+    const R hMax = fabs_(tEnd - t);
+    const R hMin(tol.h_min_floor);
+    R h = R(0.5) * fabs_(tEnd - t);
+    const R uround(tol.uround), eps(tol.eps), tiny(tol.tiny);
+
+    R A0[M];  // acceleration half of f0 = f(t, y)
+    bool haveF = false;
+
+#pragma unroll 1
+    while (tEnd - t > uround * fabs_(tEnd)) {
+        h = fmin_(tEnd - t, h);
+        if (!haveF) {  // rejected retries reuse f(t, y) (rkck.cpp:133-137)
+            P::template accel<R>(q, A0);
+            ++st.rhs_evals;
+            haveF = true;
+        }
+        R Q[M], Acc[M];
+        // ---- stage 2: arg = y + h*b21*f0 (rkck.cpp:42-44) ----
+        {
+            const R hb = h * R(b21);
+#pragma unroll
+            for (int i = 0; i < M; ++i) kset(0, i, v[i] + hb * A0[i]);
+#pragma unroll
+            for (int i = 0; i < M; ++i) Q[i] = q[i] + hb * v[i];
+            BODE_FENCE();
+            P::template accel<R>(Q, Acc);
+#pragma unroll
+            for (int i = 0; i < M; ++i) kset(0, M + i, Acc[i]);
+            BODE_FENCE();
+        }
+        // ---- stages 3..6 (rkck.cpp:46-64): arg = y + h*(b_j1 f0 + b_j2 k2 + ...)
+#pragma unroll 1
+        for (int j = 3; j <= 6; ++j) {
+            const double* bj = c_ck_b[j - 3];
+            const int nk = j - 2;                 // k2..k_{j-1} enter this stage
+            const int out = (j == 6) ? 0 : j - 2;  // k6 reuses k2's slot
+            // velocity half of k_j (= of arg_j); the sums run in the
+            // reference's left-to-right order
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                R s = R(bj[0]) * A0[i];
+#pragma unroll 1
+                for (int m = 0; m < nk; ++m) s = s + R(bj[m + 1]) * kget(m, M + i);
+                Acc[i] = v[i] + h * s;
+            }
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                R s = R(bj[0]) * v[i];
+#pragma unroll 1
+                for (int m = 0; m < nk; ++m) s = s + R(bj[m + 1]) * kget(m, i);
+                Q[i] = q[i] + h * s;
+            }
+            BODE_FENCE();
+#pragma unroll
+            for (int i = 0; i < M; ++i) kset(out, i, Acc[i]);
+            BODE_FENCE();
+            P::template accel<R>(Q, Acc);
+#pragma unroll
+            for (int i = 0; i < M; ++i) kset(out, M + i, Acc[i]);
+            BODE_FENCE();
+        }
+        st.rhs_evals += 5;
+        st.stages_total += 6;
+
+        // ---- yErr folded into errorNorm (rkck.cpp:75-76, :88-98) ----
+        // err = max_i |yErr_i / (|y_i| + |h f0_i| + tiny)| / eps; the max is
+        // order-independent, so the q and v halves are visited together.
+        R err;
+        bool nanFlag = false;
+        {
+            QuotMax qm;
+            double fm = 0.0;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const R eq = h * (R(d1) * v[i] + R(d3) * kget(1, i) + R(d4) * kget(2, i) +
+                                  R(d5) * kget(3, i) + R(d6) * kget(0, i));
+                const R ev = h * (R(d1) * A0[i] + R(d3) * kget(1, M + i) +
+                                  R(d4) * kget(2, M + i) + R(d5) * kget(3, M + i) +
+                                  R(d6) * kget(0, M + i));
+                if (!isfinite_(eq) || !isfinite_(ev)) nanFlag = true;
+                const R dq = fabs_(q[i]) + fabs_(h * v[i]) + tiny;
+                const R dv = fabs_(v[i]) + fabs_(h * A0[i]) + tiny;
+                if constexpr (is_exact<R>::value) {
+                    qm.push(fabs(val(eq)), val(dq));
+                    qm.push(fabs(val(ev)), val(dv));
+                } else {
+                    fm = fmax(fm, fabs(val(eq)) * rcp_fast(val(dq)));
+                    fm = fmax(fm, fabs(val(ev)) * rcp_fast(val(dv)));
+                }
+            }
+            if constexpr (is_exact<R>::value)
+                err = R(qm.value());
+            else
+                err = R(fm);
+        }
+        err = err / eps;
+
+        R hNew;
+        bool accepted;
+        if constexpr (is_exact<R>::value) {
+            accepted = rkck_adjust(h, err, nanFlag, hMin, hMax, tol, hNew);
+        } else {  // adjustStep (rkck.cpp:100-113) with a call-free pow
+            if (err > 1.0 || !isfinite(err) || nanFlag) {
+                accepted = false;
+                hNew = (!isfinite(err) || nanFlag)
+                           ? tol.p1 * h
+                           : fmax(tol.safety * h * pow_fast(err, tol.pshrnk), tol.p1 * h);
+            } else {
+                accepted = true;
+                const double hn =
+                    (err > tol.errcon) ? tol.safety * h * pow_fast(err, tol.pgrow) : 5.0 * h;
+                hNew = fmax(val(hMin), fmin(val(hMax), hn));
+            }
+        }
+        if (accepted) {
+            t += h;
+            stats_accept(st, val(h));
+            // yNext (rkck.cpp:74): the q half reads the old v, so it goes first
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+                q[i] = q[i] + h * (R(c1) * v[i] + R(c3) * kget(1, i) + R(c4) * kget(2, i) +
+                                   R(c6) * kget(0, i));
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+                v[i] = v[i] + h * (R(c1) * A0[i] + R(c3) * kget(1, M + i) +
+                                   R(c4) * kget(2, M + i) + R(c6) * kget(0, M + i));
+            haveF = false;
+            h = hNew;
+        } else {
+            ++st.steps_rejected;
+            if (hNew < R(tol.h_min_floor)) {  // freeze at the last accepted state
+                st.underflow = 1;
+                break;
+            }
+            h = hNew;
+        }
+    }
+}
+
+}  // namespace bode

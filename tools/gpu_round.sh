@@ -1,0 +1,32 @@
+#!/bin/bash
+# One GPU session: tests, smoke, bench, ncu launch list + full captures.
+# Usage (under gpurun): bash tools/gpu_round.sh <tag> [parts...]
+# parts: tests smoke bench ncu  (default: all)
+set -u
+TAG=${1:-r01}; shift || true
+PARTS=${*:-"tests smoke bench ncu"}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi > $OUT/nvidia-smi.txt 2>&1
+nproc > $OUT/nproc.txt
+for p in $PARTS; do
+  case $p in
+    tests) timeout 1500 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $OUT/status.txt ;;
+    smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1; echo "smoke rc=$?" >> $OUT/status.txt ;;
+    bench) timeout 900 python bench.py > $OUT/bench.txt 2>&1; echo "bench rc=$?" >> $OUT/status.txt ;;
+    bench_exact) timeout 900 python bench.py --arith exact --no-cpu > $OUT/bench_exact.txt 2>&1; echo "bench_exact rc=$?" >> $OUT/status.txt ;;
+    ncu)
+      timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 1 --num 1048576 \
+        --rkc-num 262144 --no-e2e --no-cpu > $OUT/ncu_launches_bench.txt 2>&1
+      echo "ncu_launches rc=$?" >> $OUT/status.txt
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:integrate \
+        -s 1 -c 1 -o $OUT/prof_rkck python bench.py --steps 1 --warmup 1 --num 262144 \
+        --rkc-num 0 --no-e2e --no-cpu > $OUT/ncu_full_rkck.txt 2>&1
+      echo "ncu_full_rkck rc=$?" >> $OUT/status.txt
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:integrate \
+        -s 3 -c 1 -o $OUT/prof_rkc python bench.py --steps 1 --warmup 1 --num 4096 \
+        --rkc-num 131072 --no-e2e --no-cpu > $OUT/ncu_full_rkc.txt 2>&1
+      echo "ncu_full_rkc rc=$?" >> $OUT/status.txt ;;
+  esac
+done
