@@ -10,6 +10,7 @@
  * Third-party arithmetic on the path: glibc libm (pow, cbrt, sqrt, lround),
  * called exactly where the reference calls it.
  */
+#define _GNU_SOURCE
 #include "bode_oracle.h"
 
 #include <math.h>
@@ -866,4 +867,134 @@ double orc_glibc_cbrt(double x) {
     const double t2 = u * u * u;
     const double ym = u * (t2 + 2.0 * xm) / (2.0 * t2 + xm) * factor[2 + xe % 3];
     return ldexp(x > 0.0 ? ym : -ym, xe / 3);
+}
+
+/* ------------------------------------------------------------------ */
+/* glibc 2.39 pow, x86-64 FMA variant (__pow_fma, selected by ifunc on */
+/* FMA/AVX2 hosts), restated from its instruction sequence: the ARM    */
+/* optimized-routines algorithm (sysdeps/ieee754/dbl-64/e_pow.c) with  */
+/* GCC's contractions. Tables (__pow_log_data, __exp_data) are read    */
+/* from the libm loaded in this process, located by signature. The    */
+/* reference calls pow in rkck::adjustStep (rkck.cpp:105, :109).       */
+/* ------------------------------------------------------------------ */
+#include <link.h>
+
+typedef struct {
+    const double* log_head; /* ln2hi, ln2lo, A[0..6], then tab[128][4] */
+    const double* exp_head; /* invln2N, shift, negln2hiN, negln2loN, C2..C5 */
+    const uint64_t* exp_tab; /* tab[256] */
+} orc_powtab_t;
+
+static orc_powtab_t g_powtab;
+static int g_powtab_state = 0; /* 0 unknown, 1 found, -1 absent */
+
+static const unsigned char* memfind(const unsigned char* h, size_t n, const void* pat, size_t m) {
+    for (size_t i = 0; i + m <= n; i += 8)
+        if (memcmp(h + i, pat, m) == 0) return h + i;
+    return NULL;
+}
+
+static int phdr_cb(struct dl_phdr_info* info, size_t size, void* data) {
+    (void)size;
+    if (!info->dlpi_name || !strstr(info->dlpi_name, "libm.so")) return 0;
+    orc_powtab_t* t = (orc_powtab_t*)data;
+    const double log_sig[3] = {0x1.62e42fefa3800p-1, 0x1.ef35793c76730p-45, -0.5};
+    const double exp_sig[2] = {0x1.71547652b82fep+7, 0x1.8p52};
+    const uint64_t tab_sig[4] = {0x0ull, 0x3ff0000000000000ull, 0x3c9b3b4f1a88bf6eull,
+                                 0x3feff63da9fb3335ull};
+    for (int j = 0; j < info->dlpi_phnum; ++j) {
+        const ElfW(Phdr)* ph = &info->dlpi_phdr[j];
+        if (ph->p_type != PT_LOAD || !(ph->p_flags & PF_R) || (ph->p_flags & PF_X)) continue;
+        const unsigned char* base = (const unsigned char*)(info->dlpi_addr + ph->p_vaddr);
+        size_t n = ph->p_memsz & ~(size_t)7;
+        base = (const unsigned char*)(((uintptr_t)base + 7) & ~(uintptr_t)7);
+        if (!t->log_head) t->log_head = (const double*)memfind(base, n, log_sig, sizeof log_sig);
+        if (!t->exp_head) t->exp_head = (const double*)memfind(base, n, exp_sig, sizeof exp_sig);
+        if (!t->exp_tab) t->exp_tab = (const uint64_t*)memfind(base, n, tab_sig, sizeof tab_sig);
+    }
+    return 1;
+}
+
+int orc_glibc_pow_tables(const double** log_head, const double** exp_head,
+                         const uint64_t** exp_tab) {
+    if (g_powtab_state == 0) {
+        memset(&g_powtab, 0, sizeof g_powtab);
+        dl_iterate_phdr(phdr_cb, &g_powtab);
+        g_powtab_state = (g_powtab.log_head && g_powtab.exp_head && g_powtab.exp_tab) ? 1 : -1;
+    }
+    if (g_powtab_state != 1) return 0;
+    *log_head = g_powtab.log_head;
+    *exp_head = g_powtab.exp_head;
+    *exp_tab = g_powtab.exp_tab;
+    return 1;
+}
+
+static inline uint64_t asu64(double d) { uint64_t u; memcpy(&u, &d, 8); return u; }
+static inline double asf64(uint64_t u) { double d; memcpy(&d, &u, 8); return d; }
+
+/* Main path only (x positive normal, 2^-65 <= |y| < 2^64, |y log x| < 512);
+ * everything else returns libm pow itself (the reference's own value). */
+double orc_glibc_pow(double x, double y) {
+    const double *L, *E;
+    const uint64_t* ET;
+    const uint64_t ix = asu64(x), iy = asu64(y);
+    const uint32_t topx = (uint32_t)(ix >> 52), topy = (uint32_t)(iy >> 52);
+    if (!orc_glibc_pow_tables(&L, &E, &ET) || topx - 1u >= 0x7feu ||
+        (topy & 0x7ffu) - 0x3beu > 0x7fu)
+        return pow(x, y);
+    /* log_inline */
+    const uint64_t tmp = ix - 0x3fe6955500000000ull;
+    const int i = (int)((tmp >> 45) & 0x7f);
+    const int k = (int)((int64_t)tmp >> 52);
+    const double z = asf64(ix - (tmp & 0xfff0000000000000ull));
+    const double kd = (double)k;
+    const double* T = L + 9 + 4 * i; /* invc, pad, logc, logctail */
+    const double* A = L + 2;
+    const double t1 = fma(kd, L[0], T[2]);
+    const double lo1 = fma(kd, L[1], T[3]);
+    const double r = fma(z, T[0], -1.0);
+    const double ar = r * A[0];
+    const double p12 = fma(r, A[2], A[1]);
+    const double p34 = fma(r, A[4], A[3]);
+    const double t2 = r + t1;
+    const double lo2 = (t1 - t2) + r;
+    const double ar2 = r * ar;
+    const double ar3 = r * ar2;
+    const double lo3 = fma(ar, r, -ar2);
+    const double hi = t2 + ar2;
+    const double p56 = fma(r, A[6], A[5]);
+    const double lo4 = (t2 - hi) + ar2;
+    const double q = fma(p56, ar2, p34);
+    const double pp = fma(ar2, q, p12);
+    double lo = ((lo1 + lo2) + lo3) + lo4;
+    lo = fma(ar3, pp, lo);
+    const double ly = hi + lo;
+    const double ltail = (hi - ly) + lo;
+    /* y * log(x) as ehi + elo */
+    const double ehi = y * ly;
+    const double elo = fma(y, ltail, fma(ly, y, -ehi));
+    /* exp_inline */
+    const uint32_t abstop = (uint32_t)(asu64(ehi) >> 52) & 0x7ffu;
+    if (abstop - 0x3c9u > 0x3eu) {
+        if (abstop - 0x3c9u >= 0x80000000u) return 1.0 + ehi; /* tiny: avoid spurious underflow */
+        return pow(x, y);
+    }
+    double kk = fma(ehi, E[0], E[1]);
+    const uint64_t ki = asu64(kk);
+    kk = kk - E[1];
+    double rr = fma(kk, E[2], ehi);
+    rr = fma(kk, E[3], rr);
+    rr = elo + rr;
+    const uint64_t idx = 2 * (ki & 0x7f);
+    const uint64_t top = ki << 45;
+    const double tail = asf64(ET[idx]);
+    const uint64_t sbits = ET[idx + 1] + top;
+    double a = fma(rr, E[5], E[4]);
+    const double b = rr + tail;
+    const double r2 = rr * rr;
+    const double c = fma(rr, E[7], E[6]);
+    a = fma(a, r2, b);
+    const double t = fma(c, r2 * r2, a);
+    const double scale = asf64(sbits);
+    return fma(scale, t, scale);
 }

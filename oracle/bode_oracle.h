@@ -94,6 +94,10 @@ int orc_power_method(const bode_problem_t* p, double t, const double* y,
                      const double* vWarm, double* sigma, double* eigvec,
                      int* iterations, int* converged);
 
+/* glibc pow (x86-64 FMA build) restated; tables read from the loaded libm */
+double orc_glibc_pow(double x, double y);
+int orc_glibc_pow_tables(const double** log_head, const double** exp_head, const uint64_t** exp_tab);
+
 /* glibc cbrt restated (see bode_oracle.c) */
 double orc_glibc_cbrt(double x);
 

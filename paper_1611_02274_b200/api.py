@@ -100,6 +100,8 @@ def lib():
         "bode_heat_initial_condition": (None, [c_i32, PD]),
         "bode_selftest_cbrt": (ctypes.c_int, [PD, PD, c_i64]),
         "bode_selftest_fp64_peak": (ctypes.c_int, [PD, PD]),
+        "bode_selftest_pow": (ctypes.c_int, [PD, PD, PD, c_i64]),
+        "bode_pow_exact_available": (ctypes.c_int, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

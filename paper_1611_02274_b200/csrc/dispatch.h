@@ -10,6 +10,8 @@ constexpr int kMaxBlock = 256;
 struct DevTol {  // bode_tol_t, by value in the kernel parameters
     double eps, abs_tol, rel_tol, uround, tiny, safety, p1, errcon, pgrow, pshrnk,
         h_min_floor, kappa;
+    const double* powtab;    // host-libm pow tables on this device (arith.cuh), or null
+    const double* rkc_coef;  // RKC coefficient table for this kappa/policy (rkc.cuh), or null
 };
 
 struct DevStats {  // bode_stats_t, per system (AoS, 64 bytes)
@@ -33,8 +35,11 @@ struct KernelEntry {
     int default_block;
     const void* fn;
     LaunchFn launch;
+    void (*build_rkc_table)(double* tab, double kappa, cudaStream_t s);  // null for RKCK
 };
 
 const KernelEntry* kernel_table(int* count);
+const double* device_powtab();
+long long rkc_table_doubles();
 
 }  // namespace bode

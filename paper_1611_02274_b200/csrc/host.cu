@@ -9,11 +9,14 @@
 //   outerLoop window schedule        batch_driver.cpp:99-105
 //   per-system stats merge           batch_driver.cpp:109-110, ode_problem.hpp:72-80
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <link.h>
 
 #include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -65,19 +68,90 @@ DevTol to_dev(const bode_tol_t* t) {
     d.pshrnk = t->pshrnk;
     d.h_min_floor = t->h_min_floor;
     d.kappa = t->kappa;
+    d.powtab = nullptr;
+    d.rkc_coef = nullptr;
     return d;
 }
 
+// ---- host libm pow tables for the EXACT policy (arith.cuh pow_glibc) ----
+// glibc's pow reads __pow_log_data and __exp_data (hidden symbols); they are
+// located in the loaded libm by content signature and copied verbatim, so
+// the device evaluates pow over exactly the host's tables. Only the x86-64
+// FMA build of pow is restated, so this also requires the ifunc condition
+// that selects it (FMA and AVX2).
+struct PowTabSearch {
+    const double* log_head = nullptr;
+    const double* exp_head = nullptr;
+    const uint64_t* exp_tab = nullptr;
+};
+
+const unsigned char* find8(const unsigned char* h, size_t n, const void* pat, size_t m) {
+    for (size_t i = 0; i + m <= n; i += 8)
+        if (std::memcmp(h + i, pat, m) == 0) return h + i;
+    return nullptr;
+}
+
+int powtab_cb(struct dl_phdr_info* info, size_t, void* data) {
+    if (!info->dlpi_name || !std::strstr(info->dlpi_name, "libm.so")) return 0;
+    auto* s = static_cast<PowTabSearch*>(data);
+    const double log_sig[3] = {0x1.62e42fefa3800p-1, 0x1.ef35793c76730p-45, -0.5};
+    const double exp_sig[2] = {0x1.71547652b82fep+7, 0x1.8p52};
+    const uint64_t tab_sig[4] = {0x0ull, 0x3ff0000000000000ull, 0x3c9b3b4f1a88bf6eull,
+                                 0x3feff63da9fb3335ull};
+    for (int j = 0; j < info->dlpi_phnum; ++j) {
+        const ElfW(Phdr)& ph = info->dlpi_phdr[j];
+        if (ph.p_type != PT_LOAD || !(ph.p_flags & PF_R) || (ph.p_flags & PF_X)) continue;
+        uintptr_t b = (info->dlpi_addr + ph.p_vaddr + 7) & ~uintptr_t(7);
+        const auto* base = reinterpret_cast<const unsigned char*>(b);
+        const size_t n = ph.p_memsz & ~size_t(7);
+        if (!s->log_head) s->log_head = (const double*)find8(base, n, log_sig, sizeof log_sig);
+        if (!s->exp_head) s->exp_head = (const double*)find8(base, n, exp_sig, sizeof exp_sig);
+        if (!s->exp_tab) s->exp_tab = (const uint64_t*)find8(base, n, tab_sig, sizeof tab_sig);
+    }
+    return 1;
+}
+
+// host copy of the 785-double table image, or empty when unavailable
+const std::vector<double>& host_powtab() {
+    static std::vector<double> img;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        __builtin_cpu_init();
+        if (!__builtin_cpu_supports("fma") || !__builtin_cpu_supports("avx2")) return;
+        dlopen("libm.so.6", RTLD_NOW | RTLD_GLOBAL);  // make sure it is mapped
+        PowTabSearch s;
+        dl_iterate_phdr(powtab_cb, &s);
+        if (!s.log_head || !s.exp_head || !s.exp_tab) return;
+        img.resize(785);
+        std::memcpy(img.data(), s.log_head, 9 * sizeof(double));
+        std::memcpy(img.data() + 9, s.log_head + 9, 512 * sizeof(double));
+        std::memcpy(img.data() + 521, s.exp_head, 8 * sizeof(double));
+        std::memcpy(img.data() + 529, s.exp_tab, 256 * sizeof(double));
+    });
+    return img;
+}
+
+// First compiled kernel for (problem, solver, policy). Several lane-group
+// widths may be compiled for one problem; BODE_LANES=<L> (tuning knob, e.g.
+// for A/B measurements) prefers the variant with that width. All variants
+// give bitwise-identical results.
 const KernelEntry* find_entry(const bode_problem_t* p, int solver, int arith) {
     int n = 0;
     const KernelEntry* tab = bode::kernel_table(&n);
+    static const int want_lanes = [] {
+        const char* s = std::getenv("BODE_LANES");
+        return s ? std::atoi(s) : 0;
+    }();
+    const KernelEntry* first = nullptr;
     for (int i = 0; i < n; ++i) {
         const KernelEntry& e = tab[i];
         if (e.kind == p->kind && e.dim == p->dim && e.param_dim == p->param_dim &&
-            e.solver == solver && e.arith == arith)
-            return &e;
+            e.solver == solver && e.arith == arith) {
+            if (want_lanes == 0 || e.lanes == want_lanes) return &e;
+            if (!first) first = &e;
+        }
     }
-    return nullptr;
+    return first;
 }
 
 int check_problem_shape(const bode_problem_t* p) {
@@ -113,6 +187,34 @@ int validate_call(const bode_problem_t* p, int solver, int arith, double t, doub
     return BODE_OK;
 }
 
+// RKC stage-coefficient tables (rkc.cuh), one per (device, policy, kappa),
+// built on first use by the device generator itself.
+int rkc_table_for(const KernelEntry* e, double kappa, cudaStream_t s, const double** out) {
+    struct Key {
+        int dev, arith;
+        double kappa;
+        const double* tab;
+    };
+    static std::mutex m;
+    static std::vector<Key> cache;
+    int dev = 0;
+    BODE_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(m);
+    for (const Key& k : cache)
+        if (k.dev == dev && k.arith == e->arith && k.kappa == kappa) {
+            *out = k.tab;
+            return BODE_OK;
+        }
+    double* tab = nullptr;
+    BODE_CUDA(cudaMalloc(&tab, bode::rkc_table_doubles() * sizeof(double)));
+    e->build_rkc_table(tab, kappa, s);
+    BODE_CUDA(cudaGetLastError());
+    BODE_CUDA(cudaStreamSynchronize(s));
+    cache.push_back({dev, e->arith, kappa, tab});
+    *out = tab;
+    return BODE_OK;
+}
+
 int block_for(const KernelEntry* e) {
     int b = g_block_override.load();
     if (b <= 0) b = e->default_block;
@@ -121,8 +223,15 @@ int block_for(const KernelEntry* e) {
 
 // Launch one window over `num` systems resident on the current device.
 int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double* y,
-                  DevStats* st, long long num, double t, double tEnd, const DevTol& tol,
+                  DevStats* st, long long num, double t, double tEnd, const DevTol& tol_in,
                   int merge) {
+    DevTol tol = tol_in;
+    tol.powtab = bode::device_powtab();
+    tol.rkc_coef = nullptr;
+    if (e->build_rkc_table != nullptr) {
+        int rc = rkc_table_for(e, tol.kappa, s, &tol.rkc_coef);
+        if (rc) return rc;
+    }
     const int block = block_for(e);
     const long long threads = num * e->lanes;
     const long long grid = (threads + block - 1) / block;
@@ -264,7 +373,34 @@ int for_each_shard(const std::vector<Shard>& shards, F&& f) {
 
 }  // namespace
 
+namespace bode {
+// Device copy of the host libm pow tables on the current device (uploaded
+// once per device), or null when the host pow is not the restated variant.
+const double* device_powtab() {
+    static std::mutex m;
+    static const double* dev[64] = {nullptr};
+    static bool tried[64] = {false};
+    const auto& img = host_powtab();
+    if (img.empty()) return nullptr;
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(m);
+    if (!tried[d]) {
+        tried[d] = true;
+        double* p = nullptr;
+        if (cudaMalloc(&p, img.size() * sizeof(double)) == cudaSuccess &&
+            cudaMemcpy(p, img.data(), img.size() * sizeof(double), cudaMemcpyHostToDevice) ==
+                cudaSuccess)
+            dev[d] = p;
+    }
+    return dev[d];
+}
+}  // namespace bode
+
 extern "C" {
+
+int bode_pow_exact_available(void) { return host_powtab().empty() ? 0 : 1; }
+
 
 const char* bode_version(void) { return "bode 0.1.0 (sm_100a, FP64)"; }
 const char* bode_last_error(void) { return g_last_error.c_str(); }

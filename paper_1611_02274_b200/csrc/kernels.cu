@@ -16,8 +16,8 @@
 
 namespace bode {
 
-template <class P, class R, int L, int SOLVER, bool KSMEM>
-__global__ void __launch_bounds__(kMaxBlock)
+template <class P, class R, int L, int SOLVER, bool KSMEM, int MINB>
+__global__ void __launch_bounds__(kMaxBlock, MINB)
     integrate_kernel(const double* __restrict__ g_soa, double* __restrict__ y_soa,
                      DevStats* __restrict__ stats, long long num, double t, double tEnd,
                      DevTol tol, int merge) {
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kMaxBlock)
 }
 
 // ---- dispatch table ----
-template <class P, class R, int L, int SOLVER, bool KSMEM>
+template <class P, class R, int L, int SOLVER, bool KSMEM, int MINB>
 static KernelEntry make_entry(int kind, int arith) {
     KernelEntry e;
     e.kind = kind;
@@ -64,7 +64,7 @@ static KernelEntry make_entry(int kind, int arith) {
     e.arith = arith;
     e.lanes = L;
     e.smem_per_thread = KSMEM ? kSmemStride<C_of<P, L>()>() * (int)sizeof(double) : 0;
-    e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM>;
+    e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MINB>;
     e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                   const double* g, double* y, DevStats* st, long long num, double t,
                   double tEnd, DevTol tol, int merge) {
@@ -73,12 +73,22 @@ static KernelEntry make_entry(int kind, int arith) {
         k<<<grid, block, smem, s>>>(g, y, st, num, t, tEnd, tol, merge);
     };
     e.default_block = KSMEM ? 128 : 128;
+    e.build_rkc_table = nullptr;
+    if constexpr (SOLVER == 1)
+        e.build_rkc_table = [](double* tab, double kappa, cudaStream_t s) {
+            rkc_coef_table_kernel<R><<<(unsigned)((kRkcTableMaxS + 63) / 64), 64, 0, s>>>(tab, kappa);
+        };
     return e;
 }
 
-#define BODE_BOTH_ARITH(P, L, SOLVER, KSMEM, KIND)                           \
-    make_entry<P, xd, L, SOLVER, KSMEM>(KIND, 0),                            \
-        make_entry<P, double, L, SOLVER, KSMEM>(KIND, 1)
+// MINB = minimum resident 256-thread blocks per SM the register budget must
+// allow (1: up to 255 registers/thread, 2: up to 128).
+#define BODE_BOTH_ARITH_B(P, L, SOLVER, KSMEM, KIND, MINB)                    \
+    make_entry<P, xd, L, SOLVER, KSMEM, MINB>(KIND, 0),                      \
+        make_entry<P, double, L, SOLVER, KSMEM, MINB>(KIND, 1)
+#define BODE_BOTH_ARITH(P, L, SOLVER, KSMEM, KIND) BODE_BOTH_ARITH_B(P, L, SOLVER, KSMEM, KIND, 1)
+
+long long rkc_table_doubles() { return kRkcTableDoubles; }
 
 const KernelEntry* kernel_table(int* count) {
     static const KernelEntry table[] = {
@@ -94,6 +104,7 @@ const KernelEntry* kernel_table(int* count) {
         BODE_BOTH_ARITH(Heat<8>, 1, 0, false, 1),
         // RKC (moderately stiff)
         BODE_BOTH_ARITH(Heat<64>, 4, 1, false, 1),
+        BODE_BOTH_ARITH(Heat<64>, 8, 1, false, 1),
         BODE_BOTH_ARITH(Heat<32>, 4, 1, false, 1),
         BODE_BOTH_ARITH(Heat<16>, 2, 1, false, 1),
         BODE_BOTH_ARITH(Heat<8>, 1, 1, false, 1),

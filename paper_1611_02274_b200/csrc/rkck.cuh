@@ -98,10 +98,10 @@ __device__ __forceinline__ bool rkck_adjust(R h, R err, bool nanFlag, R hMin, R 
     if (err > R(1.0) || !isfinite_(err) || nanFlag) {
         hNew = (!isfinite_(err) || nanFlag)
                    ? R(tol.p1) * h
-                   : fmax_(R(tol.safety) * h * pow_(err, R(tol.pshrnk)), R(tol.p1) * h);
+                   : fmax_(R(tol.safety) * h * pow_(err, R(tol.pshrnk), tol.powtab), R(tol.p1) * h);
         return false;
     }
-    R hn = (err > R(tol.errcon)) ? R(tol.safety) * h * pow_(err, R(tol.pgrow)) : R(5.0) * h;
+    R hn = (err > R(tol.errcon)) ? R(tol.safety) * h * pow_(err, R(tol.pgrow), tol.powtab) : R(5.0) * h;
     hNew = fmax_(hMin, fmin_(hMax, hn));
     return true;
 }

@@ -5,6 +5,7 @@
 
 #include "../../include/bode.h"
 #include "arith.cuh"
+#include "dispatch.h"
 
 namespace {
 
@@ -92,4 +93,34 @@ extern "C" int bode_selftest_fp64_peak(double* flops_per_s, double* seconds) {
     *seconds = best * 1e-3;
     *flops_per_s = flops / (*seconds);
     return BODE_OK;
+}
+
+namespace {
+__global__ void pow_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                           double* __restrict__ out, long long n, const double* T) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = bode::pow_glibc(x[i], y[i], T);
+}
+}  // namespace
+
+extern "C" int bode_selftest_pow(const double* x, const double* y, double* out, int64_t n) {
+    if (n < 1 || !x || !y || !out) return BODE_E_INVALID_SHAPE;
+    int dev = 0;
+    if (cudaGetDeviceCount(&dev) != cudaSuccess || dev < 1) {
+        cudaGetLastError();
+        return BODE_E_NO_DEVICE;
+    }
+    const double* T = bode::device_powtab();
+    double *dx = nullptr, *dy = nullptr, *dz = nullptr;
+    if (cudaMalloc(&dx, n * 8) != cudaSuccess || cudaMalloc(&dy, n * 8) != cudaSuccess ||
+        cudaMalloc(&dz, n * 8) != cudaSuccess)
+        return BODE_E_CUDA;
+    cudaMemcpy(dx, x, n * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(dy, y, n * 8, cudaMemcpyHostToDevice);
+    pow_kernel<<<(unsigned)((n + 255) / 256), 256>>>(dx, dy, dz, n, T);
+    cudaError_t e = cudaMemcpy(out, dz, n * 8, cudaMemcpyDeviceToHost);
+    cudaFree(dx);
+    cudaFree(dy);
+    cudaFree(dz);
+    return e == cudaSuccess ? BODE_OK : BODE_E_CUDA;
 }
