@@ -13,11 +13,26 @@
 #include "dispatch.h"
 #include "rkc.cuh"
 #include "rkck_nystrom.cuh"
+#include "rkck_pleiades2.cuh"
 
 namespace bode {
 
-template <class P, class R, int L, int SOLVER, bool KSMEM, int MINB>
-__global__ void __launch_bounds__(kMaxBlock, MINB)
+// Global component held by lane `lane` of a group in local slot c. Blocks of
+// C consecutive components by default; the 2-lane Pleiades split is by axis:
+// lane l holds positions [7l, 7l+7) and velocities [14+7l, 14+7l+7).
+template <class P, int L>
+__device__ __forceinline__ int comp_index(int lane, int c) {
+    constexpr int C = P::N / L;
+    if constexpr (is_second_order<P>::value && L == 2)
+        return c < 7 ? 7 * lane + c : 14 + 7 * lane + (c - 7);
+    else
+        return lane * C + c;
+}
+
+// MAXREG > 0 caps registers per thread (__maxnreg__) to reach a target
+// occupancy; 0 leaves ptxas the full 255 (launch bound kMaxBlock threads).
+template <class P, class R, int L, int SOLVER, bool KSMEM, int MAXREG>
+__global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
     integrate_kernel(const double* __restrict__ g_soa, double* __restrict__ y_soa,
                      DevStats* __restrict__ stats, long long num, double t, double tEnd,
                      DevTol tol, int merge) {
@@ -30,18 +45,20 @@ __global__ void __launch_bounds__(kMaxBlock, MINB)
     R y[C];
     R g[PP];
 #pragma unroll
-    for (int c = 0; c < C; ++c) y[c] = R(y_soa[sys + num * (long long)(G.lane * C + c)]);
+    for (int c = 0; c < C; ++c) y[c] = R(y_soa[sys + num * (long long)comp_index<P, L>(G.lane, c)]);
 #pragma unroll
     for (int p = 0; p < PP; ++p) g[p] = R(P::P > 0 ? g_soa[sys + num * (long long)p] : 0.0);
     DevStats st;
-    if constexpr (SOLVER == 0 && is_second_order<P>::value)
+    if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 2)
+        rkck_pleiades2_system<R>(G, t, tEnd, y, tol, st);
+    else if constexpr (SOLVER == 0 && is_second_order<P>::value)
         rkck_nystrom_system<P, R>(t, tEnd, y, tol, st);
     else if constexpr (SOLVER == 0)
         rkck_system<P, R, L, KSMEM>(G, t, tEnd, y, g, tol, st);
     else
         rkc_system<P, R, L>(G, t, tEnd, y, g, tol, st);
 #pragma unroll
-    for (int c = 0; c < C; ++c) y_soa[sys + num * (long long)(G.lane * C + c)] = val(y[c]);
+    for (int c = 0; c < C; ++c) y_soa[sys + num * (long long)comp_index<P, L>(G.lane, c)] = val(y[c]);
     if (stats != nullptr && G.lane == 0) {
         if (merge) {
             DevStats o = stats[sys];
@@ -54,7 +71,7 @@ __global__ void __launch_bounds__(kMaxBlock, MINB)
 }
 
 // ---- dispatch table ----
-template <class P, class R, int L, int SOLVER, bool KSMEM, int MINB>
+template <class P, class R, int L, int SOLVER, bool KSMEM, int MAXREG>
 static KernelEntry make_entry(int kind, int arith) {
     KernelEntry e;
     e.kind = kind;
@@ -64,7 +81,7 @@ static KernelEntry make_entry(int kind, int arith) {
     e.arith = arith;
     e.lanes = L;
     e.smem_per_thread = KSMEM ? kSmemStride<C_of<P, L>()>() * (int)sizeof(double) : 0;
-    e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MINB>;
+    e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG>;
     e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                   const double* g, double* y, DevStats* st, long long num, double t,
                   double tEnd, DevTol tol, int merge) {
@@ -81,18 +98,17 @@ static KernelEntry make_entry(int kind, int arith) {
     return e;
 }
 
-// MINB = minimum resident 256-thread blocks per SM the register budget must
-// allow (1: up to 255 registers/thread, 2: up to 128).
-#define BODE_BOTH_ARITH_B(P, L, SOLVER, KSMEM, KIND, MINB)                    \
-    make_entry<P, xd, L, SOLVER, KSMEM, MINB>(KIND, 0),                      \
-        make_entry<P, double, L, SOLVER, KSMEM, MINB>(KIND, 1)
-#define BODE_BOTH_ARITH(P, L, SOLVER, KSMEM, KIND) BODE_BOTH_ARITH_B(P, L, SOLVER, KSMEM, KIND, 1)
+#define BODE_BOTH_ARITH_R(P, L, SOLVER, KSMEM, KIND, MAXREG)                  \
+    make_entry<P, xd, L, SOLVER, KSMEM, MAXREG>(KIND, 0),                    \
+        make_entry<P, double, L, SOLVER, KSMEM, MAXREG>(KIND, 1)
+#define BODE_BOTH_ARITH(P, L, SOLVER, KSMEM, KIND) BODE_BOTH_ARITH_R(P, L, SOLVER, KSMEM, KIND, 0)
 
 long long rkc_table_doubles() { return kRkcTableDoubles; }
 
 const KernelEntry* kernel_table(int* count) {
     static const KernelEntry table[] = {
         // RKCK (nonstiff): Pleiades stages in shared memory, small systems in registers
+        BODE_BOTH_ARITH_R(Pleiades, 2, 0, true, 0, 168),  // 12 warps/SM
         BODE_BOTH_ARITH(Pleiades, 1, 0, true, 0),
         BODE_BOTH_ARITH(ExpDecay, 1, 0, false, 2),
         BODE_BOTH_ARITH(Harmonic, 1, 0, false, 3),

@@ -1,0 +1,237 @@
+// rkck_pleiades2.cuh -- RKCK on the Pleiades problem with each system split
+// across a pair of lanes by axis: lane 0 owns (x_1..x_7, x'_1..x'_7), lane 1
+// owns (y_1..y_7, y'_1..y'_7).
+//
+// Same arithmetic as rkck_nystrom.cuh (and so as rkck.cpp:34-159 with
+// problems.cpp:13-35): the Nystrom storage (f0 = (v, A0), k_j = (V_j, A_j))
+// and the step/error/controller sequence are unchanged; only the work is
+// distributed:
+//   * stage arguments, V_j, yNext and the error-norm terms are per component,
+//     so each lane does its own axis;
+//   * the acceleration needs every position: the lanes swap their 7
+//     positions (shuffles), each computes 1/r^3 for half of the 21 pairs
+//     (interleaved by pair index) and the halves are swapped back;
+//   * each lane then accumulates its own axis over all 21 pairs in the
+//     reference's (i outer, j inner) order -- the x and y accumulators never
+//     mix in the reference either, so every sum is bitwise the reference's;
+//   * r2 = dx*dx + dy*dy is computed by the lane that owns the pair; IEEE
+//     addition is commutative, so (own^2 + other^2) is the reference value;
+//   * the error norm's max is combined across the pair (order-independent),
+//     and both lanes then run the identical scalar controller.
+// Per lane: 21 doubles of state in registers and 4 stage slots of 14 doubles
+// in shared memory (456 B), which lets ~12 warps share an SM instead of 8.
+#pragma once
+
+#include "rkck_nystrom.cuh"
+
+namespace bode {
+
+// pair p = (i, j), i < j, in the reference's loop order
+__host__ __device__ constexpr int pl_pair_i(int p) {
+    return p < 6 ? 0 : p < 11 ? 1 : p < 15 ? 2 : p < 18 ? 3 : p < 20 ? 4 : 5;
+}
+__host__ __device__ constexpr int pl_pair_j(int p) {
+    return p < 6 ? p + 1 : p < 11 ? p - 4 : p < 15 ? p - 8 : p < 18 ? p - 11 : p < 20 ? p - 13 : 6;
+}
+
+// Accelerations of this lane's axis; Q = own-axis positions. Each lane squares
+// its axis' differences for all 21 pairs and swaps them with its partner, so
+// both know r2 = dx*dx + dy*dy (IEEE addition commutes: bitwise the
+// reference's); lane l then evaluates 1/(r2 sqrt r2) for pairs p = 2k + l and
+// the two halves are swapped back. The instruction stream is lane-uniform.
+template <class R>
+__device__ __forceinline__ void pleiades_accel_pair(const Group<2>& G, const R* Q, R (&a)[7]) {
+    double sq[21];
+#pragma unroll
+    for (int p = 0; p < 21; ++p) {
+        const R d = Q[pl_pair_j(p)] - Q[pl_pair_i(p)];
+        sq[p] = val(d * d);
+    }
+    double mine[11];
+#pragma unroll
+    for (int k = 0; k < 11; ++k) {
+        const int p0 = 2 * k, p1 = (2 * k + 1 < 21) ? 2 * k + 1 : 20;
+        const double s0 = __shfl_xor_sync(G.mask, sq[p0], 1);
+        const double s1 = __shfl_xor_sync(G.mask, sq[p1], 1);
+        // lane 0 takes pair p0, lane 1 pair p1 (lane 1 repeats pair 20 at k = 10)
+        const double own = G.lane ? sq[p1] : sq[p0];
+        const double oth = G.lane ? s1 : s0;
+        if constexpr (is_exact<R>::value) {
+            const R r2 = R(own) + R(oth);
+            mine[k] = val(R(1.0) / (r2 * sqrt_(r2)));
+        } else {
+            const double rs = rsqrt_fast(own + oth);
+            mine[k] = rs * rs * rs;
+        }
+    }
+    double other[11];
+#pragma unroll
+    for (int k = 0; k < 11; ++k) other[k] = __shfl_xor_sync(G.mask, mine[k], 1);
+#pragma unroll
+    for (int i = 0; i < 7; ++i) a[i] = R(0.0);
+#pragma unroll
+    for (int p = 0; p < 21; ++p) {
+        const int i = pl_pair_i(p), j = pl_pair_j(p);
+        // pair p was evaluated by lane p & 1 in its round p >> 1
+        const double inv = ((p & 1) == G.lane) ? mine[p >> 1] : other[p >> 1];
+        const R d = Q[j] - Q[i];
+        const double mi = double(i + 1), mj = double(j + 1);
+        if constexpr (is_exact<R>::value) {
+            a[i] += R(mj) * d * R(inv);
+            a[j] -= R(mi) * d * R(inv);
+        } else {
+            const double t = val(d) * inv;
+            a[i] += mj * t;
+            a[j] -= mi * t;
+        }
+    }
+}
+
+template <class R>
+__device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double t_in,
+                                                      double tEnd_in, R (&y)[14],
+                                                      const DevTol& tol, DevStats& st) {
+    constexpr int M = 7;   // components per half (positions or velocities of one axis)
+    constexpr int W = 14;  // doubles per stage slot per lane
+    using namespace ck;
+    stats_init(st);
+    extern __shared__ double bode_smem[];
+    double* const ks = bode_smem + threadIdx.x * kSmemStride<14>();
+    auto kget = [&](int m, int c) -> R { return R(ks[m * W + c]); };
+    auto kset = [&](int m, int c, R v) { ks[m * W + c] = val(v); };
+
+    R* const q = y;      // own-axis positions
+    R* const v = y + M;  // own-axis velocities
+    const R tEnd(tEnd_in);
+    R t(t_in);
+    const R hMax = fabs_(tEnd - t);
+    const R hMin(tol.h_min_floor);
+    R h = R(0.5) * fabs_(tEnd - t);
+    const R uround(tol.uround), eps(tol.eps), tiny(tol.tiny);
+
+    R A0[M];
+    bool haveF = false;
+
+#pragma unroll 1
+    while (tEnd - t > uround * fabs_(tEnd)) {
+        h = fmin_(tEnd - t, h);
+        if (!haveF) {
+            pleiades_accel_pair<R>(G, q, A0);
+            ++st.rhs_evals;
+            haveF = true;
+        }
+        R Q[M], Acc[M];
+        {  // stage 2 (rkck.cpp:42-44)
+            const R hb = h * R(b21);
+#pragma unroll
+            for (int i = 0; i < M; ++i) kset(0, i, v[i] + hb * A0[i]);
+#pragma unroll
+            for (int i = 0; i < M; ++i) Q[i] = q[i] + hb * v[i];
+            pleiades_accel_pair<R>(G, Q, Acc);
+#pragma unroll
+            for (int i = 0; i < M; ++i) kset(0, M + i, Acc[i]);
+        }
+#pragma unroll 1
+        for (int j = 3; j <= 6; ++j) {  // stages 3..6 (rkck.cpp:46-64)
+            const double* bj = c_ck_b[j - 3];
+            const int nk = j - 2;
+            const int out = (j == 6) ? 0 : j - 2;  // k6 reuses k2's slot
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                R s = R(bj[0]) * A0[i];
+#pragma unroll 1
+                for (int m = 0; m < nk; ++m) s = s + R(bj[m + 1]) * kget(m, M + i);
+                Acc[i] = v[i] + h * s;
+            }
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                R s = R(bj[0]) * v[i];
+#pragma unroll 1
+                for (int m = 0; m < nk; ++m) s = s + R(bj[m + 1]) * kget(m, i);
+                Q[i] = q[i] + h * s;
+            }
+#pragma unroll
+            for (int i = 0; i < M; ++i) kset(out, i, Acc[i]);
+            pleiades_accel_pair<R>(G, Q, Acc);
+#pragma unroll
+            for (int i = 0; i < M; ++i) kset(out, M + i, Acc[i]);
+        }
+        st.rhs_evals += 5;
+        st.stages_total += 6;
+
+        // error norm (rkck.cpp:75-76, :88-98), own components, then across the pair
+        R err;
+        bool nanFlag = false;
+        {
+            QuotMax qm;
+            double fm = 0.0;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const R eq = h * (R(d1) * v[i] + R(d3) * kget(1, i) + R(d4) * kget(2, i) +
+                                  R(d5) * kget(3, i) + R(d6) * kget(0, i));
+                const R ev = h * (R(d1) * A0[i] + R(d3) * kget(1, M + i) +
+                                  R(d4) * kget(2, M + i) + R(d5) * kget(3, M + i) +
+                                  R(d6) * kget(0, M + i));
+                if (!isfinite_(eq) || !isfinite_(ev)) nanFlag = true;
+                const R dq = fabs_(q[i]) + fabs_(h * v[i]) + tiny;
+                const R dv = fabs_(v[i]) + fabs_(h * A0[i]) + tiny;
+                if constexpr (is_exact<R>::value) {
+                    qm.push(fabs(val(eq)), val(dq));
+                    qm.push(fabs(val(ev)), val(dv));
+                } else {
+                    fm = fmax(fm, fabs(val(eq)) * rcp_fast(val(dq)));
+                    fm = fmax(fm, fabs(val(ev)) * rcp_fast(val(dv)));
+                }
+            }
+            nanFlag = G.any(nanFlag);
+            if constexpr (is_exact<R>::value) {
+                qm.push(__shfl_xor_sync(G.mask, qm.a, 1), __shfl_xor_sync(G.mask, qm.b, 1));
+                err = R(qm.value());
+            } else {
+                err = R(G.max_all(fm));
+            }
+        }
+        err = err / eps;
+
+        R hNew;
+        bool accepted;
+        if constexpr (is_exact<R>::value) {
+            accepted = rkck_adjust(h, err, nanFlag, hMin, hMax, tol, hNew);
+        } else {
+            if (err > 1.0 || !isfinite(err) || nanFlag) {
+                accepted = false;
+                hNew = (!isfinite(err) || nanFlag)
+                           ? tol.p1 * h
+                           : fmax(tol.safety * h * pow_fast(err, tol.pshrnk), tol.p1 * h);
+            } else {
+                accepted = true;
+                const double hn =
+                    (err > tol.errcon) ? tol.safety * h * pow_fast(err, tol.pgrow) : 5.0 * h;
+                hNew = fmax(val(hMin), fmin(val(hMax), hn));
+            }
+        }
+        if (accepted) {
+            t += h;
+            stats_accept(st, val(h));
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+                q[i] = q[i] + h * (R(c1) * v[i] + R(c3) * kget(1, i) + R(c4) * kget(2, i) +
+                                   R(c6) * kget(0, i));
+#pragma unroll
+            for (int i = 0; i < M; ++i)
+                v[i] = v[i] + h * (R(c1) * A0[i] + R(c3) * kget(1, M + i) +
+                                   R(c4) * kget(2, M + i) + R(c6) * kget(0, M + i));
+            haveF = false;
+            h = hNew;
+        } else {
+            ++st.steps_rejected;
+            if (hNew < R(tol.h_min_floor)) {
+                st.underflow = 1;
+                break;
+            }
+            h = hNew;
+        }
+    }
+}
+
+}  // namespace bode

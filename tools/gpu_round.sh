@@ -15,7 +15,7 @@ for p in $PARTS; do
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1; echo "smoke rc=$?" >> $OUT/status.txt ;;
     bench) timeout 900 python bench.py > $OUT/bench.txt 2>&1; echo "bench rc=$?" >> $OUT/status.txt ;;
     ab_lanes)
-      for L in 4 8; do BODE_LANES=$L timeout 600 python bench.py --no-e2e --no-cpu --num 65536 --steps 3 --rkc-num 1048576 > $OUT/bench_lanes$L.txt 2>&1; done
+      for L in 1 2 8; do BODE_LANES=$L timeout 600 python bench.py --no-e2e --no-cpu --steps 5 > $OUT/bench_lanes$L.txt 2>&1; done
       echo "ab_lanes rc=$?" >> $OUT/status.txt ;;
     bench_exact) timeout 900 python bench.py --arith exact --no-cpu > $OUT/bench_exact.txt 2>&1; echo "bench_exact rc=$?" >> $OUT/status.txt ;;
     ncu)
