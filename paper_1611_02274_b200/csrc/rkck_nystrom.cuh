@@ -94,23 +94,28 @@ __device__ __forceinline__ void rkck_nystrom_system(double t_in, double tEnd_in,
         // ---- stages 3..6 (rkck.cpp:46-64): arg = y + h*(b_j1 f0 + b_j2 k2 + ...)
 #pragma unroll 1
         for (int j = 3; j <= 6; ++j) {
-            const double* bj = c_ck_b[j - 3];
+            const double b0 = c_ck_b[j - 3][0];
+            double bm[4];  // b_j2..b_j5 (zero past the stage's last term)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) bm[m] = c_ck_b[j - 3][m + 1];
             const int nk = j - 2;                 // k2..k_{j-1} enter this stage
             const int out = (j == 6) ? 0 : j - 2;  // k6 reuses k2's slot
             // velocity half of k_j (= of arg_j); the sums run in the
             // reference's left-to-right order
 #pragma unroll
             for (int i = 0; i < M; ++i) {
-                R s = R(bj[0]) * A0[i];
-#pragma unroll 1
-                for (int m = 0; m < nk; ++m) s = s + R(bj[m + 1]) * kget(m, M + i);
+                R s = R(b0) * A0[i];
+#pragma unroll
+                for (int m = 0; m < 4; ++m)  // predicated: constant offsets, no loop
+                    if (m < nk) s = s + R(bm[m]) * kget(m, M + i);
                 Acc[i] = v[i] + h * s;
             }
 #pragma unroll
             for (int i = 0; i < M; ++i) {
-                R s = R(bj[0]) * v[i];
-#pragma unroll 1
-                for (int m = 0; m < nk; ++m) s = s + R(bj[m + 1]) * kget(m, i);
+                R s = R(b0) * v[i];
+#pragma unroll
+                for (int m = 0; m < 4; ++m)
+                    if (m < nk) s = s + R(bm[m]) * kget(m, i);
                 Q[i] = q[i] + h * s;
             }
             BODE_FENCE();

@@ -51,8 +51,8 @@ __device__ __forceinline__ void pleiades_accel_pair(const Group<2>& G, const R* 
 #pragma unroll
     for (int k = 0; k < 11; ++k) {
         const int p0 = 2 * k, p1 = (2 * k + 1 < 21) ? 2 * k + 1 : 20;
-        const double s0 = __shfl_xor_sync(G.mask, sq[p0], 1);
-        const double s1 = __shfl_xor_sync(G.mask, sq[p1], 1);
+        const double s0 = __shfl_xor_sync(0xffffffffu, sq[p0], 1);
+        const double s1 = __shfl_xor_sync(0xffffffffu, sq[p1], 1);
         // lane 0 takes pair p0, lane 1 pair p1 (lane 1 repeats pair 20 at k = 10)
         const double own = G.lane ? sq[p1] : sq[p0];
         const double oth = G.lane ? s1 : s0;
@@ -66,7 +66,7 @@ __device__ __forceinline__ void pleiades_accel_pair(const Group<2>& G, const R* 
     }
     double other[11];
 #pragma unroll
-    for (int k = 0; k < 11; ++k) other[k] = __shfl_xor_sync(G.mask, mine[k], 1);
+    for (int k = 0; k < 11; ++k) other[k] = __shfl_xor_sync(0xffffffffu, mine[k], 1);
 #pragma unroll
     for (int i = 0; i < 7; ++i) a[i] = R(0.0);
 #pragma unroll
@@ -111,14 +111,24 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
 
     R A0[M];
     bool haveF = false;
+    bool live = tEnd - t > uround * fabs_(tEnd);  // rkck.cpp:131
 
+    // Warp-uniform loop: the warp iterates while any of its systems is live,
+    // so every shuffle runs with the full mask (no collective fix-up code).
+    // Finished systems ride along with their state and stats frozen -- the
+    // SIMT cost is the same as the divergent loop's masked iterations.
 #pragma unroll 1
-    while (tEnd - t > uround * fabs_(tEnd)) {
-        h = fmin_(tEnd - t, h);
-        if (!haveF) {
-            pleiades_accel_pair<R>(G, q, A0);
-            ++st.rhs_evals;
-            haveF = true;
+    while (__any_sync(0xffffffffu, live)) {
+        if (live) h = fmin_(tEnd - t, h);
+        if (__any_sync(0xffffffffu, live && !haveF)) {  // rkck.cpp:133-137
+            R Af[M];
+            pleiades_accel_pair<R>(G, q, Af);
+            if (live && !haveF) {
+#pragma unroll
+                for (int i = 0; i < M; ++i) A0[i] = Af[i];
+                ++st.rhs_evals;
+                haveF = true;
+            }
         }
         R Q[M], Acc[M];
         {  // stage 2 (rkck.cpp:42-44)
@@ -133,21 +143,26 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
         }
 #pragma unroll 1
         for (int j = 3; j <= 6; ++j) {  // stages 3..6 (rkck.cpp:46-64)
-            const double* bj = c_ck_b[j - 3];
+            const double b0 = c_ck_b[j - 3][0];
+            double bm[4];  // b_j2..b_j5 (zero past the stage's last term)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) bm[m] = c_ck_b[j - 3][m + 1];
             const int nk = j - 2;
             const int out = (j == 6) ? 0 : j - 2;  // k6 reuses k2's slot
 #pragma unroll
             for (int i = 0; i < M; ++i) {
-                R s = R(bj[0]) * A0[i];
-#pragma unroll 1
-                for (int m = 0; m < nk; ++m) s = s + R(bj[m + 1]) * kget(m, M + i);
+                R s = R(b0) * A0[i];
+#pragma unroll
+                for (int m = 0; m < 4; ++m)  // predicated: constant offsets, no loop
+                    if (m < nk) s = s + R(bm[m]) * kget(m, M + i);
                 Acc[i] = v[i] + h * s;
             }
 #pragma unroll
             for (int i = 0; i < M; ++i) {
-                R s = R(bj[0]) * v[i];
-#pragma unroll 1
-                for (int m = 0; m < nk; ++m) s = s + R(bj[m + 1]) * kget(m, i);
+                R s = R(b0) * v[i];
+#pragma unroll
+                for (int m = 0; m < 4; ++m)
+                    if (m < nk) s = s + R(bm[m]) * kget(m, i);
                 Q[i] = q[i] + h * s;
             }
 #pragma unroll
@@ -156,8 +171,10 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
 #pragma unroll
             for (int i = 0; i < M; ++i) kset(out, M + i, Acc[i]);
         }
-        st.rhs_evals += 5;
-        st.stages_total += 6;
+        if (live) {
+            st.rhs_evals += 5;
+            st.stages_total += 6;
+        }
 
         // error norm (rkck.cpp:75-76, :88-98), own components, then across the pair
         R err;
@@ -183,12 +200,12 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
                     fm = fmax(fm, fabs(val(ev)) * rcp_fast(val(dv)));
                 }
             }
-            nanFlag = G.any(nanFlag);
+            nanFlag = (__ballot_sync(0xffffffffu, nanFlag) & G.mask) != 0u;
             if constexpr (is_exact<R>::value) {
-                qm.push(__shfl_xor_sync(G.mask, qm.a, 1), __shfl_xor_sync(G.mask, qm.b, 1));
+                qm.push(__shfl_xor_sync(0xffffffffu, qm.a, 1), __shfl_xor_sync(0xffffffffu, qm.b, 1));
                 err = R(qm.value());
             } else {
-                err = R(G.max_all(fm));
+                err = R(fmax(fm, __shfl_xor_sync(0xffffffffu, fm, 1)));
             }
         }
         err = err / eps;
@@ -210,7 +227,7 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
                 hNew = fmax(val(hMin), fmin(val(hMax), hn));
             }
         }
-        if (accepted) {
+        if (live && accepted) {
             t += h;
             stats_accept(st, val(h));
 #pragma unroll
@@ -223,14 +240,15 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
                                    R(c4) * kget(2, M + i) + R(c6) * kget(0, M + i));
             haveF = false;
             h = hNew;
-        } else {
+        } else if (live) {
             ++st.steps_rejected;
-            if (hNew < R(tol.h_min_floor)) {
+            if (hNew < R(tol.h_min_floor)) {  // freeze at the last accepted state
                 st.underflow = 1;
-                break;
+                live = false;
             }
             h = hNew;
         }
+        if (live) live = tEnd - t > uround * fabs_(tEnd);
     }
 }
 
