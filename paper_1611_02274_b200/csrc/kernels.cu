@@ -108,8 +108,8 @@ long long rkc_table_doubles() { return kRkcTableDoubles; }
 const KernelEntry* kernel_table(int* count) {
     static const KernelEntry table[] = {
         // RKCK (nonstiff): Pleiades stages in shared memory, small systems in registers
-        BODE_BOTH_ARITH_R(Pleiades, 2, 0, true, 0, 168),  // 12 warps/SM
         BODE_BOTH_ARITH(Pleiades, 1, 0, true, 0),
+        BODE_BOTH_ARITH_R(Pleiades, 2, 0, true, 0, 168),  // axis split, 12 warps/SM
         BODE_BOTH_ARITH(ExpDecay, 1, 0, false, 2),
         BODE_BOTH_ARITH(Harmonic, 1, 0, false, 3),
         BODE_BOTH_ARITH(Zero<2>, 1, 0, false, 4),

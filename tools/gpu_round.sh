@@ -17,6 +17,11 @@ for p in $PARTS; do
     ab_lanes)
       for L in 1 2 8; do BODE_LANES=$L timeout 600 python bench.py --no-e2e --no-cpu --steps 5 > $OUT/bench_lanes$L.txt 2>&1; done
       echo "ab_lanes rc=$?" >> $OUT/status.txt ;;
+    ncu_exact)
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:integrate \
+        -s 1 -c 1 -o $OUT/prof_rkck_exact python bench.py --arith exact --steps 1 --warmup 1 --num 262144 \
+        --rkc-num 0 --no-e2e --no-cpu > $OUT/ncu_full_rkck_exact.txt 2>&1
+      echo "ncu_exact rc=$?" >> $OUT/status.txt ;;
     bench_exact) timeout 900 python bench.py --arith exact --no-cpu > $OUT/bench_exact.txt 2>&1; echo "bench_exact rc=$?" >> $OUT/status.txt ;;
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
