@@ -102,6 +102,7 @@ def lib():
         "bode_selftest_fp64_peak": (ctypes.c_int, [PD, PD]),
         "bode_selftest_pow": (ctypes.c_int, [PD, PD, PD, c_i64]),
         "bode_pow_exact_available": (ctypes.c_int, []),
+        "bode_selftest_exact_math": (ctypes.c_int, [PD, c_i64, c_i32, P(c_i64), P(c_i64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

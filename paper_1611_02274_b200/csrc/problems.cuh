@@ -94,24 +94,52 @@ struct Pleiades {
     // half of the reference RHS, accumulated in the reference's order.
     template <class R>
     __device__ __forceinline__ static void accel(const R* w, R* a) {
+        // EXACT: 1/(r2 sqrt(r2)) for all pairs first, straight-line (arith.cuh
+        // sqrt_rn_bf / rcp_rn_bf), with one cold fallback to the intrinsics
+        double inv[21];
+        if constexpr (is_exact<R>::value) {
+            bool ok = true;
+#pragma unroll
+            for (int p = 0, i = 0; i < 7; ++i)
+#pragma unroll
+                for (int j = i + 1; j < 7; ++j, ++p) {
+                    const R dx = w[j] - w[i];
+                    const R dy = w[7 + j] - w[7 + i];
+                    const double r2 = val(dx * dx + dy * dy);
+                    const double d = __dmul_rn(r2, sqrt_rn_bf(r2));
+                    ok = ok && in_safe_range(r2) && in_safe_range(d);
+                    inv[p] = rcp_rn_bf(d);
+                }
+            if (!ok) {  // rare: some operand outside [2^-400, 2^400] (or NaN/Inf)
+#pragma unroll
+                for (int p = 0, i = 0; i < 7; ++i)
+#pragma unroll
+                    for (int j = i + 1; j < 7; ++j, ++p) {
+                        const R dx = w[j] - w[i];
+                        const R dy = w[7 + j] - w[7 + i];
+                        const R r2 = dx * dx + dy * dy;
+                        inv[p] = val(R(1.0) / (r2 * sqrt_(r2)));
+                    }
+            }
+        }
 #pragma unroll
         for (int i = 0; i < 14; ++i) a[i] = R(0.0);
 #pragma unroll
-        for (int i = 0; i < 7; ++i) {
+        for (int p = 0, i = 0; i < 7; ++i) {
 #pragma unroll
-            for (int j = i + 1; j < 7; ++j) {
+            for (int j = i + 1; j < 7; ++j, ++p) {
                 const R dx = w[j] - w[i];
                 const R dy = w[7 + j] - w[7 + i];
-                const R r2 = dx * dx + dy * dy;
                 const double mi = double(i + 1);
                 const double mj = double(j + 1);
                 if constexpr (is_exact<R>::value) {
-                    const R invR3 = R(1.0) / (r2 * sqrt_(r2));
+                    const R invR3(inv[p]);
                     a[i] += R(mj) * dx * invR3;
                     a[7 + i] += R(mj) * dy * invR3;
                     a[j] -= R(mi) * dx * invR3;
                     a[7 + j] -= R(mi) * dy * invR3;
                 } else {
+                    const R r2 = dx * dx + dy * dy;
                     const double rs = rsqrt_fast(val(r2));
                     const double invR3 = rs * rs * rs;
                     const double ax = val(dx) * invR3;

@@ -47,7 +47,8 @@ __device__ __forceinline__ void pleiades_accel_pair(const Group<2>& G, const R* 
         const R d = Q[pl_pair_j(p)] - Q[pl_pair_i(p)];
         sq[p] = val(d * d);
     }
-    double mine[11];
+    double mine[11], r2s[11];
+    bool ok = true;
 #pragma unroll
     for (int k = 0; k < 11; ++k) {
         const int p0 = 2 * k, p1 = (2 * k + 1 < 21) ? 2 * k + 1 : 20;
@@ -56,12 +57,22 @@ __device__ __forceinline__ void pleiades_accel_pair(const Group<2>& G, const R* 
         // lane 0 takes pair p0, lane 1 pair p1 (lane 1 repeats pair 20 at k = 10)
         const double own = G.lane ? sq[p1] : sq[p0];
         const double oth = G.lane ? s1 : s0;
-        if constexpr (is_exact<R>::value) {
-            const R r2 = R(own) + R(oth);
-            mine[k] = val(R(1.0) / (r2 * sqrt_(r2)));
+        if constexpr (is_exact<R>::value) {  // straight-line IEEE ops (arith.cuh)
+            const double r2 = __dadd_rn(own, oth);
+            const double d = __dmul_rn(r2, sqrt_rn_bf(r2));
+            ok = ok && in_safe_range(r2) && in_safe_range(d);
+            r2s[k] = r2;
+            mine[k] = rcp_rn_bf(d);
         } else {
             const double rs = rsqrt_fast(own + oth);
             mine[k] = rs * rs * rs;
+        }
+    }
+    if constexpr (is_exact<R>::value) {
+        if (!ok) {  // rare: an operand outside [2^-400, 2^400] (or NaN/Inf)
+#pragma unroll
+            for (int k = 0; k < 11; ++k)
+                mine[k] = __ddiv_rn(1.0, __dmul_rn(r2s[k], __dsqrt_rn(r2s[k])));
         }
     }
     double other[11];

@@ -124,3 +124,47 @@ extern "C" int bode_selftest_pow(const double* x, const double* y, double* out, 
     cudaFree(dz);
     return e == cudaSuccess ? BODE_OK : BODE_E_CUDA;
 }
+
+namespace {
+__global__ void exact_math_kernel(const double* __restrict__ x, long long n, int op,
+                                  unsigned long long* __restrict__ bad,
+                                  unsigned long long* __restrict__ first_bad) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double v = x[i];
+    if (!bode::in_safe_range(v)) return;
+    const double got = op == 0 ? bode::sqrt_rn_bf(v) : bode::rcp_rn_bf(v);
+    const double ref = op == 0 ? __dsqrt_rn(v) : __drcp_rn(v);
+    if (__double_as_longlong(got) != __double_as_longlong(ref)) {
+        atomicAdd(bad, 1ull);
+        atomicMin(first_bad, (unsigned long long)i);
+    }
+}
+}  // namespace
+
+// Diagnostics: counts the in-range inputs where the branch-free sqrt (op 0)
+// or reciprocal (op 1) differs from __dsqrt_rn / __drcp_rn.
+extern "C" int bode_selftest_exact_math(const double* x, int64_t n, int32_t op,
+                                        int64_t* mismatches, int64_t* first) {
+    if (n < 1 || !x || !mismatches) return BODE_E_INVALID_SHAPE;
+    int dev = 0;
+    if (cudaGetDeviceCount(&dev) != cudaSuccess || dev < 1) {
+        cudaGetLastError();
+        return BODE_E_NO_DEVICE;
+    }
+    double* dx = nullptr;
+    unsigned long long* db = nullptr;
+    if (cudaMalloc(&dx, n * 8) != cudaSuccess || cudaMalloc(&db, 16) != cudaSuccess)
+        return BODE_E_CUDA;
+    cudaMemcpy(dx, x, n * 8, cudaMemcpyHostToDevice);
+    unsigned long long init[2] = {0ull, ~0ull};
+    cudaMemcpy(db, init, 16, cudaMemcpyHostToDevice);
+    exact_math_kernel<<<(unsigned)((n + 255) / 256), 256>>>(dx, n, op, db, db + 1);
+    unsigned long long res[2];
+    cudaError_t e = cudaMemcpy(res, db, 16, cudaMemcpyDeviceToHost);
+    cudaFree(dx);
+    cudaFree(db);
+    *mismatches = (int64_t)res[0];
+    if (first) *first = res[0] ? (int64_t)res[1] : -1;
+    return e == cudaSuccess ? BODE_OK : BODE_E_CUDA;
+}
