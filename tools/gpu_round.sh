@@ -22,6 +22,10 @@ for p in $PARTS; do
         -s 1 -c 1 -o $OUT/prof_rkck_exact python bench.py --arith exact --steps 1 --warmup 1 --num 262144 \
         --rkc-num 0 --no-e2e --no-cpu > $OUT/ncu_full_rkck_exact.txt 2>&1
       echo "ncu_exact rc=$?" >> $OUT/status.txt ;;
+    diverge)
+      timeout 600 python tools/divergence.py --problem pleiades > $OUT/diverge_pleiades.txt 2>&1
+      timeout 600 python tools/divergence.py --problem heat --num 262144 --arith exact > $OUT/diverge_heat.txt 2>&1
+      echo "diverge rc=$?" >> $OUT/status.txt ;;
     bench_exact) timeout 900 python bench.py --arith exact --no-cpu > $OUT/bench_exact.txt 2>&1; echo "bench_exact rc=$?" >> $OUT/status.txt ;;
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
