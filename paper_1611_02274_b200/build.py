@@ -75,7 +75,24 @@ def build(force: bool = False, verbose: bool = True) -> str:
             raise RuntimeError(f"link failed:\n{r.stderr}")
         if verbose:
             print(f"[bode build] linked {SO}", flush=True)
+    build_examples(verbose)
     return SO
+
+
+def build_examples(verbose: bool = True):
+    """C++ drop-in example (examples/*.cpp) linked against libbode.so."""
+    repo = os.path.dirname(PKG)
+    for src in glob.glob(os.path.join(repo, "examples", "*.cpp")):
+        exe = os.path.join(LIB_DIR, os.path.splitext(os.path.basename(src))[0])
+        if not _stale(exe, [src, SO, os.path.join(INCLUDE, "bode.hpp")]):
+            continue
+        cmd = ["g++", "-std=c++17", "-O2", "-I", INCLUDE, src, "-L", LIB_DIR, "-lbode",
+               f"-Wl,-rpath,{LIB_DIR}", "-Wl,-rpath,$ORIGIN", "-o", exe]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"example build failed for {src}:\n{r.stderr}")
+        if verbose:
+            print(f"[bode build] built {exe}", flush=True)
 
 
 if __name__ == "__main__":

@@ -108,8 +108,13 @@ long long rkc_table_doubles() { return kRkcTableDoubles; }
 const KernelEntry* kernel_table(int* count) {
     static const KernelEntry table[] = {
         // RKCK (nonstiff): Pleiades stages in shared memory, small systems in registers
-        BODE_BOTH_ARITH(Pleiades, 1, 0, true, 0),
-        BODE_BOTH_ARITH_R(Pleiades, 2, 0, true, 0, 168),  // axis split, 12 warps/SM
+        // Pleiades: FAST defaults to one lane per system (255 registers, 8 warps/SM);
+        // EXACT to the axis split (168 registers, 12 warps/SM) -- the straight-line
+        // IEEE sqrt/reciprocal need more registers than one lane can spare
+        make_entry<Pleiades, double, 1, 0, true, 0>(0, 1),
+        make_entry<Pleiades, xd, 2, 0, true, 168>(0, 0),
+        make_entry<Pleiades, double, 2, 0, true, 168>(0, 1),
+        make_entry<Pleiades, xd, 1, 0, true, 0>(0, 0),
         BODE_BOTH_ARITH(ExpDecay, 1, 0, false, 2),
         BODE_BOTH_ARITH(Harmonic, 1, 0, false, 3),
         BODE_BOTH_ARITH(Zero<2>, 1, 0, false, 4),
