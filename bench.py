@@ -207,7 +207,9 @@ def main():
     ap.add_argument("--impl", default="bode", choices=["bode", "reference"])
     ap.add_argument("--num", type=int, default=1 << 22, help="systems per GPU")
     ap.add_argument("--arith", default="fast", choices=["fast", "exact"])
-    ap.add_argument("--rkc-num", type=int, default=1 << 20)
+    ap.add_argument("--rkc-num", type=int, default=1 << 22)
+    ap.add_argument("--no-secondary", dest="secondary", action="store_false",
+                    help="skip the EXACT / RKC measurements")
     ap.add_argument("--cpu-sample", type=int, default=1 << 15)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -226,6 +228,7 @@ def main():
     import paper_1611_02274_b200 as P
     from paper_1611_02274_b200 import _abi as A
     from golden_cases import PLEIADES_IC, heat_ic, perturb
+    from paper_1611_02274_b200.api import stiffness_params
 
     torch.cuda.set_device(local)
     dist = None
@@ -287,18 +290,41 @@ def main():
                "h2d_bytes_per_step": num * 28 * 8, "d2h_bytes_per_step": num * (28 * 8 + 64),
                "ms_per_step": e2e_s / args.steps * 1e3, "pinned_host": True}
 
-    # ---- secondary: RKC heat64 (config 3) on this GPU ----
-    rkc = None
-    if args.rkc_num > 0:
-        yh0 = perturb(heat_ic(64), 0.01, 42 + rank, args.rkc_num)
-        s2, per2, st2, l2, _ = measure_device(P, A, torch, "heat", "rkc", "exact", 64, yh0, None,
-                                              min(args.steps, 10), 1, stream)
-        f2 = algorithmic_flops("heat", "rkc", 64, st2, min(args.steps, 10))
-        rkc = {"workload": f"RKC heat n=64, {args.rkc_num} systems, exact arithmetic",
-               "value": args.rkc_num * min(args.steps, 10) / s2, "unit": UNIT,
-               "ms_per_step": s2 / min(args.steps, 10) * 1e3,
-               "achieved_tflops": f2 / s2 / 1e12, "frac_of_fp64_peak": f2 / s2 / peak.value,
-               "flop_per_system_window": f2 / (args.rkc_num * min(args.steps, 10))}
+    def secondary(problem, solver, arith, dim, y0s, g0s, label, steps):
+        sec, perw, sts, _, _ = measure_device(P, A, torch, problem, solver, arith, dim, y0s, g0s,
+                                               steps, 1, stream)
+        f = algorithmic_flops(problem, solver, dim, sts, steps)
+        n = y0s.size // dim
+        return {"workload": label, "value": world * n * steps / secs_max(sec),
+                "unit": UNIT, "ms_per_step": sec / steps * 1e3,
+                "achieved_tflops": f / sec / 1e12, "frac_of_fp64_peak": f / sec / peak.value,
+                "flop_per_system_window": f / (n * steps),
+                "kernel_ms_per_window": [round(x, 4) for x in perw]}
+
+    def secs_max(sec):
+        if not dist:
+            return sec
+        tt = torch.tensor([sec], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    extra = {}
+    if args.secondary:
+        extra["rkck_exact"] = secondary(
+            "pleiades", "rkck", "exact", 28, y0, None,
+            f"RKCK Pleiades, {num} systems, EXACT policy (bitwise reference arithmetic)",
+            args.steps)
+        if args.rkc_num > 0:
+            yh0 = perturb(heat_ic(64), 0.01, 42 + rank, args.rkc_num)
+            extra["rkc_heat64"] = secondary(
+                "heat", "rkc", "exact", 64, yh0, None,
+                f"RKC heat n=64 (config 3), {args.rkc_num} systems, EXACT", min(args.steps, 10))
+            ye0 = perturb(np.array([1.0]), 0.01, 42 + rank, args.rkc_num)
+            g0 = stiffness_params(args.rkc_num)
+            extra["rkc_stiff_expdecay"] = secondary(
+                "expdecay", "rkc", "exact", 1, ye0, g0,
+                f"RKC expDecay, g0 log-uniform in [1,1e4] (config 4), {args.rkc_num} systems, EXACT",
+                min(args.steps, 10))
 
     if rank != 0:
         if dist:
@@ -329,7 +355,8 @@ def main():
                      "flop_per_system_window": flops / (num * args.steps),
                      "kernel_ms_per_launch": sum(per) / len(per)},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-        "clocks": clk.summary(), "rkc_heat64": rkc,
+        "clocks": clk.summary(), **extra,
+        "kernel_ms_per_window": [round(x, 4) for x in per],
         "work_per_system_window": {
             "attempts": float((stats["steps_accepted"] + stats["steps_rejected"]).sum()) / (num * args.steps),
             "rhs_evals": float(stats["rhs_evals"].sum()) / (num * args.steps)},
