@@ -93,6 +93,7 @@ def lib():
         "bode_window_end": (c_d, [c_d, c_d, c_d, c_i64]),
         "bode_set_block_size": (ctypes.c_int, [c_i32]),
         "bode_launch_count": (c_i64, []),
+        "bode_set_persistent": (ctypes.c_int, [c_i32]),
         "bode_splitmix64_at": (c_u64, [c_u64, c_u64]),
         "bode_unit_symmetric_at": (c_d, [c_u64, c_u64]),
         "bode_perturb_initial_conditions": (ctypes.c_int, [PD, c_i32, c_d, c_u64, c_i64, PD]),

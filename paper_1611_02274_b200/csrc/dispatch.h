@@ -28,6 +28,11 @@ using LaunchFn = void (*)(const void* fn, dim3 grid, dim3 block, size_t smem, cu
                           const double* g, double* y, DevStats* st, long long num, double t,
                           double tEnd, DevTol tol, int merge);
 
+using LaunchPersistentFn = void (*)(const void* fn, dim3 grid, dim3 block, size_t smem,
+                                    cudaStream_t s, const double* g, double* y, DevStats* st,
+                                    long long num, double t, double tEnd, DevTol tol, int merge,
+                                    unsigned long long* counter);
+
 struct KernelEntry {
     int kind, dim, param_dim, solver, arith;
     int lanes;            // lanes per system (L)
@@ -36,6 +41,10 @@ struct KernelEntry {
     const void* fn;
     LaunchFn launch;
     void (*build_rkc_table)(double* tab, double kappa, cudaStream_t s);  // null for RKCK
+    // persistent variant with dynamic refill (null if none): a grid sized to the
+    // resident capacity whose lanes claim systems from `counter`
+    const void* pfn = nullptr;
+    LaunchPersistentFn launch_persistent = nullptr;
 };
 
 const KernelEntry* kernel_table(int* count);

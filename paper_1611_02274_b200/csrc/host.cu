@@ -35,6 +35,7 @@ using bode::KernelEntry;
 thread_local std::string g_last_error;
 std::atomic<long long> g_launches{0};
 std::atomic<int> g_block_override{0};
+std::atomic<int> g_persistent{1};  // dynamic-refill kernels where compiled
 
 int fail(int code, const std::string& msg) {
     g_last_error = msg;
@@ -215,6 +216,24 @@ int rkc_table_for(const KernelEntry* e, double kappa, cudaStream_t s, const doub
     return BODE_OK;
 }
 
+// Work counters for persistent launches: a per-device ring, zeroed on the
+// launch stream right before use (safe unless > kCounters launches overlap).
+constexpr int kCounters = 256;
+int claim_counter(cudaStream_t s, unsigned long long** out) {
+    static std::mutex m;
+    static unsigned long long* pool[64] = {nullptr};
+    static int next[64] = {0};
+    int dev = 0;
+    BODE_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(m);
+    if (!pool[dev]) BODE_CUDA(cudaMalloc(&pool[dev], kCounters * sizeof(unsigned long long)));
+    unsigned long long* c = pool[dev] + next[dev];
+    next[dev] = (next[dev] + 1) % kCounters;
+    BODE_CUDA(cudaMemsetAsync(c, 0, sizeof(unsigned long long), s));
+    *out = c;
+    return BODE_OK;
+}
+
 int block_for(const KernelEntry* e) {
     int b = g_block_override.load();
     if (b <= 0) b = e->default_block;
@@ -236,13 +255,28 @@ int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double*
     const long long threads = num * e->lanes;
     const long long grid = (threads + block - 1) / block;
     const size_t smem = (size_t)e->smem_per_thread * block;
+    const bool persistent = e->launch_persistent != nullptr && g_persistent.load();
+    const void* fn = persistent ? e->pfn : e->fn;
     if (smem > 48 * 1024) {
         // per-device attribute; idempotent and cheap, so set it on every launch
-        BODE_CUDA(cudaFuncSetAttribute(e->fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        BODE_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
     }
-    e->launch(e->fn, dim3((unsigned)grid), dim3(block), smem, s, g, y, st, num, t, tEnd, tol,
-              merge);
+    if (persistent) {
+        int dev = 0, sms = 0, per_sm = 0;
+        BODE_CUDA(cudaGetDevice(&dev));
+        BODE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        BODE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
+        const long long pgrid = std::max<long long>(1, std::min<long long>(grid, (long long)per_sm * sms));
+        unsigned long long* counter = nullptr;
+        int rc = claim_counter(s, &counter);
+        if (rc) return rc;
+        e->launch_persistent(fn, dim3((unsigned)pgrid), dim3(block), smem, s, g, y, st, num, t,
+                             tEnd, tol, merge, counter);
+    } else {
+        e->launch(fn, dim3((unsigned)grid), dim3(block), smem, s, g, y, st, num, t, tEnd, tol,
+                  merge);
+    }
     g_launches.fetch_add(1);
     BODE_CUDA(cudaGetLastError());
     return BODE_OK;
@@ -488,6 +522,11 @@ int bode_set_block_size(int32_t threads) {
 }
 
 int64_t bode_launch_count(void) { return g_launches.load(); }
+
+int bode_set_persistent(int32_t enable) {
+    g_persistent.store(enable ? 1 : 0);
+    return BODE_OK;
+}
 
 int bode_int_driver_device(const bode_problem_t* p, int32_t solver, int32_t arith, double t,
                            double t_end, int64_t num, const double* g_dev, double* y_dev,

@@ -70,6 +70,15 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
     }
 }
 
+// Persistent-grid RKCK for second-order problems, one lane per system.
+template <class P, class R>
+__global__ void __launch_bounds__(kMaxBlock)
+    persistent_kernel(const double* __restrict__ g_soa, double* __restrict__ y_soa,
+                      DevStats* __restrict__ stats, long long num, double t, double tEnd,
+                      DevTol tol, int merge, unsigned long long* counter) {
+    rkck_nystrom_persistent<P, R>(g_soa, y_soa, stats, num, t, tEnd, tol, merge, counter);
+}
+
 // ---- dispatch table ----
 template <class P, class R, int L, int SOLVER, bool KSMEM, int MAXREG>
 static KernelEntry make_entry(int kind, int arith) {
@@ -91,6 +100,17 @@ static KernelEntry make_entry(int kind, int arith) {
     };
     e.default_block = KSMEM ? 128 : 128;
     e.build_rkc_table = nullptr;
+    if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1) {
+        e.pfn = (const void*)&persistent_kernel<P, R>;
+        e.launch_persistent = [](const void* fn, dim3 grid, dim3 block, size_t smem,
+                                 cudaStream_t s, const double* g, double* y, DevStats* st,
+                                 long long num, double t, double tEnd, DevTol tol, int merge,
+                                 unsigned long long* counter) {
+            auto k = (void (*)(const double*, double*, DevStats*, long long, double, double,
+                               DevTol, int, unsigned long long*))fn;
+            k<<<grid, block, smem, s>>>(g, y, st, num, t, tEnd, tol, merge, counter);
+        };
+    }
     if constexpr (SOLVER == 1)
         e.build_rkc_table = [](double* tab, double kappa, cudaStream_t s) {
             rkc_coef_table_kernel<R><<<(unsigned)((kRkcTableMaxS + 63) / 64), 64, 0, s>>>(tab, kappa);

@@ -44,33 +44,41 @@ __constant__ double c_ck_b[4][5] = {
     {-11.0 / 54.0, 5.0 / 2.0, -70.0 / 27.0, 35.0 / 27.0, 0.0},
     {1631.0 / 55296.0, 175.0 / 512.0, 575.0 / 13824.0, 44275.0 / 110592.0, 253.0 / 4096.0}};
 
+// Per-lane solver state: one system, advanced one attempt at a time, so a
+// persistent kernel can hand a lane a new system as soon as its own finishes.
 template <class P, class R>
-__device__ __forceinline__ void rkck_nystrom_system(double t_in, double tEnd_in,
-                                                    R (&y)[P::N], const DevTol& tol,
-                                                    DevStats& st) {
-    constexpr int M = P::N / 2;
-    using namespace ck;
-    stats_init(st);
-    extern __shared__ double bode_smem[];
-    double* const ks = bode_smem + threadIdx.x * kSmemStride<P::N>();
-    // slot m holds k_{m+2} (slot 0 holds k6 after stage 6): V at [0, M), A at [M, 2M)
-    auto kget = [&](int m, int c) -> R { return R(ks[m * P::N + c]); };
-    auto kset = [&](int m, int c, R v) { ks[m * P::N + c] = val(v); };
+struct NystromRkck {
+    static constexpr int M = P::N / 2;
+    R y[P::N];  // (q, v)
+    R A0[M];    // acceleration half of f0 = f(t, y)
+    R t, tEnd, hMax, h;
+    bool haveF, live;
+    DevStats st;
+    double* ks;  // this lane's shared-memory row (k2..k5 / k6)
 
-    R* const q = y;      // y[0..M)
-    R* const v = y + M;  // y[M..2M)
-    const R tEnd(tEnd_in);
-    R t(t_in);
-    const R hMax = fabs_(tEnd - t);
-    const R hMin(tol.h_min_floor);
-    R h = R(0.5) * fabs_(tEnd - t);
-    const R uround(tol.uround), eps(tol.eps), tiny(tol.tiny);
+    __device__ __forceinline__ R kget(int m, int c) const { return R(ks[m * P::N + c]); }
+    __device__ __forceinline__ void kset(int m, int c, R v) { ks[m * P::N + c] = val(v); }
 
-    R A0[M];  // acceleration half of f0 = f(t, y)
-    bool haveF = false;
+    // rkck::driver prologue (rkck.cpp:119-128); y must already hold the state
+    __device__ __forceinline__ void start(double t_in, double tEnd_in, const DevTol& tol) {
+        extern __shared__ double bode_smem[];
+        ks = bode_smem + threadIdx.x * kSmemStride<P::N>();
+        stats_init(st);
+        tEnd = R(tEnd_in);
+        t = R(t_in);
+        hMax = fabs_(tEnd - t);
+        h = R(0.5) * fabs_(tEnd - t);
+        haveF = false;
+        live = tEnd - t > R(tol.uround) * fabs_(tEnd);  // rkck.cpp:131
+    }
 
-#pragma unroll 1
-    while (tEnd - t > uround * fabs_(tEnd)) {
+    // one pass of the while loop of rkck.cpp:131-157
+    __device__ __forceinline__ void attempt(const DevTol& tol) {
+        using namespace ck;
+        R* const q = y;
+        R* const v = y + M;
+        const R hMin(tol.h_min_floor);
+        const R uround(tol.uround), eps(tol.eps), tiny(tol.tiny);
         h = fmin_(tEnd - t, h);
         if (!haveF) {  // rejected retries reuse f(t, y) (rkck.cpp:133-137)
             P::template accel<R>(q, A0);
@@ -78,8 +86,7 @@ __device__ __forceinline__ void rkck_nystrom_system(double t_in, double tEnd_in,
             haveF = true;
         }
         R Q[M], Acc[M];
-        // ---- stage 2: arg = y + h*b21*f0 (rkck.cpp:42-44) ----
-        {
+        {  // stage 2: arg = y + h*b21*f0 (rkck.cpp:42-44)
             const R hb = h * R(b21);
 #pragma unroll
             for (int i = 0; i < M; ++i) kset(0, i, v[i] + hb * A0[i]);
@@ -91,17 +98,15 @@ __device__ __forceinline__ void rkck_nystrom_system(double t_in, double tEnd_in,
             for (int i = 0; i < M; ++i) kset(0, M + i, Acc[i]);
             BODE_FENCE();
         }
-        // ---- stages 3..6 (rkck.cpp:46-64): arg = y + h*(b_j1 f0 + b_j2 k2 + ...)
+        // stages 3..6 (rkck.cpp:46-64): arg = y + h*(b_j1 f0 + b_j2 k2 + ...)
 #pragma unroll 1
         for (int j = 3; j <= 6; ++j) {
             const double b0 = c_ck_b[j - 3][0];
             double bm[4];  // b_j2..b_j5 (zero past the stage's last term)
 #pragma unroll
             for (int m = 0; m < 4; ++m) bm[m] = c_ck_b[j - 3][m + 1];
-            const int nk = j - 2;                 // k2..k_{j-1} enter this stage
+            const int nk = j - 2;                  // k2..k_{j-1} enter this stage
             const int out = (j == 6) ? 0 : j - 2;  // k6 reuses k2's slot
-            // velocity half of k_j (= of arg_j); the sums run in the
-            // reference's left-to-right order
 #pragma unroll
             for (int i = 0; i < M; ++i) {
                 R s = R(b0) * A0[i];
@@ -130,9 +135,8 @@ __device__ __forceinline__ void rkck_nystrom_system(double t_in, double tEnd_in,
         st.rhs_evals += 5;
         st.stages_total += 6;
 
-        // ---- yErr folded into errorNorm (rkck.cpp:75-76, :88-98) ----
-        // err = max_i |yErr_i / (|y_i| + |h f0_i| + tiny)| / eps; the max is
-        // order-independent, so the q and v halves are visited together.
+        // yErr folded into errorNorm (rkck.cpp:75-76, :88-98); the max is
+        // order-independent, so the q and v halves are visited together
         R err;
         bool nanFlag = false;
         {
@@ -194,13 +198,91 @@ __device__ __forceinline__ void rkck_nystrom_system(double t_in, double tEnd_in,
                                    R(c4) * kget(2, M + i) + R(c6) * kget(0, M + i));
             haveF = false;
             h = hNew;
+            live = tEnd - t > uround * fabs_(tEnd);
         } else {
             ++st.steps_rejected;
             if (hNew < R(tol.h_min_floor)) {  // freeze at the last accepted state
                 st.underflow = 1;
-                break;
+                live = false;
             }
             h = hNew;
+        }
+    }
+};
+
+template <class P, class R>
+__device__ __forceinline__ void rkck_nystrom_system(double t_in, double tEnd_in,
+                                                    R (&y)[P::N], const DevTol& tol,
+                                                    DevStats& st) {
+    NystromRkck<P, R> s;
+#pragma unroll
+    for (int c = 0; c < P::N; ++c) s.y[c] = y[c];
+    s.start(t_in, tEnd_in, tol);
+#pragma unroll 1
+    while (s.live) s.attempt(tol);
+#pragma unroll
+    for (int c = 0; c < P::N; ++c) y[c] = s.y[c];
+    st = s.st;
+}
+
+// Persistent-grid driver with dynamic refill (the north_star's ballot-bounded
+// divergence): lanes claim systems from a global counter, one warp-aggregated
+// atomicAdd per claim round; a lane whose system finishes stores it and
+// claims the next, so a warp never idles behind its slowest system until the
+// queue is empty. Results are per-system deterministic, hence independent of
+// which lane integrates which system.
+template <class P, class R>
+__device__ __forceinline__ void rkck_nystrom_persistent(const double* __restrict__ y_in_unused,
+                                                        double* __restrict__ y_soa,
+                                                        DevStats* __restrict__ stats, long long num,
+                                                        double t_in, double tEnd_in,
+                                                        const DevTol& tol, int merge,
+                                                        unsigned long long* counter) {
+    constexpr unsigned kFull = 0xffffffffu;
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    NystromRkck<P, R> s;
+    long long sys = -1;
+    bool has = false, exhausted = false;
+#pragma unroll 1
+    for (;;) {
+        if (!exhausted) {
+            const unsigned need = __ballot_sync(kFull, !has);
+            if (need) {
+                unsigned long long base = 0;
+                const int leader = __ffs(need) - 1;
+                if ((int)lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(need));
+                base = __shfl_sync(kFull, base, leader);
+                if (base + __popc(need) >= (unsigned long long)num) exhausted = true;
+                if (!has) {
+                    const unsigned long long mine = base + __popc(need & lt_mask);
+                    if (mine < (unsigned long long)num) {
+                        sys = (long long)mine;
+#pragma unroll
+                        for (int c = 0; c < P::N; ++c) s.y[c] = R(y_soa[sys + num * (long long)c]);
+                        s.start(t_in, tEnd_in, tol);
+                        has = true;
+                    }
+                }
+            }
+        }
+        if (!__any_sync(kFull, has)) break;
+        if (has) {
+            if (s.live) s.attempt(tol);
+            if (!s.live) {  // done (or frozen): write back, free the lane
+#pragma unroll
+                for (int c = 0; c < P::N; ++c) y_soa[sys + num * (long long)c] = val(s.y[c]);
+                if (stats != nullptr) {
+                    if (merge) {
+                        DevStats o = stats[sys];
+                        stats_merge(o, s.st);
+                        stats[sys] = o;
+                    } else {
+                        stats[sys] = s.st;
+                    }
+                }
+                has = false;
+            }
         }
     }
 }

@@ -220,3 +220,23 @@ def test_device_pointer_entry_with_torch(gpu):
     host = B.integrate_batch(problem_of(prob), B.BatchStates(num, 28, 0, y0.copy(), np.zeros(0)),
                              0.0, 0.1)
     assert np.array_equal(yd.cpu().numpy().view(np.uint64), host.states.values.view(np.uint64))
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_persistent_refill_is_bitwise_static(gpu, arith):
+    """Dynamic refill changes which lane integrates which system, never the result."""
+    import os as _os
+    prob = A.make_problem(A.PLEIADES)
+    y0 = perturb(PLEIADES_IC, 0.1, 17, 50_000)
+    L = B.lib()
+    outs = []
+    try:
+        for persistent in (0, 1):
+            L.bode_set_persistent(persistent)
+            outs.append(run_gpu(prob, A.SOLVER_RKCK, y0, None, arith))
+    finally:
+        L.bode_set_persistent(1)
+    (ys, ss), (yp, sp) = outs
+    assert np.array_equal(ys.view(np.uint64), yp.view(np.uint64))
+    for k in COUNTS + ("stages_total", "h_min_seen", "h_max_seen"):
+        assert np.array_equal(ss[k], sp[k]), k
