@@ -208,8 +208,8 @@ def main():
     ap.add_argument("--num", type=int, default=1 << 22, help="systems per GPU")
     ap.add_argument("--arith", default="fast", choices=["fast", "exact"])
     ap.add_argument("--rkc-num", type=int, default=1 << 22)
-    ap.add_argument("--static", action="store_true",
-                    help="one static system per lane group (disable persistent refill)")
+    ap.add_argument("--persistent", action="store_true",
+                    help="persistent kernels with dynamic refill (default: static)")
     ap.add_argument("--no-secondary", dest="secondary", action="store_false",
                     help="skip the EXACT / RKC measurements")
     ap.add_argument("--cpu-sample", type=int, default=1 << 15)
@@ -238,7 +238,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L = P.lib()
-    L.bode_set_persistent(0 if args.static else 1)
+    L.bode_set_persistent(1 if args.persistent else 0)
     stream = torch.cuda.Stream()
 
     peak = ctypes.c_double()
@@ -349,7 +349,7 @@ def main():
         "config": {"workload": f"RKCK Pleiades (N=28), {num} systems per GPU, perturb 0.01 "
                                f"seed 42+rank, eps 1e-10, window 0.1 (restart)",
                    "arith": args.arith, "systems_per_gpu": num, "window": 0.1,
-                   "scheduling": "static" if args.static else "persistent refill",
+                   "scheduling": "persistent refill" if args.persistent else "static",
                    "l2": "state (num*28*8 B) exceeds the 126 MB L2; no flush needed",
                    "parallelism": f"dp{world} (independent shards, no collective)"},
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak.value / 1e12,

@@ -12,6 +12,7 @@ struct DevTol {  // bode_tol_t, by value in the kernel parameters
         h_min_floor, kappa;
     const double* powtab;    // host-libm pow tables on this device (arith.cuh), or null
     const double* rkc_coef;  // RKC coefficient table for this kappa/policy (rkc.cuh), or null
+    int refill_min;          // persistent kernels: idle lanes that trigger a refill round
 };
 
 struct DevStats {  // bode_stats_t, per system (AoS, 64 bytes)

@@ -35,7 +35,7 @@ using bode::KernelEntry;
 thread_local std::string g_last_error;
 std::atomic<long long> g_launches{0};
 std::atomic<int> g_block_override{0};
-std::atomic<int> g_persistent{1};  // dynamic-refill kernels where compiled
+std::atomic<int> g_persistent{0};  // dynamic-refill kernels where compiled (opt-in)
 
 int fail(int code, const std::string& msg) {
     g_last_error = msg;
@@ -71,6 +71,12 @@ DevTol to_dev(const bode_tol_t* t) {
     d.kappa = t->kappa;
     d.powtab = nullptr;
     d.rkc_coef = nullptr;
+    static const int refill_min = [] {
+        const char* s = std::getenv("BODE_REFILL_MIN");  // tuning knob, default 8
+        const int v = s ? std::atoi(s) : 8;
+        return v < 1 ? 1 : v > 32 ? 32 : v;
+    }();
+    d.refill_min = refill_min;
     return d;
 }
 

@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(kMaxBlock)
     persistent_kernel(const double* __restrict__ g_soa, double* __restrict__ y_soa,
                       DevStats* __restrict__ stats, long long num, double t, double tEnd,
                       DevTol tol, int merge, unsigned long long* counter) {
-    rkck_nystrom_persistent<P, R>(g_soa, y_soa, stats, num, t, tEnd, tol, merge, counter);
+    rkck_nystrom_persistent<P, R>(g_soa, y_soa, stats, num, t, tEnd, tol, merge, counter,
+                                  tol.refill_min);
 }
 
 // ---- dispatch table ----
@@ -89,7 +90,9 @@ static KernelEntry make_entry(int kind, int arith) {
     e.solver = SOLVER;
     e.arith = arith;
     e.lanes = L;
-    e.smem_per_thread = KSMEM ? kSmemStride<C_of<P, L>()>() * (int)sizeof(double) : 0;
+    e.smem_per_thread = SOLVER == 1 ? kRkcSmemStride<C_of<P, L>()>() * (int)sizeof(double)
+                        : KSMEM     ? kSmemStride<C_of<P, L>()>() * (int)sizeof(double)
+                                    : 0;
     e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG>;
     e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                   const double* g, double* y, DevStats* st, long long num, double t,

@@ -237,7 +237,8 @@ __device__ __forceinline__ void rkck_nystrom_persistent(const double* __restrict
                                                         DevStats* __restrict__ stats, long long num,
                                                         double t_in, double tEnd_in,
                                                         const DevTol& tol, int merge,
-                                                        unsigned long long* counter) {
+                                                        unsigned long long* counter,
+                                                        int refill_min) {
     constexpr unsigned kFull = 0xffffffffu;
     const unsigned lane = threadIdx.x & 31u;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -248,7 +249,9 @@ __device__ __forceinline__ void rkck_nystrom_persistent(const double* __restrict
     for (;;) {
         if (!exhausted) {
             const unsigned need = __ballot_sync(kFull, !has);
-            if (need) {
+            // refill in batches of >= refill_min idle lanes: each refill round
+            // costs the warp one scattered-load latency, so amortize it
+            if (need && (__popc(need) >= refill_min || need == kFull)) {
                 unsigned long long base = 0;
                 const int leader = __ffs(need) - 1;
                 if ((int)lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(need));

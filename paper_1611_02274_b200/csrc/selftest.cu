@@ -130,11 +130,20 @@ __global__ void exact_math_kernel(const double* __restrict__ x, long long n, int
                                   unsigned long long* __restrict__ bad,
                                   unsigned long long* __restrict__ first_bad) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    if (i >= n || (op == 2 && i + 1 >= n)) return;
     const double v = x[i];
-    if (!bode::in_safe_range(v)) return;
-    const double got = op == 0 ? bode::sqrt_rn_bf(v) : bode::rcp_rn_bf(v);
-    const double ref = op == 0 ? __dsqrt_rn(v) : __drcp_rn(v);
+    double got, ref;
+    if (op == 2) {  // division: pairs (x[2k], x[2k+1])
+        if (i % 2) return;
+        const double a = v, b = x[i + 1];
+        ref = __ddiv_rn(a, b);
+        if (!bode::div_in_range(a, b, ref)) return;
+        got = bode::div_rn_bf(a, b);
+    } else {
+        if (!bode::in_safe_range(v)) return;
+        got = op == 0 ? bode::sqrt_rn_bf(v) : bode::rcp_rn_bf(v);
+        ref = op == 0 ? __dsqrt_rn(v) : __drcp_rn(v);
+    }
     if (__double_as_longlong(got) != __double_as_longlong(ref)) {
         atomicAdd(bad, 1ull);
         atomicMin(first_bad, (unsigned long long)i);

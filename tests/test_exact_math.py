@@ -25,12 +25,15 @@ def cases(n, seed):
     return np.concatenate([rand_bits, edges, pleiades, pleiades * np.sqrt(pleiades)])
 
 
-@pytest.mark.parametrize("op", [0, 1], ids=["sqrt", "rcp"])
+@pytest.mark.parametrize("op", [0, 1, 2], ids=["sqrt", "rcp", "div"])
 def test_branch_free_matches_ieee(gpu, op):
     from paper_1611_02274_b200 import _abi as A
     bad, first = ctypes.c_int64(), ctypes.c_int64()
     for seed in range(10):
         x = cases(10_000_000, seed)
+        if op == 2:  # random (a, b) pairs, signs included
+            rng = np.random.default_rng(100 + seed)
+            x = x[rng.permutation(x.size)] * rng.choice([-1.0, 1.0], x.size)
         gpu.api.check(gpu.lib().bode_selftest_exact_math(A.dptr(x), x.size, op,
                                                          ctypes.byref(bad), ctypes.byref(first)))
         assert bad.value == 0, f"{bad.value} mismatches, first x = {x[first.value]!r}"

@@ -224,7 +224,9 @@ def test_device_pointer_entry_with_torch(gpu):
 
 @pytest.mark.parametrize("arith", ["exact", "fast"])
 def test_persistent_refill_is_bitwise_static(gpu, arith):
-    """Dynamic refill changes which lane integrates which system, never the result."""
+    """Dynamic refill changes which lane integrates which system, never the
+    result: bitwise under EXACT; under FAST the two kernels may contract FMAs
+    differently, so the tolerance bar applies."""
     import os as _os
     prob = A.make_problem(A.PLEIADES)
     y0 = perturb(PLEIADES_IC, 0.1, 17, 50_000)
@@ -235,8 +237,12 @@ def test_persistent_refill_is_bitwise_static(gpu, arith):
             L.bode_set_persistent(persistent)
             outs.append(run_gpu(prob, A.SOLVER_RKCK, y0, None, arith))
     finally:
-        L.bode_set_persistent(1)
+        L.bode_set_persistent(0)
     (ys, ss), (yp, sp) = outs
-    assert np.array_equal(ys.view(np.uint64), yp.view(np.uint64))
-    for k in COUNTS + ("stages_total", "h_min_seen", "h_max_seen"):
-        assert np.array_equal(ss[k], sp[k]), k
+    if arith == "exact":
+        assert np.array_equal(ys.view(np.uint64), yp.view(np.uint64))
+        for k in COUNTS + ("stages_total", "h_min_seen", "h_max_seen"):
+            assert np.array_equal(ss[k], sp[k]), k
+    else:
+        assert sysrel(yp, ys, y0.size // 28, 28).max() <= 1e-8
+        assert np.array_equal(ss["steps_accepted"], sp["steps_accepted"])

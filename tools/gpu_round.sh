@@ -27,8 +27,8 @@ for p in $PARTS; do
       timeout 600 python tools/divergence.py --problem heat --num 262144 --arith exact > $OUT/diverge_heat.txt 2>&1
       echo "diverge rc=$?" >> $OUT/status.txt ;;
     ab_persist)
-      timeout 600 python bench.py --static --no-e2e --no-cpu --no-secondary > $OUT/bench_static.txt 2>&1
-      timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/bench_persistent.txt 2>&1
+      timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/bench_static.txt 2>&1
+      for T in 4 8 16; do BODE_REFILL_MIN=$T timeout 600 python bench.py --persistent --no-e2e --no-cpu --no-secondary > $OUT/bench_persistent$T.txt 2>&1; done
       echo "ab_persist rc=$?" >> $OUT/status.txt ;;
     bench_exact) timeout 900 python bench.py --arith exact --no-cpu > $OUT/bench_exact.txt 2>&1; echo "bench_exact rc=$?" >> $OUT/status.txt ;;
     ncu)
