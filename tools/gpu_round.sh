@@ -18,12 +18,12 @@ for p in $PARTS; do
       for L in 1 2 8; do BODE_LANES=$L timeout 600 python bench.py --no-e2e --no-cpu --steps 5 > $OUT/bench_lanes$L.txt 2>&1; done
       echo "ab_lanes rc=$?" >> $OUT/status.txt ;;
     ncu_rkc)
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:Heat \
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:Heat \
         -s 1 -c 1 -o $OUT/prof_rkc python bench.py --steps 2 --warmup 1 --num 4096 \
         --rkc-num 131072 --no-e2e --no-cpu > $OUT/ncu_full_rkc.txt 2>&1
       echo "ncu_rkc rc=$?" >> $OUT/status.txt ;;
     ncu_exact)
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:Pleiades \
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:Pleiades \
         -s 1 -c 1 -o $OUT/prof_rkck_exact python bench.py --arith exact --steps 1 --warmup 1 --num 262144 \
         --no-secondary --no-e2e --no-cpu > $OUT/ncu_full_rkck_exact.txt 2>&1
       echo "ncu_exact rc=$?" >> $OUT/status.txt ;;
@@ -41,11 +41,11 @@ for p in $PARTS; do
         --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --num 1048576 \
         --rkc-num 262144 --no-e2e --no-cpu > $OUT/ncu_launches_bench.txt 2>&1
       echo "ncu_launches rc=$?" >> $OUT/status.txt
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:Pleiades \
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:Pleiades \
         -s 1 -c 1 -o $OUT/prof_rkck python bench.py --steps 1 --warmup 1 --num 262144 \
         --no-secondary --no-e2e --no-cpu > $OUT/ncu_full_rkck.txt 2>&1
       echo "ncu_full_rkck rc=$?" >> $OUT/status.txt
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:Heat \
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:Heat \
         -s 1 -c 1 -o $OUT/prof_rkc python bench.py --steps 2 --warmup 1 --num 4096 \
         --rkc-num 131072 --no-e2e --no-cpu > $OUT/ncu_full_rkc.txt 2>&1
       echo "ncu_full_rkc rc=$?" >> $OUT/status.txt ;;
