@@ -166,6 +166,17 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def measured_traffic(capture: str, num: int):
+    """DRAM bytes per launch for `num` systems, from the newest committed ncu
+    capture summary (profiles/*_ncu.json: dram read+write per system-window)."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(REPO, "profiles", "*_ncu.json")), reverse=True):
+        d = json.load(open(path)).get(capture)
+        if d and d.get("dram_bytes_per_system"):
+            return d["dram_bytes_per_system"] * num, os.path.basename(path)
+    return None, None
+
+
 def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warmup, stream):
     """K windows on HBM-resident state; per-launch CUDA events on `stream`."""
     num = y0.size // dim
@@ -334,6 +345,8 @@ def main():
             dist.destroy_process_group()
         return
 
+    traffic, traffic_src = measured_traffic("rkck_fast" if args.arith == "fast" else "rkck_exact",
+                                            num)
     cpu = None
     if not args.no_cpu:
         rate, cores, kind, dt = cpu_reference_rate("pleiades", "rkck", PLEIADES_IC, 0.01, 42,
@@ -353,7 +366,9 @@ def main():
                    "l2": "state (num*28*8 B) exceeds the 126 MB L2; no flush needed",
                    "parallelism": f"dp{world} (independent shards, no collective)"},
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak.value / 1e12,
-                     "unit": "TFLOP/s", "frac": achieved / peak.value, "traffic": None,
+                     "unit": "TFLOP/s", "frac": achieved / peak.value, "traffic": traffic,
+                     "traffic_source": traffic_src,
+                     "algorithmic_bytes_per_launch": num * (28 * 8 * 2 + 64),
                      "peak_source": "DFMA microbenchmark on this device in this run "
                                     "(MEASURED_PEAKS.json has no FP64 entry); nominal 37.2",
                      "flop_per_system_window": flops / (num * args.steps),
