@@ -246,3 +246,38 @@ def test_persistent_refill_is_bitwise_static(gpu, arith):
     else:
         assert sysrel(yp, ys, y0.size // 28, 28).max() <= 1e-8
         assert np.array_equal(ss["steps_accepted"], sp["steps_accepted"])
+
+
+def _stride_check(oracle, prob, solver, base, mag, num, stride, arith, seed=42):
+    y0 = perturb(base, mag, seed, num)
+    y, st = run_gpu(prob, solver, y0, None, arith)
+    idx = np.arange(0, num, stride)
+    sub = np.ascontiguousarray(y0.reshape(prob.dim, num)[:, idx]).reshape(-1)
+    rc, yo, so, _ = oracle.outer_loop(prob, solver, 0.0, 1.0, 0.1, sub)
+    got = np.ascontiguousarray(y.reshape(prob.dim, num)[:, idx]).reshape(-1)
+    return got, yo, st, so, idx
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+def test_rkck_full_size_2_22_stride(gpu, oracle, arith):
+    """BASELINE configs[1] at its largest size: 2^22 systems on the GPU, every
+    64th re-integrated by the oracle."""
+    prob = A.make_problem(A.PLEIADES)
+    got, yo, st, so, idx = _stride_check(oracle, prob, A.SOLVER_RKCK, PLEIADES_IC, 0.01, 1 << 22,
+                                         64, arith)
+    if arith == "exact":
+        assert np.array_equal(got.view(np.uint64), yo.view(np.uint64))
+    else:
+        assert sysrel(got, yo, idx.size, 28).max() <= 1e-13
+    for k in ("steps_accepted", "steps_rejected", "rhs_evals"):
+        assert np.array_equal(st[k][idx], so[k]), k
+
+
+def test_rkc_heat64_2_20_stride(gpu, oracle):
+    """Config 3 at 2^20 systems, every 256th system re-integrated by the oracle."""
+    prob = A.make_problem(A.HEAT, 64)
+    got, yo, st, so, idx = _stride_check(oracle, prob, A.SOLVER_RKC, heat_ic(64), 0.01, 1 << 20,
+                                         256, "exact")
+    assert np.array_equal(got.view(np.uint64), yo.view(np.uint64))
+    for k in COUNTS + ("stages_total",):
+        assert np.array_equal(st[k][idx], so[k]), k
