@@ -46,6 +46,8 @@ __constant__ double c_ck_b[4][5] = {
 
 // Per-lane solver state: one system, advanced one attempt at a time, so a
 // persistent kernel can hand a lane a new system as soon as its own finishes.
+constexpr bool kRkckUnrollStages = true;
+
 template <class P, class R>
 struct NystromRkck {
     static constexpr int M = P::N / 2;
@@ -98,9 +100,24 @@ struct NystromRkck {
             for (int i = 0; i < M; ++i) kset(0, M + i, Acc[i]);
             BODE_FENCE();
         }
-        // stages 3..6 (rkck.cpp:46-64): arg = y + h*(b_j1 f0 + b_j2 k2 + ...)
+        // stages 3..6 (rkck.cpp:46-64): arg = y + h*(b_j1 f0 + b_j2 k2 + ...).
+        // kRkckUnrollStages: unrolled, every sum has its exact length; else one
+        // rolled loop whose sums are predicated to the stage's length.
+#pragma unroll
+        for (int j = 3; j <= (kRkckUnrollStages ? 6 : 3); ++j) stage_block<kRkckUnrollStages>(j, Q, Acc);
 #pragma unroll 1
-        for (int j = 3; j <= 6; ++j) {
+        for (int j = 4; j <= (kRkckUnrollStages ? 3 : 6); ++j) stage_block<false>(j, Q, Acc);
+        st.rhs_evals += 5;
+        st.stages_total += 6;
+        finish_attempt(tol);
+    }
+
+    // stage j in 3..6; UNROLLED: j is a compile-time constant after unrolling
+    template <bool UNROLLED>
+    __device__ __forceinline__ void stage_block(int j, R (&Q)[M], R (&Acc)[M]) {
+        R* const q = y;
+        R* const v = y + M;
+        {
             const double b0 = c_ck_b[j - 3][0];
             double bm[4];  // b_j2..b_j5 (zero past the stage's last term)
 #pragma unroll
@@ -132,16 +149,24 @@ struct NystromRkck {
             for (int i = 0; i < M; ++i) kset(out, M + i, Acc[i]);
             BODE_FENCE();
         }
-        st.rhs_evals += 5;
-        st.stages_total += 6;
+    }
 
+    // error norm, controller and the accept/reject update of one attempt
+    __device__ __forceinline__ void finish_attempt(const DevTol& tol) {
+        using namespace ck;
+        R* const q = y;
+        R* const v = y + M;
+        const R hMin(tol.h_min_floor);
+        const R uround(tol.uround), eps(tol.eps), tiny(tol.tiny);
         // yErr folded into errorNorm (rkck.cpp:75-76, :88-98); the max is
         // order-independent, so the q and v halves are visited together
         R err;
         bool nanFlag = false;
         {
-            QuotMax qm;
-            double fm = 0.0;
+            // four interleaved accumulators: max and exact-argmax are associative,
+            // so this only shortens the dependency chain (4x), never the result
+            QuotMax qm[4];
+            double fm[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int i = 0; i < M; ++i) {
                 const R eq = h * (R(d1) * v[i] + R(d3) * kget(1, i) + R(d4) * kget(2, i) +
@@ -153,17 +178,21 @@ struct NystromRkck {
                 const R dq = fabs_(q[i]) + fabs_(h * v[i]) + tiny;
                 const R dv = fabs_(v[i]) + fabs_(h * A0[i]) + tiny;
                 if constexpr (is_exact<R>::value) {
-                    qm.push(fabs(val(eq)), val(dq));
-                    qm.push(fabs(val(ev)), val(dv));
+                    qm[(2 * i) & 3].push(fabs(val(eq)), val(dq));
+                    qm[(2 * i + 1) & 3].push(fabs(val(ev)), val(dv));
                 } else {
-                    fm = fmax(fm, fabs(val(eq)) * rcp_fast(val(dq)));
-                    fm = fmax(fm, fabs(val(ev)) * rcp_fast(val(dv)));
+                    fm[(2 * i) & 3] = fmax(fm[(2 * i) & 3], fabs(val(eq)) * rcp_fast(val(dq)));
+                    fm[(2 * i + 1) & 3] = fmax(fm[(2 * i + 1) & 3], fabs(val(ev)) * rcp_fast(val(dv)));
                 }
             }
+            qm[0].push(qm[1].a, qm[1].b);
+            qm[2].push(qm[3].a, qm[3].b);
+            qm[0].push(qm[2].a, qm[2].b);
+            const double fmx = fmax(fmax(fm[0], fm[1]), fmax(fm[2], fm[3]));
             if constexpr (is_exact<R>::value)
-                err = R(qm.value());
+                err = R(qm[0].value());
             else
-                err = R(fm);
+                err = R(fmx);
         }
         err = err / eps;
 

@@ -191,8 +191,10 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
         R err;
         bool nanFlag = false;
         {
-            QuotMax qm;
-            double fm = 0.0;
+            // four interleaved accumulators: max and exact-argmax are associative,
+            // so this only shortens the dependency chain (4x), never the result
+            QuotMax qm[4];
+            double fm[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int i = 0; i < M; ++i) {
                 const R eq = h * (R(d1) * v[i] + R(d3) * kget(1, i) + R(d4) * kget(2, i) +
@@ -204,19 +206,24 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
                 const R dq = fabs_(q[i]) + fabs_(h * v[i]) + tiny;
                 const R dv = fabs_(v[i]) + fabs_(h * A0[i]) + tiny;
                 if constexpr (is_exact<R>::value) {
-                    qm.push(fabs(val(eq)), val(dq));
-                    qm.push(fabs(val(ev)), val(dv));
+                    qm[(2 * i) & 3].push(fabs(val(eq)), val(dq));
+                    qm[(2 * i + 1) & 3].push(fabs(val(ev)), val(dv));
                 } else {
-                    fm = fmax(fm, fabs(val(eq)) * rcp_fast(val(dq)));
-                    fm = fmax(fm, fabs(val(ev)) * rcp_fast(val(dv)));
+                    fm[(2 * i) & 3] = fmax(fm[(2 * i) & 3], fabs(val(eq)) * rcp_fast(val(dq)));
+                    fm[(2 * i + 1) & 3] = fmax(fm[(2 * i + 1) & 3], fabs(val(ev)) * rcp_fast(val(dv)));
                 }
             }
+            qm[0].push(qm[1].a, qm[1].b);
+            qm[2].push(qm[3].a, qm[3].b);
+            qm[0].push(qm[2].a, qm[2].b);
+            const double fmx = fmax(fmax(fm[0], fm[1]), fmax(fm[2], fm[3]));
             nanFlag = (__ballot_sync(0xffffffffu, nanFlag) & G.mask) != 0u;
             if constexpr (is_exact<R>::value) {
-                qm.push(__shfl_xor_sync(0xffffffffu, qm.a, 1), __shfl_xor_sync(0xffffffffu, qm.b, 1));
-                err = R(qm.value());
+                qm[0].push(__shfl_xor_sync(0xffffffffu, qm[0].a, 1),
+                           __shfl_xor_sync(0xffffffffu, qm[0].b, 1));
+                err = R(qm[0].value());
             } else {
-                err = R(fmax(fm, __shfl_xor_sync(0xffffffffu, fm, 1)));
+                err = R(fmax(fmx, __shfl_xor_sync(0xffffffffu, fmx, 1)));
             }
         }
         err = err / eps;

@@ -35,6 +35,10 @@ for p in $PARTS; do
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/bench_static.txt 2>&1
       for T in 4 8 16; do BODE_REFILL_MIN=$T timeout 600 python bench.py --persistent --no-e2e --no-cpu --no-secondary > $OUT/bench_persistent$T.txt 2>&1; done
       echo "ab_persist rc=$?" >> $OUT/status.txt ;;
+    quick)
+      timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
+      timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
+      echo "quick rc=$?" >> $OUT/status.txt ;;
     bench_exact) timeout 900 python bench.py --arith exact --no-cpu > $OUT/bench_exact.txt 2>&1; echo "bench_exact rc=$?" >> $OUT/status.txt ;;
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
