@@ -51,6 +51,8 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
     DevStats st;
     if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 2)
         rkck_pleiades2_system<R>(G, t, tEnd, y, tol, st);
+    else if constexpr (SOLVER == 0 && is_second_order<P>::value)
+        rkck_nystrom_system<P, R>(t, tEnd, y, tol, st);
     else if constexpr (SOLVER == 0)
         rkck_system<P, R, L, KSMEM>(G, t, tEnd, y, g, tol, st);
     else
@@ -102,17 +104,8 @@ static KernelEntry make_entry(int kind, int arith) {
     e.default_block = KSMEM ? 128 : 128;
     e.build_rkc_table = nullptr;
     if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1) {
-        // static launches use the same kernel with counter == nullptr (a fixed
-        // system per lane, no refill): under __launch_bounds__ ptxas allocates
-        // it without spills, unlike the __maxnreg__ template instance
-        e.fn = (const void*)&persistent_kernel<P, R>;
-        e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                      const double* g, double* y, DevStats* st, long long num, double t,
-                      double tEnd, DevTol tol, int merge) {
-            auto k = (void (*)(const double*, double*, DevStats*, long long, double, double,
-                               DevTol, int, unsigned long long*))fn;
-            k<<<grid, block, smem, s>>>(g, y, st, num, t, tEnd, tol, merge, nullptr);
-        };
+        // (routing static launches through this instance with counter == nullptr
+        // removes the spills but measured 9% slower: the any_sync loop costs more)
         e.pfn = (const void*)&persistent_kernel<P, R>;
         e.launch_persistent = [](const void* fn, dim3 grid, dim3 block, size_t smem,
                                  cudaStream_t s, const double* g, double* y, DevStats* st,
