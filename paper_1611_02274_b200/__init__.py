@@ -7,5 +7,5 @@ interface (api.py) plus the in-tree build (build.py).
 from . import _abi  # noqa: F401
 from .api import (BatchResult, BatchStates, BodeError, CudaError, InvalidInterval,  # noqa: F401
                   InvalidShape, InvalidStageCount, NoDevice, OdeProblem, OuterLoopResult,
-                  Unsupported, fill_params, int_driver_device, integrate_batch, lib,
+                  Unsupported, fill_params, int_driver_device, integrate_batch, integrate_fixed, lib,
                   outer_loop, pack, problems, stiffness_params, tolerance_settings, unpack)

@@ -94,6 +94,8 @@ def lib():
         "bode_set_block_size": (ctypes.c_int, [c_i32]),
         "bode_launch_count": (c_i64, []),
         "bode_set_persistent": (ctypes.c_int, [c_i32]),
+        "bode_integrate_fixed": (ctypes.c_int, [P(A.Problem), c_i32, c_i32, c_d, c_d, c_i64,
+                                                c_i32, c_d, c_i64, PD, PD]),
         "bode_splitmix64_at": (c_u64, [c_u64, c_u64]),
         "bode_unit_symmetric_at": (c_d, [c_u64, c_u64]),
         "bode_perturb_initial_conditions": (ctypes.c_int, [PD, c_i32, c_d, c_u64, c_i64, PD]),
@@ -282,6 +284,20 @@ def outer_loop(problem: OdeProblem, initial: BatchStates, t0: float, t_end: floa
                                 A.dptr(out.values), ctypes.byref(tol), A.vptr(stats), gpus, cb,
                                 None, ctypes.byref(steps)))
     return OuterLoopResult(out, stats, steps.value)
+
+
+def integrate_fixed(problem: OdeProblem, batch: BatchStates, t0: float, t_end: float,
+                    num_steps: int, solver="rkck", stages: int = 0,
+                    kappa: float = 2.0 / 13.0, arith="exact") -> BatchStates:
+    """rkck::integrateFixed / rkc::integrateFixed (rkck.cpp:168-181,
+    rkc.cpp:290-306) over a whole batch on the GPU."""
+    _check_batch(problem, batch)
+    out = batch.copy()
+    g = out.params if out.param_dim else None
+    check(lib().bode_integrate_fixed(ctypes.byref(problem.c()), _solver(solver), _arith(arith),
+                                     t0, t_end, num_steps, stages, kappa, batch.num_systems,
+                                     A.dptr(g), A.dptr(out.values)))
+    return out
 
 
 def int_driver_device(problem: OdeProblem, solver, arith, t: float, t_end: float, num: int,

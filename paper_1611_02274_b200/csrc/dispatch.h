@@ -46,6 +46,11 @@ struct KernelEntry {
     // resident capacity whose lanes claim systems from `counter`
     const void* pfn = nullptr;
     LaunchPersistentFn launch_persistent = nullptr;
+    // fixed-step harness (integrateFixed) for this problem/solver/policy
+    const void* ffn = nullptr;
+    void (*launch_fixed)(const void* fn, dim3 grid, dim3 block, cudaStream_t s, const double* g,
+                         double* y, long long num, double t0, double tEnd, long long numSteps,
+                         long long stages, double kappa) = nullptr;
 };
 
 const KernelEntry* kernel_table(int* count);

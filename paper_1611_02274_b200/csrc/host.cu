@@ -628,6 +628,51 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
     return BODE_OK;
 }
 
+// Fixed-step harnesses (rkck.cpp:168-181, rkc.cpp:290-306), host pointers.
+int bode_integrate_fixed(const bode_problem_t* p, int32_t solver, int32_t arith, double t0,
+                         double t_end, int64_t num_steps, int32_t stages, double kappa,
+                         int64_t num, const double* g, double* y) {
+    if (!(t_end > t0) || num_steps < 1)
+        return fail(BODE_E_INVALID_INTERVAL, "integrateFixed: bad interval or step count");
+    if (solver == BODE_SOLVER_RKC && stages < 2)
+        return fail(BODE_E_INVALID_STAGE_COUNT, "rkc::coefficients: need at least two stages");
+    bode_tol_t tol;
+    bode_tol_default(&tol);
+    const KernelEntry* e = nullptr;
+    int rc = validate_call(p, solver, arith, t0, t_end, num, g, y, &tol, &e);
+    if (rc) return rc;
+    if (e->launch_fixed == nullptr) {  // e.g. the lane-pair Pleiades kernel: try the others
+        int n = 0;
+        const KernelEntry* tab = bode::kernel_table(&n);
+        for (int i = 0; i < n; ++i)
+            if (tab[i].kind == p->kind && tab[i].dim == p->dim && tab[i].param_dim == p->param_dim &&
+                tab[i].solver == solver && tab[i].arith == arith && tab[i].launch_fixed) {
+                e = &tab[i];
+                break;
+            }
+    }
+    if (e->launch_fixed == nullptr)
+        return fail(BODE_E_UNSUPPORTED, "no fixed-step kernel for this problem/solver");
+    if ((rc = check_devices(1))) return rc;
+    BODE_CUDA(cudaSetDevice(0));
+    const int N = p->dim, P = p->param_dim;
+    double *dy = nullptr, *dg = nullptr;
+    BODE_CUDA(cudaMalloc(&dy, (size_t)num * N * sizeof(double)));
+    if (P > 0) BODE_CUDA(cudaMalloc(&dg, (size_t)num * P * sizeof(double)));
+    BODE_CUDA(cudaMemcpy(dy, y, (size_t)num * N * sizeof(double), cudaMemcpyHostToDevice));
+    if (P > 0) BODE_CUDA(cudaMemcpy(dg, g, (size_t)num * P * sizeof(double), cudaMemcpyHostToDevice));
+    const int block = 128;
+    const long long grid = (num * e->lanes + block - 1) / block;
+    e->launch_fixed(e->ffn, dim3((unsigned)grid), dim3(block), 0, dg, dy, num, t0, t_end,
+                    num_steps, stages, kappa);
+    g_launches.fetch_add(1);
+    BODE_CUDA(cudaGetLastError());
+    BODE_CUDA(cudaMemcpy(y, dy, (size_t)num * N * sizeof(double), cudaMemcpyDeviceToHost));
+    cudaFree(dy);
+    if (dg) cudaFree(dg);
+    return BODE_OK;
+}
+
 // ---- synthetic inputs (problems.cpp:158-191) ----
 uint64_t bode_splitmix64_at(uint64_t seed, uint64_t k) {
     uint64_t z = seed + (k + 1) * 0x9e3779b97f4a7c15ull;

@@ -14,6 +14,7 @@
 #include "rkc.cuh"
 #include "rkck_nystrom.cuh"
 #include "rkck_pleiades2.cuh"
+#include "fixed.cuh"
 
 namespace bode {
 
@@ -103,6 +104,16 @@ static KernelEntry make_entry(int kind, int arith) {
     };
     e.default_block = KSMEM ? 128 : 128;
     e.build_rkc_table = nullptr;
+    if constexpr (!(SOLVER == 0 && is_second_order<P>::value && L == 2)) {
+        e.ffn = (const void*)&fixed_kernel<P, R, L, SOLVER>;
+        e.launch_fixed = [](const void* fn, dim3 grid, dim3 block, cudaStream_t s,
+                            const double* g, double* y, long long num, double t0, double tEnd,
+                            long long numSteps, long long stages, double kappa) {
+            auto k = (void (*)(const double*, double*, long long, double, double, long long,
+                               long long, double))fn;
+            k<<<grid, block, 0, s>>>(g, y, num, t0, tEnd, numSteps, stages, kappa);
+        };
+    }
     if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1) {
         // (routing static launches through this instance with counter == nullptr
         // removes the spills but measured 9% slower: the any_sync loop costs more)
