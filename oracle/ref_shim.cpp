@@ -15,6 +15,9 @@
 #include "batchode/rkc.hpp"
 #include "batchode/rkck.hpp"
 #include "batchode/spectral_radius.hpp"
+#ifdef BODE_REF_HAVE_BENCH
+#include "batchode/bench.hpp"
+#endif
 
 #include "../include/bode.h"
 
@@ -285,5 +288,39 @@ int ref_power_method(const bode_problem_t* p, double t, const double* y, const d
         *converged = r.converged ? 1 : 0;
     });
 }
+
+#ifdef BODE_REF_HAVE_BENCH
+// batchode::bench::run (bench.cpp:382-397): the reference's odebench minus
+// its CLI11 front end, for comparing report files with bode's odebench.
+int ref_bench_run(const char* problem, const char* solver, const char* mode, int numSystems,
+                  double t0, double tEnd, double hOuter, double eps, double absTol,
+                  double relTol, int workers, uint64_t seed, double perturb,
+                  const char* output, const char* summary, const char* icPath,
+                  int heatPoints) {
+    try {
+        bench::RunConfig cfg;
+        cfg.problem = bench::parseProblem(problem);
+        cfg.solver = bench::parseSolver(solver);
+        cfg.mode = bench::parseMode(mode);
+        cfg.numSystems = numSystems;
+        cfg.t0 = t0;
+        cfg.tEnd = tEnd;
+        cfg.hOuter = hOuter;
+        cfg.eps = eps;
+        cfg.absTol = absTol;
+        cfg.relTol = relTol;
+        cfg.workers = workers;
+        cfg.seed = seed;
+        cfg.perturbMagnitude = perturb;
+        cfg.outputPath = output ? output : "";
+        cfg.summaryPath = summary ? summary : "";
+        cfg.pleiadesIcPath = icPath ? icPath : "";
+        cfg.heatPoints = heatPoints;
+        return bench::run(cfg);
+    } catch (...) {
+        return 2;
+    }
+}
+#endif
 
 }  // extern "C"
