@@ -140,8 +140,7 @@ struct Pleiades {
                     a[7 + j] -= R(mi) * dy * invR3;
                 } else {
                     const R r2 = dx * dx + dy * dy;
-                    const double rs = rsqrt_fast(val(r2));
-                    const double invR3 = rs * rs * rs;
+                    const double invR3 = rsqrt3_fast(val(r2));
                     const double ax = val(dx) * invR3;
                     const double ay = val(dy) * invR3;
                     a[i] += mj * ax;

@@ -124,21 +124,44 @@ struct NystromRkck {
             for (int m = 0; m < 4; ++m) bm[m] = c_ck_b[j - 3][m + 1];
             const int nk = j - 2;                  // k2..k_{j-1} enter this stage
             const int out = (j == 6) ? 0 : j - 2;  // k6 reuses k2's slot
+            if constexpr (is_exact<R>::value) {
 #pragma unroll
-            for (int i = 0; i < M; ++i) {
-                R s = R(b0) * A0[i];
+                for (int i = 0; i < M; ++i) {
+                    R s = R(b0) * A0[i];
 #pragma unroll
-                for (int m = 0; m < 4; ++m)  // predicated: constant offsets, no loop
-                    if (m < nk) s = s + R(bm[m]) * kget(m, M + i);
-                Acc[i] = v[i] + h * s;
-            }
+                    for (int m = 0; m < 4; ++m)  // predicated: constant offsets, no loop
+                        if (m < nk) s = s + R(bm[m]) * kget(m, M + i);
+                    Acc[i] = v[i] + h * s;
+                }
 #pragma unroll
-            for (int i = 0; i < M; ++i) {
-                R s = R(b0) * v[i];
+                for (int i = 0; i < M; ++i) {
+                    R s = R(b0) * v[i];
 #pragma unroll
-                for (int m = 0; m < 4; ++m)
-                    if (m < nk) s = s + R(bm[m]) * kget(m, i);
-                Q[i] = q[i] + h * s;
+                    for (int m = 0; m < 4; ++m)
+                        if (m < nk) s = s + R(bm[m]) * kget(m, i);
+                    Q[i] = q[i] + h * s;
+                }
+            } else {  // FAST: h folded into the stage weights, one FMA per term
+                const double hb0 = val(h) * b0;
+                double hbm[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) hbm[m] = val(h) * bm[m];
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    double s = fma(hb0, val(A0[i]), val(v[i]));
+#pragma unroll
+                    for (int m = 0; m < 4; ++m)
+                        if (m < nk) s = fma(hbm[m], val(kget(m, M + i)), s);
+                    Acc[i] = R(s);
+                }
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    double s = fma(hb0, val(v[i]), val(q[i]));
+#pragma unroll
+                    for (int m = 0; m < 4; ++m)
+                        if (m < nk) s = fma(hbm[m], val(kget(m, i)), s);
+                    Q[i] = R(s);
+                }
             }
             BODE_FENCE();
 #pragma unroll
@@ -162,7 +185,35 @@ struct NystromRkck {
         // order-independent, so the q and v halves are visited together
         R err;
         bool nanFlag = false;
-        {
+        if constexpr (!is_exact<R>::value) {
+            // FAST: h folded into the error weights; the max of |e_i| / d_i is
+            // tracked as an argmax by cross-multiplication (no per-component
+            // reciprocal) and divided out once; non-finite yErr components are
+            // detected from their exponent fields
+            const double hh = val(h);
+            const double hd1 = hh * d1, hd3 = hh * d3, hd4 = hh * d4, hd5 = hh * d5, hd6 = hh * d6;
+            double ma[4] = {0.0, 0.0, 0.0, 0.0}, mb[4] = {1.0, 1.0, 1.0, 1.0};
+            int bad = 0;
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                const double eq = fma(hd6, val(kget(0, i)), fma(hd5, val(kget(3, i)),
+                                  fma(hd4, val(kget(2, i)), fma(hd3, val(kget(1, i)), hd1 * val(v[i])))));
+                const double ev = fma(hd6, val(kget(0, M + i)), fma(hd5, val(kget(3, M + i)),
+                                  fma(hd4, val(kget(2, M + i)), fma(hd3, val(kget(1, M + i)), hd1 * val(A0[i])))));
+                bad |= ((__double2hiint(eq) & 0x7ff00000) == 0x7ff00000) |
+                       ((__double2hiint(ev) & 0x7ff00000) == 0x7ff00000);
+                const double dq = fma(hh, fabs(val(v[i])), fabs(val(q[i]))) + val(tiny);
+                const double dv = fma(hh, fabs(val(A0[i])), fabs(val(v[i]))) + val(tiny);
+                const int kq = (2 * i) & 3, kv = (2 * i + 1) & 3;
+                if (fabs(eq) * mb[kq] > ma[kq] * dq) { ma[kq] = fabs(eq); mb[kq] = dq; }
+                if (fabs(ev) * mb[kv] > ma[kv] * dv) { ma[kv] = fabs(ev); mb[kv] = dv; }
+            }
+#pragma unroll
+            for (int k = 1; k < 4; ++k)
+                if (ma[k] * mb[0] > ma[0] * mb[k]) { ma[0] = ma[k]; mb[0] = mb[k]; }
+            nanFlag = bad != 0;
+            err = R(ma[0] * rcp_fast(mb[0] * val(eps)));
+        } else {
             // four interleaved accumulators: max and exact-argmax are associative,
             // so this only shortens the dependency chain (4x), never the result
             QuotMax qm[4];
@@ -193,8 +244,8 @@ struct NystromRkck {
                 err = R(qm[0].value());
             else
                 err = R(fmx);
+            err = err / eps;
         }
-        err = err / eps;
 
         R hNew;
         bool accepted;
@@ -205,11 +256,11 @@ struct NystromRkck {
                 accepted = false;
                 hNew = (!isfinite(err) || nanFlag)
                            ? tol.p1 * h
-                           : fmax(tol.safety * h * pow_fast(err, tol.pshrnk), tol.p1 * h);
+                           : fmax(tol.safety * h * ctrl_pow_fast(err, tol.pshrnk), tol.p1 * h);
             } else {
                 accepted = true;
                 const double hn =
-                    (err > tol.errcon) ? tol.safety * h * pow_fast(err, tol.pgrow) : 5.0 * h;
+                    (err > tol.errcon) ? tol.safety * h * ctrl_pow_fast(err, tol.pgrow) : 5.0 * h;
                 hNew = fmax(val(hMin), fmin(val(hMax), hn));
             }
         }
@@ -217,14 +268,27 @@ struct NystromRkck {
             t += h;
             stats_accept(st, val(h));
             // yNext (rkck.cpp:74): the q half reads the old v, so it goes first
+            if constexpr (is_exact<R>::value) {
 #pragma unroll
-            for (int i = 0; i < M; ++i)
-                q[i] = q[i] + h * (R(c1) * v[i] + R(c3) * kget(1, i) + R(c4) * kget(2, i) +
-                                   R(c6) * kget(0, i));
+                for (int i = 0; i < M; ++i)
+                    q[i] = q[i] + h * (R(c1) * v[i] + R(c3) * kget(1, i) + R(c4) * kget(2, i) +
+                                       R(c6) * kget(0, i));
 #pragma unroll
-            for (int i = 0; i < M; ++i)
-                v[i] = v[i] + h * (R(c1) * A0[i] + R(c3) * kget(1, M + i) +
-                                   R(c4) * kget(2, M + i) + R(c6) * kget(0, M + i));
+                for (int i = 0; i < M; ++i)
+                    v[i] = v[i] + h * (R(c1) * A0[i] + R(c3) * kget(1, M + i) +
+                                       R(c4) * kget(2, M + i) + R(c6) * kget(0, M + i));
+            } else {  // FAST: h folded into the weights
+                const double hh = val(h);
+                const double hc1 = hh * c1, hc3 = hh * c3, hc4 = hh * c4, hc6 = hh * c6;
+#pragma unroll
+                for (int i = 0; i < M; ++i)
+                    q[i] = R(fma(hc6, val(kget(0, i)), fma(hc4, val(kget(2, i)),
+                             fma(hc3, val(kget(1, i)), fma(hc1, val(v[i]), val(q[i]))))));
+#pragma unroll
+                for (int i = 0; i < M; ++i)
+                    v[i] = R(fma(hc6, val(kget(0, M + i)), fma(hc4, val(kget(2, M + i)),
+                             fma(hc3, val(kget(1, M + i)), fma(hc1, val(A0[i]), val(v[i]))))));
+            }
             haveF = false;
             h = hNew;
             live = tEnd - t > uround * fabs_(tEnd);

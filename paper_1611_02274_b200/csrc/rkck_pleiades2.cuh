@@ -64,8 +64,7 @@ __device__ __forceinline__ void pleiades_accel_pair(const Group<2>& G, const R* 
             r2s[k] = r2;
             mine[k] = rcp_rn_bf(d);
         } else {
-            const double rs = rsqrt_fast(own + oth);
-            mine[k] = rs * rs * rs;
+            mine[k] = rsqrt3_fast(own + oth);
         }
     }
     if constexpr (is_exact<R>::value) {
@@ -160,21 +159,44 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
             for (int m = 0; m < 4; ++m) bm[m] = c_ck_b[j - 3][m + 1];
             const int nk = j - 2;
             const int out = (j == 6) ? 0 : j - 2;  // k6 reuses k2's slot
+            if constexpr (is_exact<R>::value) {
 #pragma unroll
-            for (int i = 0; i < M; ++i) {
-                R s = R(b0) * A0[i];
+                for (int i = 0; i < M; ++i) {
+                    R s = R(b0) * A0[i];
 #pragma unroll
-                for (int m = 0; m < 4; ++m)  // predicated: constant offsets, no loop
-                    if (m < nk) s = s + R(bm[m]) * kget(m, M + i);
-                Acc[i] = v[i] + h * s;
-            }
+                    for (int m = 0; m < 4; ++m)  // predicated: constant offsets, no loop
+                        if (m < nk) s = s + R(bm[m]) * kget(m, M + i);
+                    Acc[i] = v[i] + h * s;
+                }
 #pragma unroll
-            for (int i = 0; i < M; ++i) {
-                R s = R(b0) * v[i];
+                for (int i = 0; i < M; ++i) {
+                    R s = R(b0) * v[i];
 #pragma unroll
-                for (int m = 0; m < 4; ++m)
-                    if (m < nk) s = s + R(bm[m]) * kget(m, i);
-                Q[i] = q[i] + h * s;
+                    for (int m = 0; m < 4; ++m)
+                        if (m < nk) s = s + R(bm[m]) * kget(m, i);
+                    Q[i] = q[i] + h * s;
+                }
+            } else {  // FAST: h folded into the stage weights (rkck_nystrom.cuh)
+                const double hb0 = val(h) * b0;
+                double hbm[4];
+#pragma unroll
+                for (int m = 0; m < 4; ++m) hbm[m] = val(h) * bm[m];
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    double s = fma(hb0, val(A0[i]), val(v[i]));
+#pragma unroll
+                    for (int m = 0; m < 4; ++m)
+                        if (m < nk) s = fma(hbm[m], val(kget(m, M + i)), s);
+                    Acc[i] = R(s);
+                }
+#pragma unroll
+                for (int i = 0; i < M; ++i) {
+                    double s = fma(hb0, val(v[i]), val(q[i]));
+#pragma unroll
+                    for (int m = 0; m < 4; ++m)
+                        if (m < nk) s = fma(hbm[m], val(kget(m, i)), s);
+                    Q[i] = R(s);
+                }
             }
 #pragma unroll
             for (int i = 0; i < M; ++i) kset(out, i, Acc[i]);
@@ -193,40 +215,59 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
         {
             // four interleaved accumulators: max and exact-argmax are associative,
             // so this only shortens the dependency chain (4x), never the result
+            // the max is tracked as an exact (EXACT) or rounded (FAST) argmax by
+            // cross-multiplication and divided out once (arith.cuh QuotMax)
             QuotMax qm[4];
-            double fm[4] = {0.0, 0.0, 0.0, 0.0};
+            double ma[4] = {0.0, 0.0, 0.0, 0.0}, mb[4] = {1.0, 1.0, 1.0, 1.0};
+            const double hh = val(h);
+            const double hd1 = hh * d1, hd3 = hh * d3, hd4 = hh * d4, hd5 = hh * d5, hd6 = hh * d6;
+            int bad = 0;
 #pragma unroll
             for (int i = 0; i < M; ++i) {
-                const R eq = h * (R(d1) * v[i] + R(d3) * kget(1, i) + R(d4) * kget(2, i) +
-                                  R(d5) * kget(3, i) + R(d6) * kget(0, i));
-                const R ev = h * (R(d1) * A0[i] + R(d3) * kget(1, M + i) +
-                                  R(d4) * kget(2, M + i) + R(d5) * kget(3, M + i) +
-                                  R(d6) * kget(0, M + i));
-                if (!isfinite_(eq) || !isfinite_(ev)) nanFlag = true;
-                const R dq = fabs_(q[i]) + fabs_(h * v[i]) + tiny;
-                const R dv = fabs_(v[i]) + fabs_(h * A0[i]) + tiny;
                 if constexpr (is_exact<R>::value) {
+                    const R eq = h * (R(d1) * v[i] + R(d3) * kget(1, i) + R(d4) * kget(2, i) +
+                                      R(d5) * kget(3, i) + R(d6) * kget(0, i));
+                    const R ev = h * (R(d1) * A0[i] + R(d3) * kget(1, M + i) +
+                                      R(d4) * kget(2, M + i) + R(d5) * kget(3, M + i) +
+                                      R(d6) * kget(0, M + i));
+                    if (!isfinite_(eq) || !isfinite_(ev)) nanFlag = true;
+                    const R dq = fabs_(q[i]) + fabs_(h * v[i]) + tiny;
+                    const R dv = fabs_(v[i]) + fabs_(h * A0[i]) + tiny;
                     qm[(2 * i) & 3].push(fabs(val(eq)), val(dq));
                     qm[(2 * i + 1) & 3].push(fabs(val(ev)), val(dv));
                 } else {
-                    fm[(2 * i) & 3] = fmax(fm[(2 * i) & 3], fabs(val(eq)) * rcp_fast(val(dq)));
-                    fm[(2 * i + 1) & 3] = fmax(fm[(2 * i + 1) & 3], fabs(val(ev)) * rcp_fast(val(dv)));
+                    const double eq = fma(hd6, val(kget(0, i)), fma(hd5, val(kget(3, i)),
+                                      fma(hd4, val(kget(2, i)), fma(hd3, val(kget(1, i)), hd1 * val(v[i])))));
+                    const double ev = fma(hd6, val(kget(0, M + i)), fma(hd5, val(kget(3, M + i)),
+                                      fma(hd4, val(kget(2, M + i)), fma(hd3, val(kget(1, M + i)), hd1 * val(A0[i])))));
+                    bad |= ((__double2hiint(eq) & 0x7ff00000) == 0x7ff00000) |
+                           ((__double2hiint(ev) & 0x7ff00000) == 0x7ff00000);
+                    const double dq = fma(hh, fabs(val(v[i])), fabs(val(q[i]))) + val(tiny);
+                    const double dv = fma(hh, fabs(val(A0[i])), fabs(val(v[i]))) + val(tiny);
+                    const int kq = (2 * i) & 3, kv = (2 * i + 1) & 3;
+                    if (fabs(eq) * mb[kq] > ma[kq] * dq) { ma[kq] = fabs(eq); mb[kq] = dq; }
+                    if (fabs(ev) * mb[kv] > ma[kv] * dv) { ma[kv] = fabs(ev); mb[kv] = dv; }
                 }
             }
-            qm[0].push(qm[1].a, qm[1].b);
-            qm[2].push(qm[3].a, qm[3].b);
-            qm[0].push(qm[2].a, qm[2].b);
-            const double fmx = fmax(fmax(fm[0], fm[1]), fmax(fm[2], fm[3]));
-            nanFlag = (__ballot_sync(0xffffffffu, nanFlag) & G.mask) != 0u;
             if constexpr (is_exact<R>::value) {
+                qm[0].push(qm[1].a, qm[1].b);
+                qm[2].push(qm[3].a, qm[3].b);
+                qm[0].push(qm[2].a, qm[2].b);
+                nanFlag = (__ballot_sync(0xffffffffu, nanFlag) & G.mask) != 0u;
                 qm[0].push(__shfl_xor_sync(0xffffffffu, qm[0].a, 1),
                            __shfl_xor_sync(0xffffffffu, qm[0].b, 1));
-                err = R(qm[0].value());
+                err = R(qm[0].value()) / eps;
             } else {
-                err = R(fmax(fmx, __shfl_xor_sync(0xffffffffu, fmx, 1)));
+#pragma unroll
+                for (int k = 1; k < 4; ++k)
+                    if (ma[k] * mb[0] > ma[0] * mb[k]) { ma[0] = ma[k]; mb[0] = mb[k]; }
+                nanFlag = (__ballot_sync(0xffffffffu, bad != 0) & G.mask) != 0u;
+                const double oa = __shfl_xor_sync(0xffffffffu, ma[0], 1);
+                const double ob = __shfl_xor_sync(0xffffffffu, mb[0], 1);
+                if (oa * mb[0] > ma[0] * ob) { ma[0] = oa; mb[0] = ob; }
+                err = R(ma[0] * rcp_fast(mb[0] * val(eps)));
             }
         }
-        err = err / eps;
 
         R hNew;
         bool accepted;
@@ -237,25 +278,38 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
                 accepted = false;
                 hNew = (!isfinite(err) || nanFlag)
                            ? tol.p1 * h
-                           : fmax(tol.safety * h * pow_fast(err, tol.pshrnk), tol.p1 * h);
+                           : fmax(tol.safety * h * ctrl_pow_fast(err, tol.pshrnk), tol.p1 * h);
             } else {
                 accepted = true;
                 const double hn =
-                    (err > tol.errcon) ? tol.safety * h * pow_fast(err, tol.pgrow) : 5.0 * h;
+                    (err > tol.errcon) ? tol.safety * h * ctrl_pow_fast(err, tol.pgrow) : 5.0 * h;
                 hNew = fmax(val(hMin), fmin(val(hMax), hn));
             }
         }
         if (live && accepted) {
             t += h;
             stats_accept(st, val(h));
+            if constexpr (is_exact<R>::value) {
 #pragma unroll
-            for (int i = 0; i < M; ++i)
-                q[i] = q[i] + h * (R(c1) * v[i] + R(c3) * kget(1, i) + R(c4) * kget(2, i) +
-                                   R(c6) * kget(0, i));
+                for (int i = 0; i < M; ++i)
+                    q[i] = q[i] + h * (R(c1) * v[i] + R(c3) * kget(1, i) + R(c4) * kget(2, i) +
+                                       R(c6) * kget(0, i));
 #pragma unroll
-            for (int i = 0; i < M; ++i)
-                v[i] = v[i] + h * (R(c1) * A0[i] + R(c3) * kget(1, M + i) +
-                                   R(c4) * kget(2, M + i) + R(c6) * kget(0, M + i));
+                for (int i = 0; i < M; ++i)
+                    v[i] = v[i] + h * (R(c1) * A0[i] + R(c3) * kget(1, M + i) +
+                                       R(c4) * kget(2, M + i) + R(c6) * kget(0, M + i));
+            } else {  // FAST: h folded into the weights
+                const double hh = val(h);
+                const double hc1 = hh * c1, hc3 = hh * c3, hc4 = hh * c4, hc6 = hh * c6;
+#pragma unroll
+                for (int i = 0; i < M; ++i)
+                    q[i] = R(fma(hc6, val(kget(0, i)), fma(hc4, val(kget(2, i)),
+                             fma(hc3, val(kget(1, i)), fma(hc1, val(v[i]), val(q[i]))))));
+#pragma unroll
+                for (int i = 0; i < M; ++i)
+                    v[i] = R(fma(hc6, val(kget(0, M + i)), fma(hc4, val(kget(2, M + i)),
+                             fma(hc3, val(kget(1, M + i)), fma(hc1, val(A0[i]), val(v[i]))))));
+            }
             haveF = false;
             h = hNew;
         } else if (live) {

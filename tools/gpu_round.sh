@@ -15,7 +15,7 @@ for p in $PARTS; do
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1; echo "smoke rc=$?" >> $OUT/status.txt ;;
     bench) timeout 900 python bench.py > $OUT/bench.txt 2>&1; echo "bench rc=$?" >> $OUT/status.txt ;;
     ab_lanes)
-      for L in 1 2 8; do BODE_LANES=$L timeout 600 python bench.py --no-e2e --no-cpu --steps 5 > $OUT/bench_lanes$L.txt 2>&1; done
+      for L in 1 2; do BODE_LANES=$L timeout 600 python bench.py --no-e2e --no-cpu --steps 5 > $OUT/bench_lanes$L.txt 2>&1; done
       echo "ab_lanes rc=$?" >> $OUT/status.txt ;;
     ncu_rkc)
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:Heat \
@@ -35,6 +35,8 @@ for p in $PARTS; do
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/bench_static.txt 2>&1
       for T in 4 8 16; do BODE_REFILL_MIN=$T timeout 600 python bench.py --persistent --no-e2e --no-cpu --no-secondary > $OUT/bench_persistent$T.txt 2>&1; done
       echo "ab_persist rc=$?" >> $OUT/status.txt ;;
+    tfast) timeout 900 python -m pytest tests -x -q -m gpu -k "fast or persistent or block_size" > $OUT/pytest_fast.txt 2>&1; echo "tfast rc=$?" >> $OUT/status.txt ;;
+    qfast) timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1; echo "qfast rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
