@@ -224,6 +224,8 @@ def main():
     ap.add_argument("--no-secondary", dest="secondary", action="store_false",
                     help="skip the EXACT / RKC measurements")
     ap.add_argument("--cpu-sample", type=int, default=1 << 15)
+    ap.add_argument("--block", type=int, default=0,
+                    help="threads per block override (0: each kernel's default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -250,6 +252,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L = P.lib()
     L.bode_set_persistent(1 if args.persistent else 0)
+    P.api.check(L.bode_set_block_size(args.block))
     stream = torch.cuda.Stream()
 
     peak = ctypes.c_double()

@@ -37,6 +37,7 @@ using LaunchPersistentFn = void (*)(const void* fn, dim3 grid, dim3 block, size_
 struct KernelEntry {
     int kind, dim, param_dim, solver, arith;
     int lanes;            // lanes per system (L)
+    int maxreg;           // register cap of this instance (0: ptxas default, up to 255)
     int smem_per_thread;  // dynamic shared memory bytes per thread
     int default_block;
     const void* fn;

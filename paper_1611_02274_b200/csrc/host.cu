@@ -149,12 +149,19 @@ const KernelEntry* find_entry(const bode_problem_t* p, int solver, int arith) {
         const char* s = std::getenv("BODE_LANES");
         return s ? std::atoi(s) : 0;
     }();
+    static const int want_maxreg = [] {  // BODE_MAXREG=<cap> (255 = uncapped)
+        const char* s = std::getenv("BODE_MAXREG");
+        return s ? std::atoi(s) : -1;
+    }();
     const KernelEntry* first = nullptr;
     for (int i = 0; i < n; ++i) {
         const KernelEntry& e = tab[i];
         if (e.kind == p->kind && e.dim == p->dim && e.param_dim == p->param_dim &&
             e.solver == solver && e.arith == arith) {
-            if (want_lanes == 0 || e.lanes == want_lanes) return &e;
+            const int cap = e.maxreg > 0 ? e.maxreg : 255;
+            if ((want_lanes == 0 || e.lanes == want_lanes) &&
+                (want_maxreg < 0 || cap == want_maxreg))
+                return &e;
             if (!first) first = &e;
         }
     }

@@ -1,0 +1,144 @@
+// kernel_entry.cuh -- the intDriver kernel templates and
+// their dispatch-table entries, shared by the built-in table (kernels.cu) and
+// by problems registered through include/bode_problem.cuh.
+//
+// One lane group (L lanes) integrates one system over one window [t, tEnd]:
+// coalesced SoA load of y[i + num*j] (batch.hpp:15-29), the
+// fused solver (rkck*.cuh / rkc.cuh), SoA store, per-system stats (AoS).
+// All arithmetic is FP64 on the CUDA cores; nothing here is a contraction,
+// so there are no tensor cores on this path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "dispatch.h"
+#include "rkc.cuh"
+#include "rkck_nystrom.cuh"
+#include "rkck_pleiades2.cuh"
+#include "fixed.cuh"
+
+namespace bode {
+
+// Global component held by lane `lane` of a group in local slot c. Blocks of
+// C consecutive components by default; the 2-lane Pleiades split is by axis:
+// lane l holds positions [7l, 7l+7) and velocities [14+7l, 14+7l+7).
+template <class P, int L>
+__device__ __forceinline__ int comp_index(int lane, int c) {
+    constexpr int C = P::N / L;
+    if constexpr (is_second_order<P>::value && L == 2)
+        return c < 7 ? 7 * lane + c : 14 + 7 * lane + (c - 7);
+    else
+        return lane * C + c;
+}
+
+// MAXREG > 0 caps registers per thread (__maxnreg__) to reach a target
+// occupancy; 0 leaves ptxas the full 255 (launch bound kMaxBlock threads).
+template <class P, class R, int L, int SOLVER, bool KSMEM, int MAXREG>
+__global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
+    integrate_kernel(const double* __restrict__ g_soa, double* __restrict__ y_soa,
+                     DevStats* __restrict__ stats, long long num, double t, double tEnd,
+                     DevTol tol, int merge) {
+    constexpr int C = P::N / L;
+    constexpr int PP = P::P > 0 ? P::P : 1;
+    const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long sys = gt / L;
+    if (sys >= num) return;  // whole lane groups retire together
+    Group<L> G;
+    R y[C];
+    R g[PP];
+#pragma unroll
+    for (int c = 0; c < C; ++c) y[c] = R(y_soa[sys + num * (long long)comp_index<P, L>(G.lane, c)]);
+#pragma unroll
+    for (int p = 0; p < PP; ++p) g[p] = R(P::P > 0 ? g_soa[sys + num * (long long)p] : 0.0);
+    DevStats st;
+    if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 2)
+        rkck_pleiades2_system<R>(G, t, tEnd, y, tol, st);
+    else if constexpr (SOLVER == 0 && is_second_order<P>::value)
+        rkck_nystrom_system<P, R>(t, tEnd, y, tol, st);
+    else if constexpr (SOLVER == 0)
+        rkck_system<P, R, L, KSMEM>(G, t, tEnd, y, g, tol, st);
+    else
+        rkc_system<P, R, L>(G, t, tEnd, y, g, tol, st);
+#pragma unroll
+    for (int c = 0; c < C; ++c) y_soa[sys + num * (long long)comp_index<P, L>(G.lane, c)] = val(y[c]);
+    if (stats != nullptr && G.lane == 0) {
+        if (merge) {
+            DevStats o = stats[sys];
+            stats_merge(o, st);
+            stats[sys] = o;
+        } else {
+            stats[sys] = st;
+        }
+    }
+}
+
+// Persistent-grid RKCK for second-order problems, one lane per system.
+template <class P, class R>
+__global__ void __launch_bounds__(kMaxBlock)
+    persistent_kernel(const double* __restrict__ g_soa, double* __restrict__ y_soa,
+                      DevStats* __restrict__ stats, long long num, double t, double tEnd,
+                      DevTol tol, int merge, unsigned long long* counter) {
+    rkck_nystrom_persistent<P, R>(g_soa, y_soa, stats, num, t, tEnd, tol, merge, counter,
+                                  tol.refill_min);
+}
+
+// ---- dispatch table ----
+template <class P, class R, int L, int SOLVER, bool KSMEM, int MAXREG>
+static KernelEntry make_entry(int kind, int arith) {
+    KernelEntry e;
+    e.kind = kind;
+    e.dim = P::N;
+    e.param_dim = P::P;
+    e.solver = SOLVER;
+    e.arith = arith;
+    e.lanes = L;
+    e.maxreg = MAXREG;
+    e.smem_per_thread = SOLVER == 1 ? kRkcSmemStride<C_of<P, L>()>() * (int)sizeof(double)
+                        : KSMEM     ? kSmemStride<C_of<P, L>()>() * (int)sizeof(double)
+                                    : 0;
+    e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG>;
+    e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                  const double* g, double* y, DevStats* st, long long num, double t,
+                  double tEnd, DevTol tol, int merge) {
+        auto k = (void (*)(const double*, double*, DevStats*, long long, double, double, DevTol,
+                           int))fn;
+        k<<<grid, block, smem, s>>>(g, y, st, num, t, tEnd, tol, merge);
+    };
+    e.default_block = KSMEM ? 128 : 128;
+    e.build_rkc_table = nullptr;
+    if constexpr (!(SOLVER == 0 && is_second_order<P>::value && L == 2)) {
+        e.ffn = (const void*)&fixed_kernel<P, R, L, SOLVER>;
+        e.launch_fixed = [](const void* fn, dim3 grid, dim3 block, cudaStream_t s,
+                            const double* g, double* y, long long num, double t0, double tEnd,
+                            long long numSteps, long long stages, double kappa) {
+            auto k = (void (*)(const double*, double*, long long, double, double, long long,
+                               long long, double))fn;
+            k<<<grid, block, 0, s>>>(g, y, num, t0, tEnd, numSteps, stages, kappa);
+        };
+    }
+    if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1) {
+        // (routing static launches through this instance with counter == nullptr
+        // removes the spills but measured 9% slower: the any_sync loop costs more)
+        e.pfn = (const void*)&persistent_kernel<P, R>;
+        e.launch_persistent = [](const void* fn, dim3 grid, dim3 block, size_t smem,
+                                 cudaStream_t s, const double* g, double* y, DevStats* st,
+                                 long long num, double t, double tEnd, DevTol tol, int merge,
+                                 unsigned long long* counter) {
+            auto k = (void (*)(const double*, double*, DevStats*, long long, double, double,
+                               DevTol, int, unsigned long long*))fn;
+            k<<<grid, block, smem, s>>>(g, y, st, num, t, tEnd, tol, merge, counter);
+        };
+    }
+    if constexpr (SOLVER == 1)
+        e.build_rkc_table = [](double* tab, double kappa, cudaStream_t s) {
+            rkc_coef_table_kernel<R><<<(unsigned)((kRkcTableMaxS + 63) / 64), 64, 0, s>>>(tab, kappa);
+        };
+    return e;
+}
+
+#define BODE_BOTH_ARITH_R(P, L, SOLVER, KSMEM, KIND, MAXREG)                  \
+    make_entry<P, xd, L, SOLVER, KSMEM, MAXREG>(KIND, 0),                    \
+        make_entry<P, double, L, SOLVER, KSMEM, MAXREG>(KIND, 1)
+#define BODE_BOTH_ARITH(P, L, SOLVER, KSMEM, KIND) BODE_BOTH_ARITH_R(P, L, SOLVER, KSMEM, KIND, 0)
+
+}  // namespace bode

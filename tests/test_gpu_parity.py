@@ -284,3 +284,46 @@ def test_rkc_heat64_2_20_stride(gpu, oracle):
     assert np.array_equal(got.view(np.uint64), yo.view(np.uint64))
     for k in COUNTS + ("stages_total",):
         assert np.array_equal(st[k][idx], so[k]), k
+
+
+def test_very_stiff_generator_path_bitwise(gpu, oracle):
+    """expDecay with g0 log-uniform in [1e9, 1e11]: about 1700 stages per step,
+    far above the per-device coefficient table (s <= 160), so the chunked
+    on-the-fly generator path of rkc.cuh runs; states and counters stay bitwise.
+    (The oracle rebuilds the coefficients per stage like the reference, O(s^2)
+    per step, hence the small batch.)"""
+    num = 8
+    prob = A.make_problem(A.EXPDECAY)
+    u = np.linspace(-1.0, 1.0, num)
+    g = 10.0 ** (10.0 + u)
+    y0 = 1.0 + 0.5 * u
+    y, st = run_gpu(prob, A.SOLVER_RKC, y0, g, "exact", t1=0.1)
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKC, 0.0, 0.1, 0.1, y0, g)
+    assert np.array_equal(y.view(np.uint64), yo.view(np.uint64))
+    for k in COUNTS + ("stages_total",):
+        assert np.array_equal(st[k], so[k]), k
+    per_step = st["stages_total"] / np.maximum(st["steps_accepted"] + st["steps_rejected"], 1)
+    assert per_step.max() > 160, per_step.max()
+
+
+@pytest.mark.parametrize("env", [("4", "255"), ("8", "168"), ("8", "128"), ("8", "96"), ("16", "96"), ("16", "128")])
+def test_heat64_lane_variants_bitwise(gpu, oracle, env):
+    """Every compiled heat64 RKC instance (lanes per system x register cap,
+    selected with BODE_LANES / BODE_MAXREG) gives the oracle's bits."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, 'tests'); import numpy as np;"
+            "from test_gpu_parity import run_gpu; from golden_cases import heat_ic, perturb;"
+            "from paper_1611_02274_b200 import _abi as A;"
+            "p = A.make_problem(A.HEAT, 64); y0 = perturb(heat_ic(64), 0.01, 42, 2048);"
+            "y, st = run_gpu(p, A.SOLVER_RKC, y0, None, 'exact');"
+            "np.save(sys.argv[1], y)")
+    out = os.path.join(os.environ.get("TMPDIR", "/tmp"), f"heat_variant_{env[0]}_{env[1]}.npy")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code, out], cwd=repo, capture_output=True, text=True,
+                       env=dict(os.environ, BODE_LANES=env[0], BODE_MAXREG=env[1]))
+    assert r.returncode == 0, r.stderr[-2000:]
+    prob = A.make_problem(A.HEAT, 64)
+    y0 = perturb(heat_ic(64), 0.01, 42, 2048)
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKC, 0.0, 1.0, 0.1, y0)
+    assert np.array_equal(np.load(out).view(np.uint64), yo.view(np.uint64))

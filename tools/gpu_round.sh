@@ -37,6 +37,15 @@ for p in $PARTS; do
       echo "ab_persist rc=$?" >> $OUT/status.txt ;;
     tfast) timeout 900 python -m pytest tests -x -q -m gpu -k "fast or persistent or block_size" > $OUT/pytest_fast.txt 2>&1; echo "tfast rc=$?" >> $OUT/status.txt ;;
     qfast) timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1; echo "qfast rc=$?" >> $OUT/status.txt ;;
+    ab_block)
+      for B in 32 64 128; do timeout 600 python bench.py --no-e2e --no-cpu --no-secondary --block $B > $OUT/bench_block$B.txt 2>&1; done
+      for B in 32 64; do timeout 600 python bench.py --no-e2e --no-cpu --no-secondary --block $B --persistent > $OUT/bench_pblock$B.txt 2>&1; done
+      echo "ab_block rc=$?" >> $OUT/status.txt ;;
+    ab_rkc)
+      for V in "8 128" "8 96" "16 96" "16 128"; do set -- $V
+        BODE_LANES=$1 BODE_MAXREG=$2 timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --num 1048576 --rkc-num 1048576 > $OUT/bench_rkc_L$1_R$2.txt 2>&1; done
+      for R in 96 80; do BODE_LANES=1 BODE_MAXREG=$R timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --num 1048576 --rkc-num 1048576 > $OUT/bench_rkc_exp$R.txt 2>&1; done
+      echo "ab_rkc rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
