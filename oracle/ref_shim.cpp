@@ -63,6 +63,31 @@ OdeProblem makeProblem(const bode_problem_t* p) {
             q.rhs = [](double t, std::span<const double> y, std::span<const double>,
                        std::span<double> out) { out[0] = std::sin(t) * y[0]; };
             break;
+        case BODE_PROBLEM_BRUSSELATOR:
+            // Not a reference problem: the host form of the device Brusselator
+            // (paper_1611_02274_b200/csrc/problems_ext.cu), written as a user of
+            // the reference would write an OdeProblem, so the reference drivers
+            // integrate it. y = (u_1, v_1, ..., u_n, v_n), g = (A, B, alpha),
+            // boundary values (A, B/A), stencil (1, -2, 1)/dx^2, dx = 1/(n+1).
+            q.rhs = [](double, std::span<const double> y, std::span<const double> g,
+                       std::span<double> out) {
+                const int n = static_cast<int>(y.size()) / 2;
+                const double A = g[0], B = g[1], alpha = g[2];
+                const double dx = 1.0 / (n + 1);
+                const double c = alpha / (dx * dx);
+                const double ub = A, vb = B / A;
+                for (int i = 0; i < n; ++i) {
+                    const double u = y[2 * i], v = y[2 * i + 1];
+                    const double uL = i > 0 ? y[2 * i - 2] : ub;
+                    const double vL = i > 0 ? y[2 * i - 1] : vb;
+                    const double uR = i < n - 1 ? y[2 * i + 2] : ub;
+                    const double vR = i < n - 1 ? y[2 * i + 3] : vb;
+                    const double uuv = u * u * v;
+                    out[2 * i] = A + uuv - (B + 1.0) * u + c * (uL - 2.0 * u + uR);
+                    out[2 * i + 1] = B * u - uuv + c * (vL - 2.0 * v + vR);
+                }
+            };
+            break;
         default: break;
     }
     return q;
@@ -159,6 +184,33 @@ int ref_integrate_batch(const bode_problem_t* p, int solver, double t, double tN
         std::memcpy(y, r.states.values.data(), sizeof(double) * r.states.values.size());
         if (stats)
             for (int64_t i = 0; i < num; ++i) toStats(r.stats[i], &stats[i], -1);
+    });
+}
+
+// batchode::outerLoop on an OdeProblem whose rhs is a C function pointer:
+// the oracle for problems registered from user libraries, whose host form
+// the library exports (e.g. examples/user_problem.cu).
+typedef void (*ref_rhs_fn)(double t, const double* y, const double* g, double* out);
+int ref_outer_loop_fn(ref_rhs_fn rhs, int dim, int param_dim, int solver, double t0,
+                      double tEnd, double hOuter, int64_t num, double* y, const double* g,
+                      const bode_tol_t* tol, bode_stats_t* stats, int workers,
+                      int* outerSteps) {
+    return guarded([&] {
+        bode_problem_t p{BODE_PROBLEM_USER_BASE, dim, param_dim, 0};
+        const BatchStates b = toBatch(&p, num, y, g);
+        OdeProblem q;
+        q.dim = dim;
+        q.paramDim = param_dim;
+        q.rhs = [rhs](double t, std::span<const double> yy, std::span<const double> gg,
+                      std::span<double> out) { rhs(t, yy.data(), gg.data(), out.data()); };
+        const OuterLoopResult r =
+            outerLoop(q, b, t0, tEnd, hOuter,
+                      solver == BODE_SOLVER_RKCK ? SolverChoice::RKCK : SolverChoice::RKC,
+                      toTol(tol), workers, {});
+        std::memcpy(y, r.states.values.data(), sizeof(double) * r.states.values.size());
+        if (stats)
+            for (int64_t i = 0; i < num; ++i) toStats(r.stats[i], &stats[i], -1);
+        if (outerSteps) *outerSteps = r.outerSteps;
     });
 }
 

@@ -34,10 +34,13 @@ RICCATI = 5
 DIAG = 6
 CONST = 7
 SINT = 8
+BRUSSELATOR = 9  # registered through include/bode_problem.cuh (csrc/problems_ext.cu)
+USER_BASE = 1000
 
 PROBLEM_NAMES = {
     "pleiades": PLEIADES, "heat": HEAT, "expdecay": EXPDECAY, "harmonic": HARMONIC,
     "zero": ZERO, "riccati": RICCATI, "diag": DIAG, "const": CONST, "sint": SINT,
+    "brusselator": BRUSSELATOR,
 }
 SOLVER_NAMES = {"rkck": SOLVER_RKCK, "rkc": SOLVER_RKC}
 ARITH_NAMES = {"exact": ARITH_EXACT, "fast": ARITH_FAST}
@@ -93,6 +96,8 @@ def make_problem(kind, dim: int = 0) -> Problem:
         d, p = (dim or 64), 0
     elif kind == DIAG:
         d, p = dim, dim
+    elif kind == BRUSSELATOR:
+        d, p = (dim or 64), 3
     else:
         d, p = dim, 0
     return Problem(kind=kind, dim=d, param_dim=p, reserved=0)

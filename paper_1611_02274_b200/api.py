@@ -94,6 +94,8 @@ def lib():
         "bode_set_block_size": (ctypes.c_int, [c_i32]),
         "bode_launch_count": (c_i64, []),
         "bode_set_persistent": (ctypes.c_int, [c_i32]),
+        "bode_register_kernels": (ctypes.c_int, [vp, c_i32, c_i32]),
+        "bode_registered_count": (ctypes.c_int, []),
         "bode_integrate_fixed": (ctypes.c_int, [P(A.Problem), c_i32, c_i32, c_d, c_d, c_i64,
                                                 c_i32, c_d, c_i64, PD, PD]),
         "bode_splitmix64_at": (c_u64, [c_u64, c_u64]),
@@ -113,6 +115,26 @@ def lib():
         f.argtypes = args
     _LIB = L
     return L
+
+
+def load_problem_library(path: str) -> ctypes.CDLL:
+    """Loads a problem library built against include/bode_problem.cuh (after
+    libbode): its static initializer registers the problem's kernels with
+    bode_register_kernels, so its kind is accepted everywhere afterwards."""
+    L = lib()
+    before = L.bode_registered_count()
+    h = ctypes.CDLL(os.path.abspath(path))
+    if L.bode_registered_count() <= before:
+        raise Unsupported(f"{path}: no kernels registered "
+                          f"({L.bode_last_error().decode(errors='replace')})")
+    return h
+
+
+def problem(kind: int, dim: int = 0) -> "OdeProblem":
+    """OdeProblem for a built-in or registered kind (bode_problem_init)."""
+    p = A.Problem()
+    check(lib().bode_problem_init(ctypes.byref(p), int(kind), int(dim)))
+    return OdeProblem(p.kind, p.dim, p.param_dim)
 
 
 def check(rc: int):

@@ -34,7 +34,7 @@ def _sources():
 
 def _headers():
     return (glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
-            + glob.glob(os.path.join(INCLUDE, "*.h")))
+            + glob.glob(os.path.join(INCLUDE, "*.h")) + glob.glob(os.path.join(INCLUDE, "*.cuh")))
 
 
 def _stale(target, deps):
@@ -80,8 +80,22 @@ def build(force: bool = False, verbose: bool = True) -> str:
 
 
 def build_examples(verbose: bool = True):
-    """C++ drop-in example (examples/*.cpp) linked against libbode.so."""
+    """C++ drop-in example (examples/*.cpp) linked against libbode.so, and the
+    out-of-tree problem libraries (examples/*.cu -> lib/lib<name>.so)."""
     repo = os.path.dirname(PKG)
+    for src in glob.glob(os.path.join(repo, "examples", "*.cu")):
+        so = os.path.join(LIB_DIR, "lib" + os.path.splitext(os.path.basename(src))[0] + ".so")
+        if not _stale(so, [src, SO] + _headers() + [os.path.join(INCLUDE, "bode_problem.cuh")]):
+            continue
+        cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-Xptxas", "-v", src, "-L", LIB_DIR, "-lbode",
+               "-Xlinker", f"-rpath,{LIB_DIR}", "-Xlinker", "-rpath,$ORIGIN", "-o", so]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"problem library build failed for {src}:\n{r.stderr}")
+        with open(os.path.join(OBJ_DIR, os.path.basename(src) + ".ptxas.txt"), "w") as f:
+            f.write(r.stderr)
+        if verbose:
+            print(f"[bode build] built {so}", flush=True)
     for src in glob.glob(os.path.join(repo, "examples", "*.cpp")):
         exe = os.path.join(LIB_DIR, os.path.splitext(os.path.basename(src))[0])
         if not _stale(exe, [src, SO, os.path.join(INCLUDE, "bode.hpp")]):

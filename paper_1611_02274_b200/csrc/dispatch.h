@@ -25,11 +25,12 @@ static_assert(sizeof(DevStats) == 64, "DevStats must match bode_stats_t");
 template <class P, int L>
 constexpr int C_of() { return P::N / L; }
 
-using LaunchFn = void (*)(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+// Launchers return the launching runtime's cudaGetLastError() as an int.
+using LaunchFn = int (*)(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                           const double* g, double* y, DevStats* st, long long num, double t,
                           double tEnd, DevTol tol, int merge);
 
-using LaunchPersistentFn = void (*)(const void* fn, dim3 grid, dim3 block, size_t smem,
+using LaunchPersistentFn = int (*)(const void* fn, dim3 grid, dim3 block, size_t smem,
                                     cudaStream_t s, const double* g, double* y, DevStats* st,
                                     long long num, double t, double tEnd, DevTol tol, int merge,
                                     unsigned long long* counter);
@@ -42,14 +43,18 @@ struct KernelEntry {
     int default_block;
     const void* fn;
     LaunchFn launch;
-    void (*build_rkc_table)(double* tab, double kappa, cudaStream_t s);  // null for RKCK
+    int (*build_rkc_table)(double* tab, double kappa, cudaStream_t s);  // null for RKCK
     // persistent variant with dynamic refill (null if none): a grid sized to the
     // resident capacity whose lanes claim systems from `counter`
     const void* pfn = nullptr;
     LaunchPersistentFn launch_persistent = nullptr;
+    // Makes `device` current and raises fn's dynamic shared-memory limit to
+    // smem_bytes, in the CUDA runtime of the translation unit that compiled the
+    // kernel (a problem registered from another library carries its own).
+    int (*prepare)(const void* fn, int device, int smem_bytes) = nullptr;
     // fixed-step harness (integrateFixed) for this problem/solver/policy
     const void* ffn = nullptr;
-    void (*launch_fixed)(const void* fn, dim3 grid, dim3 block, cudaStream_t s, const double* g,
+    int (*launch_fixed)(const void* fn, dim3 grid, dim3 block, cudaStream_t s, const double* g,
                          double* y, long long num, double t0, double tEnd, long long numSteps,
                          long long stages, double kappa) = nullptr;
 };

@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -142,6 +143,34 @@ const std::vector<double>& host_powtab() {
 // widths may be compiled for one problem; BODE_LANES=<L> (tuning knob, e.g.
 // for A/B measurements) prefers the variant with that width. All variants
 // give bitwise-identical results.
+// Kernels registered at load time by problem libraries built against
+// include/bode_problem.cuh (bode_register_kernels). Function-local statics, so
+// registration from another library's static initializers is order-safe.
+std::mutex& registry_mutex() {
+    static std::mutex m;
+    return m;
+}
+std::deque<KernelEntry>& registry() {  // deque: entries never move once added
+    static std::deque<KernelEntry>* v = new std::deque<KernelEntry>();
+    return *v;
+}
+
+template <class Seq>
+const KernelEntry* find_in(const Seq& tab, const bode_problem_t* p, int solver, int arith,
+                           int want_lanes, int want_maxreg, const KernelEntry** first) {
+    for (const KernelEntry& e : tab) {
+        if (e.kind == p->kind && e.dim == p->dim && e.param_dim == p->param_dim &&
+            e.solver == solver && e.arith == arith) {
+            const int cap = e.maxreg > 0 ? e.maxreg : 255;
+            if ((want_lanes == 0 || e.lanes == want_lanes) &&
+                (want_maxreg < 0 || cap == want_maxreg))
+                return &e;
+            if (!*first) *first = &e;
+        }
+    }
+    return nullptr;
+}
+
 const KernelEntry* find_entry(const bode_problem_t* p, int solver, int arith) {
     int n = 0;
     const KernelEntry* tab = bode::kernel_table(&n);
@@ -153,18 +182,19 @@ const KernelEntry* find_entry(const bode_problem_t* p, int solver, int arith) {
         const char* s = std::getenv("BODE_MAXREG");
         return s ? std::atoi(s) : -1;
     }();
+    struct Span {
+        const KernelEntry *b, *e;
+        const KernelEntry* begin() const { return b; }
+        const KernelEntry* end() const { return e; }
+    };
     const KernelEntry* first = nullptr;
-    for (int i = 0; i < n; ++i) {
-        const KernelEntry& e = tab[i];
-        if (e.kind == p->kind && e.dim == p->dim && e.param_dim == p->param_dim &&
-            e.solver == solver && e.arith == arith) {
-            const int cap = e.maxreg > 0 ? e.maxreg : 255;
-            if ((want_lanes == 0 || e.lanes == want_lanes) &&
-                (want_maxreg < 0 || cap == want_maxreg))
-                return &e;
-            if (!first) first = &e;
-        }
-    }
+    if (const KernelEntry* e =
+            find_in(Span{tab, tab + n}, p, solver, arith, want_lanes, want_maxreg, &first))
+        return e;
+    std::lock_guard<std::mutex> lock(registry_mutex());
+    if (const KernelEntry* e =
+            find_in(registry(), p, solver, arith, want_lanes, want_maxreg, &first))
+        return e;
     return first;
 }
 
@@ -221,8 +251,8 @@ int rkc_table_for(const KernelEntry* e, double kappa, cudaStream_t s, const doub
         }
     double* tab = nullptr;
     BODE_CUDA(cudaMalloc(&tab, bode::rkc_table_doubles() * sizeof(double)));
-    e->build_rkc_table(tab, kappa, s);
-    BODE_CUDA(cudaGetLastError());
+    BODE_CUDA((cudaError_t)e->prepare(e->fn, dev, 0));
+    BODE_CUDA((cudaError_t)e->build_rkc_table(tab, kappa, s));
     BODE_CUDA(cudaStreamSynchronize(s));
     cache.push_back({dev, e->arith, kappa, tab});
     *out = tab;
@@ -270,10 +300,12 @@ int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double*
     const size_t smem = (size_t)e->smem_per_thread * block;
     const bool persistent = e->launch_persistent != nullptr && g_persistent.load();
     const void* fn = persistent ? e->pfn : e->fn;
-    if (smem > 48 * 1024) {
-        // per-device attribute; idempotent and cheap, so set it on every launch
-        BODE_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
+    {
+        // current device and the per-device smem attribute, in the runtime that
+        // owns the kernel (idempotent and cheap, so done on every launch)
+        int dev = 0;
+        BODE_CUDA(cudaGetDevice(&dev));
+        BODE_CUDA((cudaError_t)e->prepare(fn, dev, (int)smem));
     }
     if (persistent) {
         int dev = 0, sms = 0, per_sm = 0;
@@ -284,11 +316,12 @@ int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double*
         unsigned long long* counter = nullptr;
         int rc = claim_counter(s, &counter);
         if (rc) return rc;
-        e->launch_persistent(fn, dim3((unsigned)pgrid), dim3(block), smem, s, g, y, st, num, t,
-                             tEnd, tol, merge, counter);
+        BODE_CUDA((cudaError_t)e->launch_persistent(fn, dim3((unsigned)pgrid), dim3(block), smem,
+                                                    s, g, y, st, num, t, tEnd, tol, merge,
+                                                    counter));
     } else {
-        e->launch(fn, dim3((unsigned)grid), dim3(block), smem, s, g, y, st, num, t, tEnd, tol,
-                  merge);
+        BODE_CUDA((cudaError_t)e->launch(fn, dim3((unsigned)grid), dim3(block), smem, s, g, y, st,
+                                         num, t, tEnd, tol, merge));
     }
     g_launches.fetch_add(1);
     BODE_CUDA(cudaGetLastError());
@@ -507,9 +540,47 @@ int bode_problem_init(bode_problem_t* p, int32_t kind, int32_t dim) {
         case BODE_PROBLEM_CONST:
             if (dim < 1) return fail(BODE_E_INVALID_SHAPE, "dim must be positive");
             p->dim = dim; p->param_dim = 0; break;
-        default: return fail(BODE_E_INVALID_SHAPE, "unknown problem kind");
+        default: {  // a registered problem: dim/param_dim from its kernels
+            std::lock_guard<std::mutex> lock(registry_mutex());
+            const KernelEntry* hit = nullptr;
+            for (const KernelEntry& e : registry())
+                if (e.kind == kind && (dim <= 0 || e.dim == dim)) {
+                    hit = &e;
+                    break;
+                }
+            if (hit == nullptr) return fail(BODE_E_INVALID_SHAPE, "unknown problem kind");
+            p->dim = hit->dim;
+            p->param_dim = hit->param_dim;
+        }
     }
     return BODE_OK;
+}
+
+int bode_register_kernels(const void* table, int32_t count, int32_t entry_bytes) {
+    if (table == nullptr || count < 1)
+        return fail(BODE_E_INVALID_SHAPE, "bode_register_kernels: empty table");
+    if (entry_bytes != (int32_t)sizeof(KernelEntry))
+        return fail(BODE_E_UNSUPPORTED,
+                    "bode_register_kernels: entry layout differs from this libbode "
+                    "(rebuild the problem library against this include/)");
+    const KernelEntry* es = static_cast<const KernelEntry*>(table);
+    for (int32_t i = 0; i < count; ++i) {
+        const KernelEntry& e = es[i];
+        if (e.fn == nullptr || e.launch == nullptr || e.prepare == nullptr || e.dim < 1 ||
+            e.param_dim < 0 || e.lanes < 1 || 32 % e.lanes != 0 || e.dim % e.lanes != 0 ||
+            (e.solver != BODE_SOLVER_RKCK && e.solver != BODE_SOLVER_RKC) ||
+            (e.arith != BODE_ARITH_EXACT && e.arith != BODE_ARITH_FAST) ||
+            (e.solver == BODE_SOLVER_RKC && e.build_rkc_table == nullptr))
+            return fail(BODE_E_INVALID_SHAPE, "bode_register_kernels: malformed entry");
+    }
+    std::lock_guard<std::mutex> lock(registry_mutex());
+    for (int32_t i = 0; i < count; ++i) registry().push_back(es[i]);
+    return BODE_OK;
+}
+
+int bode_registered_count(void) {
+    std::lock_guard<std::mutex> lock(registry_mutex());
+    return (int)registry().size();
 }
 
 int bode_problem_supported(const bode_problem_t* p, int32_t solver, int32_t arith) {
@@ -670,10 +741,10 @@ int bode_integrate_fixed(const bode_problem_t* p, int32_t solver, int32_t arith,
     if (P > 0) BODE_CUDA(cudaMemcpy(dg, g, (size_t)num * P * sizeof(double), cudaMemcpyHostToDevice));
     const int block = 128;
     const long long grid = (num * e->lanes + block - 1) / block;
-    e->launch_fixed(e->ffn, dim3((unsigned)grid), dim3(block), 0, dg, dy, num, t0, t_end,
-                    num_steps, stages, kappa);
+    BODE_CUDA((cudaError_t)e->prepare(e->ffn, 0, 0));
+    BODE_CUDA((cudaError_t)e->launch_fixed(e->ffn, dim3((unsigned)grid), dim3(block), 0, dg, dy,
+                                           num, t0, t_end, num_steps, stages, kappa));
     g_launches.fetch_add(1);
-    BODE_CUDA(cudaGetLastError());
     BODE_CUDA(cudaMemcpy(y, dy, (size_t)num * N * sizeof(double), cudaMemcpyDeviceToHost));
     cudaFree(dy);
     if (dg) cudaFree(dg);

@@ -99,21 +99,29 @@ static KernelEntry make_entry(int kind, int arith) {
     e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG>;
     e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                   const double* g, double* y, DevStats* st, long long num, double t,
-                  double tEnd, DevTol tol, int merge) {
+                  double tEnd, DevTol tol, int merge) -> int {
         auto k = (void (*)(const double*, double*, DevStats*, long long, double, double, DevTol,
                            int))fn;
         k<<<grid, block, smem, s>>>(g, y, st, num, t, tEnd, tol, merge);
+        return (int)cudaGetLastError();
     };
     e.default_block = KSMEM ? 128 : 128;
+    e.prepare = [](const void* fn, int device, int smem_bytes) -> int {
+        cudaError_t err = cudaSetDevice(device);
+        if (err == cudaSuccess && smem_bytes > 48 * 1024)
+            err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+        return (int)err;
+    };
     e.build_rkc_table = nullptr;
     if constexpr (!(SOLVER == 0 && is_second_order<P>::value && L == 2)) {
         e.ffn = (const void*)&fixed_kernel<P, R, L, SOLVER>;
         e.launch_fixed = [](const void* fn, dim3 grid, dim3 block, cudaStream_t s,
                             const double* g, double* y, long long num, double t0, double tEnd,
-                            long long numSteps, long long stages, double kappa) {
+                            long long numSteps, long long stages, double kappa) -> int {
             auto k = (void (*)(const double*, double*, long long, double, double, long long,
                                long long, double))fn;
             k<<<grid, block, 0, s>>>(g, y, num, t0, tEnd, numSteps, stages, kappa);
+            return (int)cudaGetLastError();
         };
     }
     if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1) {
@@ -123,15 +131,17 @@ static KernelEntry make_entry(int kind, int arith) {
         e.launch_persistent = [](const void* fn, dim3 grid, dim3 block, size_t smem,
                                  cudaStream_t s, const double* g, double* y, DevStats* st,
                                  long long num, double t, double tEnd, DevTol tol, int merge,
-                                 unsigned long long* counter) {
+                                 unsigned long long* counter) -> int {
             auto k = (void (*)(const double*, double*, DevStats*, long long, double, double,
                                DevTol, int, unsigned long long*))fn;
             k<<<grid, block, smem, s>>>(g, y, st, num, t, tEnd, tol, merge, counter);
+            return (int)cudaGetLastError();
         };
     }
     if constexpr (SOLVER == 1)
-        e.build_rkc_table = [](double* tab, double kappa, cudaStream_t s) {
+        e.build_rkc_table = [](double* tab, double kappa, cudaStream_t s) -> int {
             rkc_coef_table_kernel<R><<<(unsigned)((kRkcTableMaxS + 63) / 64), 64, 0, s>>>(tab, kappa);
+            return (int)cudaGetLastError();
         };
     return e;
 }

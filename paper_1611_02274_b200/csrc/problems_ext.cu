@@ -1,0 +1,56 @@
+// problems_ext.cu -- problems beyond the reference's set, built through the
+// public user-problem interface (include/bode_problem.cuh) exactly as an
+// out-of-tree library would be, and registered when libbode loads.
+//
+// Brusselator: 1-D reaction-diffusion of the autocatalytic Brusselator
+// mechanism (a chemical-kinetics RHS with diffusion, the moderately stiff
+// workload RKC is designed for; the paper's motivating use is chemical
+// kinetics):
+//   u' = A + u^2 v - (B + 1) u + alpha (u_{i-1} - 2u_i + u_{i+1}) / dx^2
+//   v' = B u - u^2 v        + alpha (v_{i-1} - 2v_i + v_{i+1}) / dx^2
+// on n interior points, dx = 1/(n+1), boundary values (A, B/A), per-system
+// parameters g = (A, B, alpha) -- so stiffness varies per system with alpha.
+// State interleaved y = (u_1, v_1, ..., u_n, v_n): a lane's slice holds whole
+// grid points, and the halo is one (u, v) pair from each neighbouring lane.
+// The host form that the reference drivers integrate for the parity tests is
+// in oracle/ref_shim.cpp (same expression order).
+#include "../../include/bode_problem.cuh"
+
+namespace bode {
+
+template <int NN>
+struct Brusselator {
+    static constexpr int N = 2 * NN, P = 3;
+    static constexpr const char* name = "brusselator";
+    template <class R, int L>
+    __device__ __forceinline__ static void rhs(const Group<L>& G, R, const R (&y)[N / L],
+                                               const R* g, R (&out)[N / L]) {
+        constexpr int C = N / L;
+        static_assert(C % 2 == 0, "a lane holds whole (u, v) grid points");
+        const R A = g[0], B = g[1], alpha = g[2];
+        const R dx = R(1.0) / R(double(NN + 1));
+        const R c = alpha / (dx * dx);
+        const R ub = A, vb = B / A;
+        const R Bp1 = B + R(1.0);
+        const R uLh = R(G.from_prev(val(y[C - 2]))), vLh = R(G.from_prev(val(y[C - 1])));
+        const R uRh = R(G.from_next(val(y[0]))), vRh = R(G.from_next(val(y[1])));
+        const bool first = G.lane == 0, last = G.lane == L - 1;
+#pragma unroll
+        for (int k = 0; k < C / 2; ++k) {
+            const R u = y[2 * k], v = y[2 * k + 1];
+            const R uL = k > 0 ? y[2 * k - 2] : (first ? ub : uLh);
+            const R vL = k > 0 ? y[2 * k - 1] : (first ? vb : vLh);
+            const R uR = k < C / 2 - 1 ? y[2 * k + 2] : (last ? ub : uRh);
+            const R vR = k < C / 2 - 1 ? y[2 * k + 3] : (last ? vb : vRh);
+            const R uuv = u * u * v;
+            out[2 * k] = A + uuv - Bp1 * u + c * (uL - R(2.0) * u + uR);
+            out[2 * k + 1] = B * u - uuv + c * (vL - R(2.0) * v + vR);
+        }
+    }
+};
+
+}  // namespace bode
+
+// n = 32 grid points (dim 64): RKCK with 4 lanes per system (stage slots in
+// shared memory), RKC with 8 lanes, 128 registers (16 warps/SM)
+BODE_REGISTER_PROBLEM_R(brusselator32, bode::Brusselator<32>, BODE_PROBLEM_BRUSSELATOR, 4, 8, 128)

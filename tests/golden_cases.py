@@ -42,6 +42,21 @@ def heat_ic(n):
     return 4.0 * x * (1.0 - x)
 
 
+def brusselator_ic(n):
+    """u = 1 + sin(2 pi x), v = 3 on the interior points x_i = i/(n+1), interleaved."""
+    x = (np.arange(n) + 1) / (n + 1)
+    y = np.empty(2 * n)
+    y[0::2] = 1.0 + np.sin(2.0 * np.pi * x)
+    y[1::2] = 3.0
+    return y
+
+
+def brusselator_params(num, alpha_lo, alpha_hi, A=1.0, B=3.0):
+    """SoA params (A, B, alpha) with alpha log-spaced over the batch."""
+    alpha = np.exp(np.linspace(np.log(alpha_lo), np.log(alpha_hi), num))
+    return np.concatenate([np.full(num, A), np.full(num, B), alpha])
+
+
 def build_inputs(case, num=None):
     num = num or case["num"]
     kind = case["problem"]

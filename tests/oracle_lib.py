@@ -143,6 +143,8 @@ class RefLib:
         L = self.lib = ctypes.CDLL(REF_SO)
         sig = {
             "ref_outer_loop": (c_i, [PProb, c_i, c_d, c_d, c_d, c_i64, PD, PD, PTol, PSt, c_i, P(c_i)]),
+            "ref_outer_loop_fn": (c_i, [ctypes.c_void_p, c_i, c_i, c_i, c_d, c_d, c_d, c_i64, PD,
+                                        PD, PTol, PSt, c_i, P(c_i)]),
             "ref_integrate_batch": (c_i, [PProb, c_i, c_d, c_d, c_i64, PD, PD, PTol, PSt, c_i]),
             "ref_driver": (c_i, [PProb, c_i, c_d, c_d, PD, PD, PTol, PSt]),
             "ref_splitmix64_at": (c_u64, [c_u64, c_u64]),
@@ -174,6 +176,20 @@ class RefLib:
         rc = self.lib.ref_outer_loop(ctypes.byref(prob), solver, t0, t_end, h_outer, num,
                                      A.dptr(y), A.dptr(g), ctypes.byref(tol or A.default_tol()),
                                      A.vptr(st), workers or os.cpu_count(), ctypes.byref(steps))
+        return rc, y, st, steps.value
+
+    def outer_loop_fn(self, rhs_addr, dim, param_dim, solver, t0, t_end, h_outer, y_soa,
+                      g_soa=None, tol=None, workers=None):
+        """outerLoop on an OdeProblem whose rhs is the C function at rhs_addr."""
+        num = y_soa.size // dim
+        y = np.array(y_soa, dtype=np.float64)
+        g = None if g_soa is None else np.ascontiguousarray(g_soa, dtype=np.float64)
+        st = A.empty_stats(num)
+        steps = c_i(0)
+        rc = self.lib.ref_outer_loop_fn(rhs_addr, dim, param_dim, solver, t0, t_end, h_outer,
+                                        num, A.dptr(y), A.dptr(g),
+                                        ctypes.byref(tol or A.default_tol()), A.vptr(st),
+                                        workers or os.cpu_count(), ctypes.byref(steps))
         return rc, y, st, steps.value
 
     def driver(self, prob, solver, t, t_end, y, g=None, tol=None):

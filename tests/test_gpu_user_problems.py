@@ -1,0 +1,99 @@
+"""Parity of problems registered through include/bode_problem.cuh: the
+built-in extension (Brusselator, csrc/problems_ext.cu) and an out-of-tree
+library (examples/user_problem.cu, Lorenz-96), against the REFERENCE drivers
+(oracle/_ref) integrating the same right-hand side written as a reference
+OdeProblem. EXACT: bitwise states and counters; FAST: the north_star bar."""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+import paper_1611_02274_b200 as B
+from paper_1611_02274_b200 import _abi as A
+from golden_cases import brusselator_ic, brusselator_params, perturb
+
+pytestmark = pytest.mark.gpu
+
+COUNTS = ("steps_accepted", "steps_rejected", "rhs_evals", "spec_rad_evals", "underflow")
+USER_LIB = os.path.join(A.PKG_DIR, "lib", "libuser_problem.so")
+LORENZ = A.USER_BASE + 96
+
+
+def sysrel(y, yref, num, dim):
+    a = y.reshape(dim, num)
+    b = yref.reshape(dim, num)
+    return np.max(np.abs(a - b), axis=0) / np.maximum(np.max(np.abs(b), axis=0), 1e-300)
+
+
+def run(prob, solver, y0, g, arith, t1=1.0):
+    num = y0.size // prob.dim
+    batch = B.BatchStates(num, prob.dim, prob.param_dim, y0.copy(), g.copy())
+    r = B.outer_loop(B.OdeProblem(prob.kind, prob.dim, prob.param_dim), batch, 0.0, t1, 0.1,
+                     solver=solver, arith=arith)
+    return r.states.values, r.stats
+
+
+@pytest.mark.parametrize("solver,alpha", [(A.SOLVER_RKC, (0.02, 0.5)),
+                                          (A.SOLVER_RKCK, (0.002, 0.02))])
+def test_brusselator_exact_bitwise(gpu, ref, solver, alpha):
+    num = 1024
+    prob = A.make_problem(A.BRUSSELATOR)
+    y0 = perturb(brusselator_ic(32), 0.01, 7, num)
+    g = brusselator_params(num, *alpha)
+    y, st = run(prob, solver, y0, g, "exact")
+    rc, yo, so, _ = ref.outer_loop(prob, solver, 0.0, 1.0, 0.1, y0, g)
+    assert rc == 0
+    assert np.array_equal(y.view(np.uint64), yo.view(np.uint64))
+    for k in COUNTS:
+        assert np.array_equal(st[k], so[k]), k
+    assert st["steps_accepted"].min() > 0
+
+
+def test_brusselator_fast_within_bar(gpu, ref):
+    num = 1024
+    prob = A.make_problem(A.BRUSSELATOR)
+    y0 = perturb(brusselator_ic(32), 0.01, 7, num)
+    g = brusselator_params(num, 0.002, 0.02)
+    y, st = run(prob, A.SOLVER_RKCK, y0, g, "fast")
+    rc, yo, so, _ = ref.outer_loop(prob, A.SOLVER_RKCK, 0.0, 1.0, 0.1, y0, g)
+    assert sysrel(y, yo, num, 64).max() <= 1e-13  # 1e-3 * eps
+    for k in ("steps_accepted", "steps_rejected", "rhs_evals"):
+        assert np.array_equal(st[k], so[k]), k
+
+
+@pytest.fixture(scope="module")
+def user_lib(gpu):
+    return B.api.load_problem_library(USER_LIB)
+
+
+def _lorenz_inputs(num):
+    base = 8.0 + np.sin(np.arange(40))
+    y0 = perturb(base, 0.01, 11, num)
+    g = np.linspace(6.0, 10.0, num)
+    return y0, g
+
+
+@pytest.mark.parametrize("solver", [A.SOLVER_RKCK, A.SOLVER_RKC])
+def test_out_of_tree_problem_exact_bitwise(user_lib, ref, solver):
+    num = 512
+    prob = A.Problem(kind=LORENZ, dim=40, param_dim=1, reserved=0)
+    y0, g = _lorenz_inputs(num)
+    y, st = run(prob, solver, y0, g, "exact", t1=0.5)
+    rhs = ctypes.cast(user_lib.bode_example_lorenz96_rhs, ctypes.c_void_p).value
+    rc, yo, so, _ = ref.outer_loop_fn(rhs, 40, 1, solver, 0.0, 0.5, 0.1, y0, g)
+    assert rc == 0
+    assert np.array_equal(y.view(np.uint64), yo.view(np.uint64))
+    for k in COUNTS:
+        assert np.array_equal(st[k], so[k]), k
+
+
+def test_out_of_tree_problem_fast(user_lib, ref):
+    num = 512
+    prob = A.Problem(kind=LORENZ, dim=40, param_dim=1, reserved=0)
+    y0, g = _lorenz_inputs(num)
+    y, st = run(prob, A.SOLVER_RKCK, y0, g, "fast", t1=0.5)
+    rhs = ctypes.cast(user_lib.bode_example_lorenz96_rhs, ctypes.c_void_p).value
+    rc, yo, so, _ = ref.outer_loop_fn(rhs, 40, 1, A.SOLVER_RKCK, 0.0, 0.5, 0.1, y0, g)
+    # chaotic flow: FMA-level differences grow, but stay far inside 1e-3 * eps
+    assert sysrel(y, yo, num, 40).max() <= 1e-13
