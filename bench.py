@@ -49,7 +49,12 @@ F_RHS = {"pleiades": 420, "heat": None, "expdecay": 1, "harmonic": 0}
 def algorithmic_flops(problem: str, solver: str, dim: int, stats: np.ndarray, windows: int) -> float:
     """SURVEY.md 8d: RKCK F = rhs*F_rhs + (acc+rej)*58*N;
     RKC F = rhs*F_rhs + N*(10*S + 6*I + 7*C + 8) per window, I = rhs - 2 - S."""
-    f_rhs = (4 * dim - 2) if problem == "heat" else F_RHS[problem]
+    if problem == "heat":
+        f_rhs = 4 * dim - 2
+    elif problem == "brusselator":  # 17 per grid point + 5 per call (csrc/problems_ext.cu)
+        f_rhs = 17 * (dim // 2) + 5
+    else:
+        f_rhs = F_RHS[problem]
     rhs = float(stats["rhs_evals"].sum())
     if solver == "rkck":
         att = float(stats["steps_accepted"].sum() + stats["steps_rejected"].sum())
@@ -184,7 +189,7 @@ def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warm
     gd = torch.from_numpy(g0).to("cuda") if g0 is not None else None
     st = torch.zeros(num * 8, dtype=torch.int64, device="cuda")
     tol = A.default_tol()
-    prob = P.OdeProblem(A.PROBLEM_NAMES[problem], dim, 0 if g0 is None else 1)
+    prob = P.OdeProblem(A.PROBLEM_NAMES[problem], dim, 0 if g0 is None else g0.size // num)
     gp = gd.data_ptr() if gd is not None else 0
 
     def window(k, merge):
@@ -242,7 +247,7 @@ def main():
     import torch
     import paper_1611_02274_b200 as P
     from paper_1611_02274_b200 import _abi as A
-    from golden_cases import PLEIADES_IC, heat_ic, perturb
+    from golden_cases import PLEIADES_IC, brusselator_ic, brusselator_params, heat_ic, perturb
     from paper_1611_02274_b200.api import stiffness_params
 
     torch.cuda.set_device(local)
@@ -342,6 +347,12 @@ def main():
                 "expdecay", "rkc", "exact", 1, ye0, g0,
                 f"RKC expDecay, g0 log-uniform in [1,1e4] (config 4), {args.rkc_num} systems, EXACT",
                 min(args.steps, 10))
+            yb0 = perturb(brusselator_ic(32), 0.01, 7 + rank, args.rkc_num)
+            gb0 = brusselator_params(args.rkc_num, 0.02, 0.5)
+            extra["rkc_brusselator"] = secondary(
+                "brusselator", "rkc", "exact", 64, yb0, gb0,
+                f"RKC Brusselator reaction-diffusion n=32 (dim 64, registered problem), alpha "
+                f"log-spaced in [0.02, 0.5], {args.rkc_num} systems, EXACT", min(args.steps, 10))
 
     if rank != 0:
         if dist:

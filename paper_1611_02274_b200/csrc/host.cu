@@ -328,6 +328,8 @@ int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double*
     return BODE_OK;
 }
 
+constexpr int kMaxChunks = 16;  // host-pointer pipeline depth per shard
+
 // Per-device buffers reused across calls (no cudaMalloc on the hot path once warm).
 struct DeviceBuffers {
     std::mutex m;
@@ -335,7 +337,8 @@ struct DeviceBuffers {
     double* g = nullptr;
     DevStats* st = nullptr;
     size_t y_cap = 0, g_cap = 0, st_cap = 0;
-    cudaStream_t streams[3] = {nullptr, nullptr, nullptr};
+    cudaStream_t streams[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
+    cudaEvent_t events[2 * kMaxChunks] = {};                 // per chunk: H2D done, kernel done
 };
 
 DeviceBuffers g_dev[64];
@@ -388,8 +391,12 @@ int check_devices(int gpus) {
     return BODE_OK;
 }
 
-// One shard of a host-pointer window: pipelined H2D -> kernel -> D2H in chunks
-// over up to three streams, so copies in both directions overlap compute.
+// One shard of a host-pointer window, pipelined in chunks over three streams
+// with one role each: H2D copies back to back on streams[0], the kernels on
+// streams[1] (chunk k waits for its H2D), D2H copies on streams[2] (chunk k
+// waits for its kernel). With pinned host memory both PCIe directions then run
+// continuously and overlap the compute; the window costs about
+// max(H2D, D2H) + one chunk's kernel.
 int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard& sh,
                      int64_t num, const double* g, double* y, bode_stats_t* stats, double t,
                      double tEnd, const DevTol& tol) {
@@ -403,31 +410,39 @@ int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard&
     if (stats && (rc = ensure(&B.st, &B.st_cap, (size_t)sh.count))) return rc;
     for (auto& s : B.streams)
         if (!s) BODE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    for (auto& ev : B.events)
+        if (!ev) BODE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
 
     const bool pinned = host_pinned(y);
     const int64_t min_chunk = 1 << 16;
-    int nchunks = pinned ? (int)std::min<int64_t>(8, std::max<int64_t>(1, sh.count / min_chunk)) : 1;
+    const int nchunks =
+        pinned ? (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, sh.count / min_chunk)) : 1;
     const int64_t cbase = sh.count / nchunks, crem = sh.count % nchunks;
+    cudaStream_t sh2d = B.streams[0], sk = B.streams[1], sd2h = B.streams[2];
     int64_t off = 0;
     for (int k = 0; k < nchunks; ++k) {
         const int64_t nk = cbase + (k < crem ? 1 : 0);
-        cudaStream_t s = B.streams[k % 3];
         double* dy = B.y + off * N;
         double* dg = P > 0 ? B.g + off * P : nullptr;
         DevStats* dst = stats ? B.st + off : nullptr;
         const int64_t src = sh.begin + off;
+        cudaEvent_t in_done = B.events[2 * k], k_done = B.events[2 * k + 1];
         BODE_CUDA(cudaMemcpy2DAsync(dy, nk * sizeof(double), y + src, num * sizeof(double),
-                                    nk * sizeof(double), N, cudaMemcpyHostToDevice, s));
+                                    nk * sizeof(double), N, cudaMemcpyHostToDevice, sh2d));
         if (P > 0)
             BODE_CUDA(cudaMemcpy2DAsync(dg, nk * sizeof(double), g + src, num * sizeof(double),
-                                        nk * sizeof(double), P, cudaMemcpyHostToDevice, s));
-        rc = launch_window(e, s, dg, dy, dst, nk, t, tEnd, tol, 0);
+                                        nk * sizeof(double), P, cudaMemcpyHostToDevice, sh2d));
+        BODE_CUDA(cudaEventRecord(in_done, sh2d));
+        BODE_CUDA(cudaStreamWaitEvent(sk, in_done, 0));
+        rc = launch_window(e, sk, dg, dy, dst, nk, t, tEnd, tol, 0);
         if (rc) return rc;
+        BODE_CUDA(cudaEventRecord(k_done, sk));
+        BODE_CUDA(cudaStreamWaitEvent(sd2h, k_done, 0));
         BODE_CUDA(cudaMemcpy2DAsync(y + src, num * sizeof(double), dy, nk * sizeof(double),
-                                    nk * sizeof(double), N, cudaMemcpyDeviceToHost, s));
+                                    nk * sizeof(double), N, cudaMemcpyDeviceToHost, sd2h));
         if (stats)
             BODE_CUDA(cudaMemcpyAsync(stats + src, dst, nk * sizeof(DevStats),
-                                      cudaMemcpyDeviceToHost, s));
+                                      cudaMemcpyDeviceToHost, sd2h));
         off += nk;
     }
     for (auto& s : B.streams) BODE_CUDA(cudaStreamSynchronize(s));

@@ -348,13 +348,27 @@ __device__ __forceinline__ void rkck_nystrom_persistent(const double* __restrict
             has = true;
         }
     }
+    auto retire = [&]() {  // store a finished (or frozen) system and free the lane
+#pragma unroll
+        for (int c = 0; c < P::N; ++c) y_soa[sys + num * (long long)c] = val(s.y[c]);
+        if (stats != nullptr) {
+            if (merge) {
+                DevStats o = stats[sys];
+                stats_merge(o, s.st);
+                stats[sys] = o;
+            } else {
+                stats[sys] = s.st;
+            }
+        }
+        has = false;
+    };
 #pragma unroll 1
     for (;;) {
+        // refill round: idle lanes claim consecutive systems with one
+        // warp-aggregated atomicAdd (loads of the claimed range stay coalesced)
         if (!exhausted) {
             const unsigned need = __ballot_sync(kFull, !has);
-            // refill in batches of >= refill_min idle lanes: each refill round
-            // costs the warp one scattered-load latency, so amortize it
-            if (need && (__popc(need) >= refill_min || need == kFull)) {
+            if (need) {
                 unsigned long long base = 0;
                 const int leader = __ffs(need) - 1;
                 if ((int)lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(need));
@@ -368,28 +382,21 @@ __device__ __forceinline__ void rkck_nystrom_persistent(const double* __restrict
                         for (int c = 0; c < P::N; ++c) s.y[c] = R(y_soa[sys + num * (long long)c]);
                         s.start(t_in, tEnd_in, tol);
                         has = true;
+                        if (!s.live) retire();  // empty interval: nothing to integrate
                     }
                 }
             }
         }
         if (!__any_sync(kFull, has)) break;
-        if (has) {
-            if (s.live) s.attempt(tol);
-            if (!s.live) {  // done (or frozen): write back, free the lane
-#pragma unroll
-                for (int c = 0; c < P::N; ++c) y_soa[sys + num * (long long)c] = val(s.y[c]);
-                if (stats != nullptr) {
-                    if (merge) {
-                        DevStats o = stats[sys];
-                        stats_merge(o, s.st);
-                        stats[sys] = o;
-                    } else {
-                        stats[sys] = s.st;
-                    }
-                }
-                has = false;
-            }
-        }
+        // attempts until refill_min lanes are idle (all of them once the queue
+        // is exhausted): the same lean loop body as the static kernel, one
+        // ballot per attempt
+        const int stop = exhausted ? 32 : refill_min;
+#pragma unroll 1
+        do {
+            if (has && s.live) s.attempt(tol);
+            if (has && !s.live) retire();
+        } while (__popc(__ballot_sync(kFull, !has)) < stop);
     }
 }
 

@@ -46,6 +46,16 @@ for p in $PARTS; do
         BODE_LANES=$1 BODE_MAXREG=$2 timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --num 1048576 --rkc-num 1048576 > $OUT/bench_rkc_L$1_R$2.txt 2>&1; done
       for R in 96 80; do BODE_LANES=1 BODE_MAXREG=$R timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --num 1048576 --rkc-num 1048576 > $OUT/bench_rkc_exp$R.txt 2>&1; done
       echo "ab_rkc rc=$?" >> $OUT/status.txt ;;
+    ncu_late)
+      for W in 0 9; do
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:Pleiades, double" \
+        -s $W -c 1 -o $OUT/prof_rkck_w$W python bench.py --steps 10 --warmup 0 --num 262144 \
+        --no-secondary --no-e2e --no-cpu > $OUT/ncu_rkck_w$W.txt 2>&1; done
+      echo "ncu_late rc=$?" >> $OUT/status.txt ;;
+    e2e)
+      timeout 300 python tools/pcie.py > $OUT/pcie.txt 2>&1
+      timeout 600 python bench.py --no-secondary --no-cpu > $OUT/bench_e2e.txt 2>&1
+      echo "e2e rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
