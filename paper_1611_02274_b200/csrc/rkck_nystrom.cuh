@@ -109,7 +109,7 @@ struct NystromRkck {
         for (int j = 4; j <= (kRkckUnrollStages ? 3 : 6); ++j) stage_block<false>(j, Q, Acc);
         st.rhs_evals += 5;
         st.stages_total += 6;
-        finish_attempt(tol);
+        finish_attempt(tol, Q, Acc);
     }
 
     // stage j in 3..6; UNROLLED: j is a compile-time constant after unrolling
@@ -141,8 +141,10 @@ struct NystromRkck {
                         if (m < nk) s = s + R(bm[m]) * kget(m, i);
                     Q[i] = q[i] + h * s;
                 }
-            } else {  // FAST: h folded into the stage weights, one FMA per term
+            } else {  // FAST: h folded into the stage weights, one FMA per term;
+                      // the newest acceleration A_{j-1} is still in Acc (no reload)
                 const double hb0 = val(h) * b0;
+                const double hlast = val(h) * c_ck_b[j - 3][nk];
                 double hbm[4];
 #pragma unroll
                 for (int m = 0; m < 4; ++m) hbm[m] = val(h) * bm[m];
@@ -150,9 +152,9 @@ struct NystromRkck {
                 for (int i = 0; i < M; ++i) {
                     double s = fma(hb0, val(A0[i]), val(v[i]));
 #pragma unroll
-                    for (int m = 0; m < 4; ++m)
-                        if (m < nk) s = fma(hbm[m], val(kget(m, M + i)), s);
-                    Acc[i] = R(s);
+                    for (int m = 0; m < 3; ++m)
+                        if (m < nk - 1) s = fma(hbm[m], val(kget(m, M + i)), s);
+                    Acc[i] = R(fma(hlast, val(Acc[i]), s));
                 }
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
@@ -168,14 +170,19 @@ struct NystromRkck {
             for (int i = 0; i < M; ++i) kset(out, i, Acc[i]);
             BODE_FENCE();
             P::template accel<R>(Q, Acc);
+            // FAST reads A6 from registers (finish_attempt), so its slot is never stored
+            if (is_exact<R>::value || j != 6) {
 #pragma unroll
-            for (int i = 0; i < M; ++i) kset(out, M + i, Acc[i]);
+                for (int i = 0; i < M; ++i) kset(out, M + i, Acc[i]);
+            }
             BODE_FENCE();
         }
     }
 
     // error norm, controller and the accept/reject update of one attempt
-    __device__ __forceinline__ void finish_attempt(const DevTol& tol) {
+    // Q/Acc: stage scratch, free here; FAST computes the candidate yNext into
+    // them in the same pass as the error norm (one read of each stage slot)
+    __device__ __forceinline__ void finish_attempt(const DevTol& tol, R (&Q)[M], R (&Acc)[M]) {
         using namespace ck;
         R* const q = y;
         R* const v = y + M;
@@ -193,13 +200,20 @@ struct NystromRkck {
             const double hh = val(h);
             const double hd1 = hh * d1, hd3 = hh * d3, hd4 = hh * d4, hd5 = hh * d5, hd6 = hh * d6;
             double ma[4] = {0.0, 0.0, 0.0, 0.0}, mb[4] = {1.0, 1.0, 1.0, 1.0};
+            const double hc1 = hh * c1, hc3 = hh * c3, hc4 = hh * c4, hc6 = hh * c6;
             int bad = 0;
 #pragma unroll
             for (int i = 0; i < M; ++i) {
-                const double eq = fma(hd6, val(kget(0, i)), fma(hd5, val(kget(3, i)),
-                                  fma(hd4, val(kget(2, i)), fma(hd3, val(kget(1, i)), hd1 * val(v[i])))));
-                const double ev = fma(hd6, val(kget(0, M + i)), fma(hd5, val(kget(3, M + i)),
-                                  fma(hd4, val(kget(2, M + i)), fma(hd3, val(kget(1, M + i)), hd1 * val(A0[i])))));
+                const double k0q = val(kget(0, i)), k1q = val(kget(1, i)), k2q = val(kget(2, i));
+                const double k0v = val(Acc[i]), k1v = val(kget(1, M + i)),
+                             k2v = val(kget(2, M + i));  // A6 = Acc (never stored)
+                const double eq = fma(hd6, k0q, fma(hd5, val(kget(3, i)),
+                                  fma(hd4, k2q, fma(hd3, k1q, hd1 * val(v[i])))));
+                const double ev = fma(hd6, k0v, fma(hd5, val(kget(3, M + i)),
+                                  fma(hd4, k2v, fma(hd3, k1v, hd1 * val(A0[i])))));
+                // candidate yNext (rkck.cpp:74), kept only if the step is accepted
+                Q[i] = R(fma(hc6, k0q, fma(hc4, k2q, fma(hc3, k1q, fma(hc1, val(v[i]), val(q[i]))))));
+                Acc[i] = R(fma(hc6, k0v, fma(hc4, k2v, fma(hc3, k1v, fma(hc1, val(A0[i]), val(v[i]))))));
                 bad |= ((__double2hiint(eq) & 0x7ff00000) == 0x7ff00000) |
                        ((__double2hiint(ev) & 0x7ff00000) == 0x7ff00000);
                 const double dq = fma(hh, fabs(val(v[i])), fabs(val(q[i]))) + val(tiny);
@@ -277,17 +291,12 @@ struct NystromRkck {
                 for (int i = 0; i < M; ++i)
                     v[i] = v[i] + h * (R(c1) * A0[i] + R(c3) * kget(1, M + i) +
                                        R(c4) * kget(2, M + i) + R(c6) * kget(0, M + i));
-            } else {  // FAST: h folded into the weights
-                const double hh = val(h);
-                const double hc1 = hh * c1, hc3 = hh * c3, hc4 = hh * c4, hc6 = hh * c6;
+            } else {  // FAST: the candidate formed with the error norm
 #pragma unroll
-                for (int i = 0; i < M; ++i)
-                    q[i] = R(fma(hc6, val(kget(0, i)), fma(hc4, val(kget(2, i)),
-                             fma(hc3, val(kget(1, i)), fma(hc1, val(v[i]), val(q[i]))))));
-#pragma unroll
-                for (int i = 0; i < M; ++i)
-                    v[i] = R(fma(hc6, val(kget(0, M + i)), fma(hc4, val(kget(2, M + i)),
-                             fma(hc3, val(kget(1, M + i)), fma(hc1, val(A0[i]), val(v[i]))))));
+                for (int i = 0; i < M; ++i) {
+                    q[i] = Q[i];
+                    v[i] = Acc[i];
+                }
             }
             haveF = false;
             h = hNew;
