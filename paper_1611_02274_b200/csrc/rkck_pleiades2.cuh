@@ -159,13 +159,18 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
             for (int m = 0; m < 4; ++m) bm[m] = c_ck_b[j - 3][m + 1];
             const int nk = j - 2;
             const int out = (j == 6) ? 0 : j - 2;  // k6 reuses k2's slot
+            // the newest acceleration A_{j-1} is still in Acc; it is the last
+            // term of every stage sum, so reading it from registers keeps the
+            // reference's summation order
+            const double blast = c_ck_b[j - 3][nk];
             if constexpr (is_exact<R>::value) {
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
                     R s = R(b0) * A0[i];
 #pragma unroll
-                    for (int m = 0; m < 4; ++m)  // predicated: constant offsets, no loop
-                        if (m < nk) s = s + R(bm[m]) * kget(m, M + i);
+                    for (int m = 0; m < 3; ++m)  // predicated: constant offsets, no loop
+                        if (m < nk - 1) s = s + R(bm[m]) * kget(m, M + i);
+                    s = s + R(blast) * Acc[i];
                     Acc[i] = v[i] + h * s;
                 }
 #pragma unroll
@@ -185,9 +190,9 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
                 for (int i = 0; i < M; ++i) {
                     double s = fma(hb0, val(A0[i]), val(v[i]));
 #pragma unroll
-                    for (int m = 0; m < 4; ++m)
-                        if (m < nk) s = fma(hbm[m], val(kget(m, M + i)), s);
-                    Acc[i] = R(s);
+                    for (int m = 0; m < 3; ++m)
+                        if (m < nk - 1) s = fma(hbm[m], val(kget(m, M + i)), s);
+                    Acc[i] = R(fma(val(h) * blast, val(Acc[i]), s));
                 }
 #pragma unroll
                 for (int i = 0; i < M; ++i) {
@@ -201,8 +206,10 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
 #pragma unroll
             for (int i = 0; i < M; ++i) kset(out, i, Acc[i]);
             pleiades_accel_pair<R>(G, Q, Acc);
+            if (j != 6) {  // A6 stays in Acc for the error norm and yNext
 #pragma unroll
-            for (int i = 0; i < M; ++i) kset(out, M + i, Acc[i]);
+                for (int i = 0; i < M; ++i) kset(out, M + i, Acc[i]);
+            }
         }
         if (live) {
             st.rhs_evals += 5;
@@ -224,22 +231,30 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
             int bad = 0;
 #pragma unroll
             for (int i = 0; i < M; ++i) {
+                const R k0q = kget(0, i), k1q = kget(1, i), k2q = kget(2, i);
+                const R k0v = Acc[i], k1v = kget(1, M + i), k2v = kget(2, M + i);  // A6 = Acc
                 if constexpr (is_exact<R>::value) {
-                    const R eq = h * (R(d1) * v[i] + R(d3) * kget(1, i) + R(d4) * kget(2, i) +
-                                      R(d5) * kget(3, i) + R(d6) * kget(0, i));
-                    const R ev = h * (R(d1) * A0[i] + R(d3) * kget(1, M + i) +
-                                      R(d4) * kget(2, M + i) + R(d5) * kget(3, M + i) +
-                                      R(d6) * kget(0, M + i));
+                    const R eq = h * (R(d1) * v[i] + R(d3) * k1q + R(d4) * k2q +
+                                      R(d5) * kget(3, i) + R(d6) * k0q);
+                    const R ev = h * (R(d1) * A0[i] + R(d3) * k1v + R(d4) * k2v +
+                                      R(d5) * kget(3, M + i) + R(d6) * k0v);
+                    // candidate yNext (rkck.cpp:74), kept only if the step is accepted
+                    Q[i] = q[i] + h * (R(c1) * v[i] + R(c3) * k1q + R(c4) * k2q + R(c6) * k0q);
+                    Acc[i] = v[i] + h * (R(c1) * A0[i] + R(c3) * k1v + R(c4) * k2v + R(c6) * k0v);
                     if (!isfinite_(eq) || !isfinite_(ev)) nanFlag = true;
                     const R dq = fabs_(q[i]) + fabs_(h * v[i]) + tiny;
                     const R dv = fabs_(v[i]) + fabs_(h * A0[i]) + tiny;
                     qm[(2 * i) & 3].push(fabs(val(eq)), val(dq));
                     qm[(2 * i + 1) & 3].push(fabs(val(ev)), val(dv));
                 } else {
-                    const double eq = fma(hd6, val(kget(0, i)), fma(hd5, val(kget(3, i)),
-                                      fma(hd4, val(kget(2, i)), fma(hd3, val(kget(1, i)), hd1 * val(v[i])))));
-                    const double ev = fma(hd6, val(kget(0, M + i)), fma(hd5, val(kget(3, M + i)),
-                                      fma(hd4, val(kget(2, M + i)), fma(hd3, val(kget(1, M + i)), hd1 * val(A0[i])))));
+                    const double eq = fma(hd6, val(k0q), fma(hd5, val(kget(3, i)),
+                                      fma(hd4, val(k2q), fma(hd3, val(k1q), hd1 * val(v[i])))));
+                    const double ev = fma(hd6, val(k0v), fma(hd5, val(kget(3, M + i)),
+                                      fma(hd4, val(k2v), fma(hd3, val(k1v), hd1 * val(A0[i])))));
+                    Q[i] = R(fma(hh * c6, val(k0q), fma(hh * c4, val(k2q),
+                             fma(hh * c3, val(k1q), fma(hh * c1, val(v[i]), val(q[i]))))));
+                    Acc[i] = R(fma(hh * c6, val(k0v), fma(hh * c4, val(k2v),
+                               fma(hh * c3, val(k1v), fma(hh * c1, val(A0[i]), val(v[i]))))));
                     bad |= ((__double2hiint(eq) & 0x7ff00000) == 0x7ff00000) |
                            ((__double2hiint(ev) & 0x7ff00000) == 0x7ff00000);
                     const double dq = fma(hh, fabs(val(v[i])), fabs(val(q[i]))) + val(tiny);
@@ -289,26 +304,11 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
         if (live && accepted) {
             t += h;
             stats_accept(st, val(h));
-            if constexpr (is_exact<R>::value) {
+            // yNext (rkck.cpp:74), formed with the error norm
 #pragma unroll
-                for (int i = 0; i < M; ++i)
-                    q[i] = q[i] + h * (R(c1) * v[i] + R(c3) * kget(1, i) + R(c4) * kget(2, i) +
-                                       R(c6) * kget(0, i));
-#pragma unroll
-                for (int i = 0; i < M; ++i)
-                    v[i] = v[i] + h * (R(c1) * A0[i] + R(c3) * kget(1, M + i) +
-                                       R(c4) * kget(2, M + i) + R(c6) * kget(0, M + i));
-            } else {  // FAST: h folded into the weights
-                const double hh = val(h);
-                const double hc1 = hh * c1, hc3 = hh * c3, hc4 = hh * c4, hc6 = hh * c6;
-#pragma unroll
-                for (int i = 0; i < M; ++i)
-                    q[i] = R(fma(hc6, val(kget(0, i)), fma(hc4, val(kget(2, i)),
-                             fma(hc3, val(kget(1, i)), fma(hc1, val(v[i]), val(q[i]))))));
-#pragma unroll
-                for (int i = 0; i < M; ++i)
-                    v[i] = R(fma(hc6, val(kget(0, M + i)), fma(hc4, val(kget(2, M + i)),
-                             fma(hc3, val(kget(1, M + i)), fma(hc1, val(A0[i]), val(v[i]))))));
+            for (int i = 0; i < M; ++i) {
+                q[i] = Q[i];
+                v[i] = Acc[i];
             }
             haveF = false;
             h = hNew;
