@@ -56,6 +56,14 @@ for p in $PARTS; do
       timeout 300 python tools/pcie.py > $OUT/pcie.txt 2>&1
       timeout 600 python bench.py --no-secondary --no-cpu > $OUT/bench_e2e.txt 2>&1
       echo "e2e rc=$?" >> $OUT/status.txt ;;
+    ncu_persist)
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:persistent" \
+        -s 1 -c 1 -o $OUT/prof_persist_w1 python bench.py --steps 10 --warmup 0 --num 1048576 --persistent \
+        --no-secondary --no-e2e --no-cpu > $OUT/ncu_persist.txt 2>&1
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:Pleiades, double" \
+        -s 1 -c 1 -o $OUT/prof_static_w1 python bench.py --steps 10 --warmup 0 --num 1048576 \
+        --no-secondary --no-e2e --no-cpu > $OUT/ncu_static.txt 2>&1
+      echo "ncu_persist rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
