@@ -173,13 +173,21 @@ def run_reference_arm(args):
 
 def measured_traffic(capture: str, num: int):
     """DRAM bytes per launch for `num` systems, from the newest committed ncu
-    capture summary (profiles/*_ncu.json: dram read+write per system-window)."""
+    capture summary (profiles/*_ncu.json: dram read+write per system-window),
+    plus that capture's FP64 pipe use, warp execution efficiency and DRAM GB/s."""
     import glob
     for path in sorted(glob.glob(os.path.join(REPO, "profiles", "*_ncu.json")), reverse=True):
         d = json.load(open(path)).get(capture)
         if d and d.get("dram_bytes_per_system"):
-            return d["dram_bytes_per_system"] * num, os.path.basename(path)
-    return None, None
+            tpi = d.get("thread_inst_per_inst")
+            ncu = {"source": os.path.basename(path), "systems": d.get("systems"),
+                   "fp64_pipe_pct": d.get("fp64_pipe_pct"),
+                   "warp_execution_efficiency": tpi / 32.0 if tpi else None,
+                   "dram_GBps": ((d["dram_read_bytes"] + d["dram_write_bytes"]) / d["duration_ns"]
+                                 if d.get("duration_ns") else None),
+                   "hbm_peak_GBps": 6534.8}
+            return d["dram_bytes_per_system"] * num, os.path.basename(path), ncu
+    return None, None, None
 
 
 def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warmup, stream):
@@ -359,8 +367,8 @@ def main():
             dist.destroy_process_group()
         return
 
-    traffic, traffic_src = measured_traffic("rkck_fast" if args.arith == "fast" else "rkck_exact",
-                                            num)
+    traffic, traffic_src, ncu_evidence = measured_traffic(
+        "rkck_fast" if args.arith == "fast" else "rkck_exact", num)
     cpu = None
     if not args.no_cpu:
         rate, cores, kind, dt = cpu_reference_rate("pleiades", "rkck", PLEIADES_IC, 0.01, 42,
@@ -381,7 +389,7 @@ def main():
                    "parallelism": f"dp{world} (independent shards, no collective)"},
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak.value / 1e12,
                      "unit": "TFLOP/s", "frac": achieved / peak.value, "traffic": traffic,
-                     "traffic_source": traffic_src,
+                     "traffic_source": traffic_src, "ncu": ncu_evidence,
                      "algorithmic_bytes_per_launch": num * (28 * 8 * 2 + 64),
                      "peak_source": "DFMA microbenchmark on this device in this run "
                                     "(MEASURED_PEAKS.json has no FP64 entry); nominal 37.2",

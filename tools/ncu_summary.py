@@ -68,6 +68,10 @@ def summarize(report, systems):
                           sorted(stalls.items(), key=lambda kv: -kv[1])[:8]}
     if out.get("dram_read_bytes") is not None and systems:
         out["dram_bytes_per_system"] = (out["dram_read_bytes"] + out["dram_write_bytes"]) / systems
+    if out.get("dram_read_bytes") is not None and out.get("duration_ns"):
+        out["dram_GBps"] = (out["dram_read_bytes"] + out["dram_write_bytes"]) / out["duration_ns"]
+    if out.get("thread_inst_per_inst") is not None:
+        out["warp_execution_efficiency"] = out["thread_inst_per_inst"] / 32.0
     return out
 
 
@@ -105,14 +109,17 @@ def main():
         res[name] = summarize(path, int(systems))
     json.dump(res, open(prefix + ".json", "w"), indent=1)
     with open(prefix + ".md", "w") as f:
-        f.write("| capture | kernel | ms | FP64 pipe | issue | warps | regs | DRAM B/system | "
-                "local ld sectors | top stalls |\n|---|---|---|---|---|---|---|---|---|---|\n")
+        f.write("| capture | kernel | ms | FP64 pipe | warp exec eff | issue | warps | regs | "
+                "DRAM B/system | DRAM GB/s | local ld sectors | top stalls |\n"
+                "|---|---|---|---|---|---|---|---|---|---|---|---|\n")
         for n, r in res.items():
             st = ", ".join(f"{k} {v:.0%}" for k, v in list(r["stall_share"].items())[:4])
             f.write(f"| {n} | `{r['kernel'][:60]}` | {r['duration_ns'] / 1e6:.3f} | "
-                    f"{r['fp64_pipe_pct']:.1f}% | {r['issue_active_pct']:.1f}% | "
+                    f"{r['fp64_pipe_pct']:.1f}% | {r.get('warp_execution_efficiency', 0):.1%} | "
+                    f"{r['issue_active_pct']:.1f}% | "
                     f"{r['warps_active_pct']:.1f}% | {r['registers']:.0f} | "
-                    f"{r.get('dram_bytes_per_system', 0):.0f} | {r['local_ld_sectors']:.3g} | {st} |\n")
+                    f"{r.get('dram_bytes_per_system', 0):.0f} | {r.get('dram_GBps', 0):.0f} | "
+                    f"{r['local_ld_sectors']:.3g} | {st} |\n")
     print(open(prefix + ".md").read())
 
 
