@@ -17,8 +17,25 @@ def main():
     ap.add_argument("--num", type=int, default=1 << 22)
     args = ap.parse_args()
     nin, nout = args.num * 28 * 8, args.num * (28 * 8 + 64)
-    hi = torch.empty(nin, dtype=torch.uint8).pin_memory()
-    ho = torch.empty(nout, dtype=torch.uint8).pin_memory()
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import gpu_local_memory
+    res = {}
+    for placement in ("default", "gpu_local"):
+        if placement == "gpu_local":
+            with gpu_local_memory(torch, 0) as g:
+                hi = torch.zeros(nin, dtype=torch.uint8).pin_memory()
+                ho = torch.zeros(nout, dtype=torch.uint8).pin_memory()
+                res["gpu_local_cpus"] = len(g.cpus or [])
+        else:
+            hi = torch.zeros(nin, dtype=torch.uint8).pin_memory()
+            ho = torch.zeros(nout, dtype=torch.uint8).pin_memory()
+        res[placement] = measure(torch, hi, ho, nin, nout)
+    print(json.dumps(res))
+
+
+def measure(torch, hi, ho, nin, nout):
     di = torch.empty(nin, dtype=torch.uint8, device="cuda")
     do = torch.empty(nout, dtype=torch.uint8, device="cuda")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
@@ -49,10 +66,9 @@ def main():
         d2h()
 
     t_in, t_out, t_both = timed(h2d), timed(d2h), timed(both)
-    print(json.dumps({"h2d_bytes": nin, "d2h_bytes": nout, "h2d_ms": t_in, "d2h_ms": t_out,
-                      "both_ms": t_both, "h2d_GBps": nin / t_in / 1e6,
-                      "d2h_GBps": nout / t_out / 1e6,
-                      "duplex_GBps": (nin + nout) / t_both / 1e6}))
+    return {"h2d_bytes": nin, "d2h_bytes": nout, "h2d_ms": t_in, "d2h_ms": t_out,
+            "both_ms": t_both, "h2d_GBps": nin / t_in / 1e6, "d2h_GBps": nout / t_out / 1e6,
+            "duplex_GBps": (nin + nout) / t_both / 1e6}
 
 
 if __name__ == "__main__":
