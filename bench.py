@@ -143,11 +143,13 @@ def cpu_reference_rate(problem, solver, base, mag, seed, num, windows, g=None):
             ctypes.byref(A.default_tol()), None, cores)
     y = y0.copy()
     run(y, 0.0, 0.1)  # warm-up window
-    y = y0.copy()
+    # the GPU arm's schedule: windows (k mod 10) of [0, 1], restarting from y0
     t = time.perf_counter()
     for k in range(windows):
-        t0 = 0.0 + k * 0.1
-        rc = run(y, t0, 0.0 + (k + 1) * 0.1)
+        if k % 10 == 0:
+            y = y0.copy()
+        t0 = 0.0 + (k % 10) * 0.1
+        rc = run(y, t0, 0.0 + (k % 10 + 1) * 0.1)
         assert rc == 0
     dt = time.perf_counter() - t
     return num * windows / dt, cores, kind, dt
@@ -156,16 +158,18 @@ def cpu_reference_rate(problem, solver, base, mag, seed, num, windows, g=None):
 def run_reference_arm(args):
     from golden_cases import PLEIADES_IC
     rate, cores, kind, dt = cpu_reference_rate("pleiades", "rkck", PLEIADES_IC, 0.01, 42,
-                                               args.cpu_sample, args.warmup + args.steps)
+                                               args.cpu_sample, args.steps)
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / (args.warmup + args.steps) * 1e3, "higher_is_better": True,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "RKCK Pleiades, perturb 0.01 seed 42, eps 1e-10",
+        "config": {"workload": "RKCK Pleiades, perturb 0.01 seed 42, eps 1e-10, windows "
+                               "(k mod 10) of [0, 1] as in the GPU arm",
                    "systems_sampled": args.cpu_sample, "window": 0.1},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"{args.cpu_sample} systems x {args.warmup + args.steps} windows"},
+                         "sample": f"{args.cpu_sample} systems x {args.steps} windows "
+                                   f"(+1 warm-up window)"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
