@@ -93,9 +93,12 @@ static KernelEntry make_entry(int kind, int arith) {
     e.arith = arith;
     e.lanes = L;
     e.maxreg = MAXREG;
-    e.smem_per_thread = SOLVER == 1 ? kRkcSmemStride<C_of<P, L>()>() * (int)sizeof(double)
-                        : KSMEM     ? kSmemStride<C_of<P, L>()>() * (int)sizeof(double)
-                                    : 0;
+    if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1)
+        e.smem_per_thread = nystrom_smem_doubles<P, R>() * (int)sizeof(double);
+    else
+        e.smem_per_thread = SOLVER == 1 ? kRkcSmemStride<C_of<P, L>()>() * (int)sizeof(double)
+                            : KSMEM     ? kSmemStride<C_of<P, L>()>() * (int)sizeof(double)
+                                        : 0;
     e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG>;
     e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                   const double* g, double* y, DevStats* st, long long num, double t,

@@ -44,6 +44,47 @@ __constant__ double c_ck_b[4][5] = {
     {-11.0 / 54.0, 5.0 / 2.0, -70.0 / 27.0, 35.0 / 27.0, 0.0},
     {1631.0 / 55296.0, 175.0 / 512.0, 575.0 / 13824.0, 44275.0 / 110592.0, 253.0 / 4096.0}};
 
+// ---- FAST policy: the same Cash-Karp step in Runge-Kutta-Nystrom form ----
+// With k_m = (V_m, A_m), V_1 = v and V_m = v + h sum_l b_ml A_l, every
+// position-half quantity of the step is a combination of accelerations only:
+//   Q_j        = q + h a_j v + h^2 sum_{l<=j-2} BB_jl A_l,  BB_jl = sum_m b_jm b_ml
+//   yNext_q    = q + h v     + h^2 sum_l CB_l A_l,          CB_l  = sum_m c_m b_ml
+//   yErr_q     =               h^2 sum_l DB_l A_l,          DB_l  = sum_m d_m b_ml
+// (row sums of b are the nodes a_j, sum c_m = 1, sum d_m = 0). Exact algebra,
+// so the FAST step differs from the reference only by rounding, while the
+// velocity stage values V_j are never formed or stored: half the stage
+// storage (A_2..A_5 only), about 40% fewer stage FMAs and shared-memory
+// accesses. EXACT keeps the reference's own operation sequence.
+namespace rkn {
+using namespace ck;
+constexpr double BB[5][4] = {  // rows j = 2..6, columns l = 1..4
+    {0.0, 0.0, 0.0, 0.0},
+    {b32 * b21, 0.0, 0.0, 0.0},
+    {b42 * b21 + b43 * b31, b43 * b32, 0.0, 0.0},
+    {b52 * b21 + b53 * b31 + b54 * b41, b53 * b32 + b54 * b42, b54 * b43, 0.0},
+    {b62 * b21 + b63 * b31 + b64 * b41 + b65 * b51, b63 * b32 + b64 * b42 + b65 * b52,
+     b64 * b43 + b65 * b53, b65 * b54}};
+constexpr double CB0 = c3 * b31 + c4 * b41 + c6 * b61, CB1 = c3 * b32 + c4 * b42 + c6 * b62,
+                 CB2 = c4 * b43 + c6 * b63, CB3 = c6 * b64, CB4 = c6 * b65;
+constexpr double DB0 = d3 * b31 + d4 * b41 + d5 * b51 + d6 * b61,
+                 DB1 = d3 * b32 + d4 * b42 + d5 * b52 + d6 * b62,
+                 DB2 = d4 * b43 + d5 * b53 + d6 * b63, DB3 = d5 * b54 + d6 * b64, DB4 = d6 * b65;
+constexpr double NODE[5] = {a2, a3, a4, a5, a6};
+}  // namespace rkn
+__constant__ double c_rkn_bb[4][4] = {  // stages 3..6 (rolled loop)
+    {rkn::BB[1][0], 0.0, 0.0, 0.0},
+    {rkn::BB[2][0], rkn::BB[2][1], 0.0, 0.0},
+    {rkn::BB[3][0], rkn::BB[3][1], rkn::BB[3][2], 0.0},
+    {rkn::BB[4][0], rkn::BB[4][1], rkn::BB[4][2], rkn::BB[4][3]}};
+__constant__ double c_rkn_node[4] = {rkn::NODE[1], rkn::NODE[2], rkn::NODE[3], rkn::NODE[4]};
+
+// Doubles per thread in the stage-slot row: EXACT stores k2..k5 whole (4N),
+// FAST (Nystrom form) only A_2..A_5 (4 N/2); odd => conflict-free.
+template <class P, class R>
+__host__ __device__ constexpr int nystrom_smem_doubles() {
+    return is_exact<R>::value ? kSmemStride<P::N>() : kSmemStride<P::N / 2>();
+}
+
 // Per-lane solver state: one system, advanced one attempt at a time, so a
 // persistent kernel can hand a lane a new system as soon as its own finishes.
 constexpr bool kRkckUnrollStages = false;  // measured: unrolling adds spills, -16%
@@ -65,7 +106,7 @@ struct NystromRkck {
     // rkck::driver prologue (rkck.cpp:119-128); y must already hold the state
     __device__ __forceinline__ void start(double t_in, double tEnd_in, const DevTol& tol) {
         extern __shared__ double bode_smem[];
-        ks = bode_smem + threadIdx.x * kSmemStride<P::N>();
+        ks = bode_smem + threadIdx.x * nystrom_smem_doubles<P, R>();
         stats_init(st);
         tEnd = R(tEnd_in);
         t = R(t_in);
@@ -92,6 +133,10 @@ struct NystromRkck {
             P::template accel<R>(q, A0);
             if (!haveF) ++st.rhs_evals;
             haveF = true;
+        }
+        if constexpr (!is_exact<R>::value) {
+            attempt_rkn(tol);
+            return;
         }
         R Q[M], Acc[M];
         {  // stage 2: arg = y + h*b21*f0 (rkck.cpp:42-44)
@@ -182,6 +227,113 @@ struct NystromRkck {
                 for (int i = 0; i < M; ++i) kset(out, M + i, Acc[i]);
             }
             BODE_FENCE();
+        }
+    }
+
+    // FAST: one attempt in Nystrom form (see namespace rkn). Slots 0..3 of the
+    // row hold A_2..A_5 (M doubles each); A_1 = A0 and the newest acceleration
+    // stay in registers.
+    __device__ __forceinline__ void attempt_rkn(const DevTol& tol) {
+        using namespace ck;
+        double* const q = reinterpret_cast<double*>(y);
+        double* const v = reinterpret_cast<double*>(y) + M;
+        const double hh = val(h), h2 = hh * hh;
+        double Q[M], Acc[M];
+        {  // stage 2
+            const double ha = hh * a2;  // Q_2 = q + h b21 v (b21 = a2)
+#pragma unroll
+            for (int i = 0; i < M; ++i) Q[i] = fma(ha, v[i], q[i]);
+            P::template accel<double>(Q, Acc);
+        }
+        // stages 3..6: store the newest acceleration A_{j-1} (slot j-3), then
+        // form Q_j from A_1..A_{j-2}
+#pragma unroll 1
+        for (int j = 3; j <= 6; ++j) {
+#pragma unroll
+            for (int i = 0; i < M; ++i) ks[(j - 3) * M + i] = Acc[i];
+            const double ha = hh * c_rkn_node[j - 3];
+            double hb[4];
+#pragma unroll
+            for (int l = 0; l < 4; ++l) hb[l] = h2 * c_rkn_bb[j - 3][l];
+            BODE_FENCE();
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                double s = fma(hb[0], val(A0[i]), fma(ha, v[i], q[i]));
+#pragma unroll
+                for (int l = 1; l < 4; ++l)  // A_{l+1} from slot l-1, predicated to l <= j-3
+                    if (l <= j - 3) s = fma(hb[l], ks[(l - 1) * M + i], s);
+                Q[i] = s;
+            }
+            P::template accel<double>(Q, Acc);
+        }
+        st.rhs_evals += 5;
+        st.stages_total += 6;
+        // error norm (rkck.cpp:75-76, :88-98) and the candidate yNext in one
+        // pass over A_2..A_5; A6 = Acc
+        const double eps = tol.eps, tiny = tol.tiny;
+        const double hd1 = hh * d1, hd3 = hh * d3, hd4 = hh * d4, hd5 = hh * d5, hd6 = hh * d6;
+        const double hc1 = hh * c1, hc3 = hh * c3, hc4 = hh * c4, hc6 = hh * c6;
+        const double e2[5] = {h2 * rkn::DB0, h2 * rkn::DB1, h2 * rkn::DB2, h2 * rkn::DB3,
+                              h2 * rkn::DB4};
+        const double c2[5] = {h2 * rkn::CB0, h2 * rkn::CB1, h2 * rkn::CB2, h2 * rkn::CB3,
+                              h2 * rkn::CB4};
+        double ma[4] = {0.0, 0.0, 0.0, 0.0}, mb[4] = {1.0, 1.0, 1.0, 1.0};
+        int bad = 0;
+#pragma unroll
+        for (int i = 0; i < M; ++i) {
+            const double a1 = val(A0[i]), a2v = ks[i], a3v = ks[M + i], a4v = ks[2 * M + i],
+                         a5v = ks[3 * M + i], a6v = Acc[i];
+            const double eq = fma(e2[4], a5v, fma(e2[3], a4v, fma(e2[2], a3v,
+                              fma(e2[1], a2v, e2[0] * a1))));
+            const double ev = fma(hd6, a6v, fma(hd5, a5v, fma(hd4, a4v, fma(hd3, a3v, hd1 * a1))));
+            Q[i] = fma(c2[4], a5v, fma(c2[3], a4v, fma(c2[2], a3v, fma(c2[1], a2v,
+                   fma(c2[0], a1, fma(hh, v[i], q[i]))))));
+            Acc[i] = fma(hc6, a6v, fma(hc4, a4v, fma(hc3, a3v, fma(hc1, a1, v[i]))));
+            bad |= ((__double2hiint(eq) & 0x7ff00000) == 0x7ff00000) |
+                   ((__double2hiint(ev) & 0x7ff00000) == 0x7ff00000);
+            const double dq = fma(hh, fabs(v[i]), fabs(q[i])) + tiny;
+            const double dv = fma(hh, fabs(a1), fabs(v[i])) + tiny;
+            const int kq = (2 * i) & 3, kv = (2 * i + 1) & 3;
+            if (fabs(eq) * mb[kq] > ma[kq] * dq) { ma[kq] = fabs(eq); mb[kq] = dq; }
+            if (fabs(ev) * mb[kv] > ma[kv] * dv) { ma[kv] = fabs(ev); mb[kv] = dv; }
+        }
+#pragma unroll
+        for (int k = 1; k < 4; ++k)
+            if (ma[k] * mb[0] > ma[0] * mb[k]) { ma[0] = ma[k]; mb[0] = mb[k]; }
+        const double err = ma[0] * rcp_fast(mb[0] * eps);
+        const bool nanFlag = bad != 0;
+        // adjustStep (rkck.cpp:100-113) with a call-free pow
+        double hNew;
+        bool accepted;
+        if (err > 1.0 || !isfinite(err) || nanFlag) {
+            accepted = false;
+            hNew = (!isfinite(err) || nanFlag)
+                       ? tol.p1 * hh
+                       : fmax(tol.safety * hh * ctrl_pow_fast(err, tol.pshrnk), tol.p1 * hh);
+        } else {
+            accepted = true;
+            const double hn =
+                (err > tol.errcon) ? tol.safety * hh * ctrl_pow_fast(err, tol.pgrow) : 5.0 * hh;
+            hNew = fmax(tol.h_min_floor, fmin(val(hMax), hn));
+        }
+        if (accepted) {
+            t += h;
+            stats_accept(st, hh);
+#pragma unroll
+            for (int i = 0; i < M; ++i) {
+                q[i] = Q[i];
+                v[i] = Acc[i];
+            }
+            haveF = false;
+            h = R(hNew);
+            live = tEnd - t > R(tol.uround) * fabs_(tEnd);
+        } else {
+            ++st.steps_rejected;
+            if (hNew < tol.h_min_floor) {  // freeze at the last accepted state
+                st.underflow = 1;
+                live = false;
+            }
+            h = R(hNew);
         }
     }
 

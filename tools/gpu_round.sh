@@ -64,6 +64,9 @@ for p in $PARTS; do
         -s 1 -c 1 -o $OUT/prof_static_w1 python bench.py --steps 10 --warmup 0 --num 1048576 \
         --no-secondary --no-e2e --no-cpu > $OUT/ncu_static.txt 2>&1
       echo "ncu_persist rc=$?" >> $OUT/status.txt ;;
+    ab_fastreg)
+      for R in 255 200 168; do BODE_MAXREG=$R timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/bench_fastreg$R.txt 2>&1; done
+      echo "ab_fastreg rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
