@@ -121,16 +121,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_rate(problem, solver, base, mag, seed, num, windows, g=None):
+def cpu_reference_rate(problem, solver, base, mag, seed, num, windows, g=None, threads=None):
     """The reference CPU path (oracle/_ref = unmodified reference sources;
-    fallback: the oracle restatement) on all host threads."""
+    fallback: the oracle restatement) on all host threads (or `threads`)."""
     from golden_cases import perturb
     from oracle_lib import Oracle, RefLib, ref_available
     from paper_1611_02274_b200 import _abi as A
     prob = A.make_problem(problem, base.size)
     solv = A.SOLVER_NAMES[solver]
     y0 = perturb(base, mag, seed, num)
-    cores = os.cpu_count()
+    cores = threads or os.cpu_count()
     if ref_available():
         lib, kind = RefLib(), "reference"
         run = lambda y, t0, t1: lib.lib.ref_integrate_batch(
@@ -419,9 +419,14 @@ def main():
     if not args.no_cpu:
         rate, cores, kind, dt = cpu_reference_rate("pleiades", "rkck", PLEIADES_IC, 0.01, 42,
                                                    args.cpu_sample, 10)
+        rate1, _, _, dt1 = cpu_reference_rate("pleiades", "rkck", PLEIADES_IC, 0.01, 42,
+                                              max(1024, args.cpu_sample // 16), 10, threads=1)
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
                "sample": f"{args.cpu_sample} Pleiades systems x 10 windows ([0,1]), all host "
-                         f"threads, {dt:.2f} s"}
+                         f"threads, {dt:.2f} s",
+               "one_thread": {"value": rate1, "unit": UNIT, "cores": 1,
+                              "sample": f"{max(1024, args.cpu_sample // 16)} systems x 10 "
+                                        f"windows, {dt1:.2f} s"}}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -444,6 +449,7 @@ def main():
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(), **extra,
         "kernel_ms_per_window": [round(x, 4) for x in per],
+        "systems_per_s_full_protocol": value / 10.0,
         "work_per_system_window": {
             "attempts": float((stats["steps_accepted"] + stats["steps_rejected"]).sum()) / (num * args.steps),
             "rhs_evals": float(stats["rhs_evals"].sum()) / (num * args.steps)},

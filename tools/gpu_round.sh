@@ -68,6 +68,7 @@ for p in $PARTS; do
       for R in 255 200 168; do BODE_MAXREG=$R timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/bench_fastreg$R.txt 2>&1; done
       echo "ab_fastreg rc=$?" >> $OUT/status.txt ;;
     strag) timeout 600 python tools/straggler_sim.py > $OUT/straggler.txt 2>&1; echo "strag rc=$?" >> $OUT/status.txt ;;
+    sweep) timeout 1500 python tools/sweep.py > $OUT/sweep.txt 2>&1; echo "sweep rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
