@@ -274,9 +274,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="bode", choices=["bode", "reference"])
-    ap.add_argument("--num", type=int, default=1 << 22, help="systems per GPU")
+    # (not --num: torchrun's own parser would take it for --numa-binding)
+    ap.add_argument("--systems", dest="num", type=int, default=1 << 22, help="systems per GPU")
     ap.add_argument("--arith", default="fast", choices=["fast", "exact"])
-    ap.add_argument("--rkc-num", type=int, default=1 << 22)
+    ap.add_argument("--rkc-systems", dest="rkc_num", type=int, default=1 << 22)
     ap.add_argument("--persistent", action="store_true",
                     help="persistent kernels with dynamic refill (default: static)")
     ap.add_argument("--no-secondary", dest="secondary", action="store_false",
@@ -303,11 +304,19 @@ def main():
     from golden_cases import PLEIADES_IC, brusselator_ic, brusselator_params, heat_ic, perturb
     from paper_1611_02274_b200.api import stiffness_params
 
+    # BODE_BENCH_SHARE_GPU=1 (functional test of the multi-rank path on one
+    # GPU): ranks share cuda:0 and the barrier/max-over-ranks run on gloo
+    share = os.environ.get("BODE_BENCH_SHARE_GPU") == "1"
+    local = local % torch.cuda.device_count() if share else local
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if share else "cuda"
     L = P.lib()
     L.bode_set_persistent(1 if args.persistent else 0)
     P.api.check(L.bode_set_block_size(args.block))
@@ -330,7 +339,7 @@ def main():
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-        tt = torch.tensor([secs], device="cuda", dtype=torch.float64)
+        tt = torch.tensor([secs], device=red_dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         secs = float(tt.item())
     value = world * num * args.steps / secs
@@ -359,7 +368,7 @@ def main():
                                           ctypes.byref(tol), ctypes.c_void_p(sth.data_ptr()), 1))
         e2e_s = time.perf_counter() - t
         if dist:
-            tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+            tt = torch.tensor([e2e_s], device=red_dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e2e_s = float(tt.item())
         e2e = {"value": world * num * args.steps / e2e_s, "unit": UNIT,
@@ -380,7 +389,7 @@ def main():
     def secs_max(sec):
         if not dist:
             return sec
-        tt = torch.tensor([sec], device="cuda", dtype=torch.float64)
+        tt = torch.tensor([sec], device=red_dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         return float(tt.item())
 

@@ -19,12 +19,12 @@ for p in $PARTS; do
       echo "ab_lanes rc=$?" >> $OUT/status.txt ;;
     ncu_rkc)
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:Heat \
-        -s 1 -c 1 -o $OUT/prof_rkc python bench.py --steps 2 --warmup 1 --num 4096 \
-        --rkc-num 131072 --no-e2e --no-cpu > $OUT/ncu_full_rkc.txt 2>&1
+        -s 1 -c 1 -o $OUT/prof_rkc python bench.py --steps 2 --warmup 1 --systems 4096 \
+        --rkc-systems 131072 --no-e2e --no-cpu > $OUT/ncu_full_rkc.txt 2>&1
       echo "ncu_rkc rc=$?" >> $OUT/status.txt ;;
     ncu_exact)
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:Pleiades \
-        -s 1 -c 1 -o $OUT/prof_rkck_exact python bench.py --arith exact --steps 1 --warmup 1 --num 262144 \
+        -s 1 -c 1 -o $OUT/prof_rkck_exact python bench.py --arith exact --steps 1 --warmup 1 --systems 262144 \
         --no-secondary --no-e2e --no-cpu > $OUT/ncu_full_rkck_exact.txt 2>&1
       echo "ncu_exact rc=$?" >> $OUT/status.txt ;;
     diverge)
@@ -43,13 +43,13 @@ for p in $PARTS; do
       echo "ab_block rc=$?" >> $OUT/status.txt ;;
     ab_rkc)
       for V in "8 128" "8 96" "16 96" "16 128"; do set -- $V
-        BODE_LANES=$1 BODE_MAXREG=$2 timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --num 1048576 --rkc-num 1048576 > $OUT/bench_rkc_L$1_R$2.txt 2>&1; done
-      for R in 96 80; do BODE_LANES=1 BODE_MAXREG=$R timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --num 1048576 --rkc-num 1048576 > $OUT/bench_rkc_exp$R.txt 2>&1; done
+        BODE_LANES=$1 BODE_MAXREG=$2 timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 1048576 --rkc-systems 1048576 > $OUT/bench_rkc_L$1_R$2.txt 2>&1; done
+      for R in 96 80; do BODE_LANES=1 BODE_MAXREG=$R timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 1048576 --rkc-systems 1048576 > $OUT/bench_rkc_exp$R.txt 2>&1; done
       echo "ab_rkc rc=$?" >> $OUT/status.txt ;;
     ncu_late)
       for W in 0 9; do
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:Pleiades, double" \
-        -s $W -c 1 -o $OUT/prof_rkck_w$W python bench.py --steps 10 --warmup 0 --num 262144 \
+        -s $W -c 1 -o $OUT/prof_rkck_w$W python bench.py --steps 10 --warmup 0 --systems 262144 \
         --no-secondary --no-e2e --no-cpu > $OUT/ncu_rkck_w$W.txt 2>&1; done
       echo "ncu_late rc=$?" >> $OUT/status.txt ;;
     e2e)
@@ -58,10 +58,10 @@ for p in $PARTS; do
       echo "e2e rc=$?" >> $OUT/status.txt ;;
     ncu_persist)
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:persistent" \
-        -s 1 -c 1 -o $OUT/prof_persist_w1 python bench.py --steps 10 --warmup 0 --num 1048576 --persistent \
+        -s 1 -c 1 -o $OUT/prof_persist_w1 python bench.py --steps 10 --warmup 0 --systems 1048576 --persistent \
         --no-secondary --no-e2e --no-cpu > $OUT/ncu_persist.txt 2>&1
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:Pleiades, double" \
-        -s 1 -c 1 -o $OUT/prof_static_w1 python bench.py --steps 10 --warmup 0 --num 1048576 \
+        -s 1 -c 1 -o $OUT/prof_static_w1 python bench.py --steps 10 --warmup 0 --systems 1048576 \
         --no-secondary --no-e2e --no-cpu > $OUT/ncu_static.txt 2>&1
       echo "ncu_persist rc=$?" >> $OUT/status.txt ;;
     ab_fastreg)
@@ -69,6 +69,15 @@ for p in $PARTS; do
       echo "ab_fastreg rc=$?" >> $OUT/status.txt ;;
     strag) timeout 600 python tools/straggler_sim.py > $OUT/straggler.txt 2>&1; echo "strag rc=$?" >> $OUT/status.txt ;;
     sweep) timeout 1500 python tools/sweep.py > $OUT/sweep.txt 2>&1; echo "sweep rc=$?" >> $OUT/status.txt ;;
+    multirank)
+      BODE_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+        --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 3 --warmup 3 \
+        --systems 262144 --rkc-systems 65536 --no-cpu > $OUT/bench_2rank.txt 2>&1
+      echo "multirank bode rc=$?" >> $OUT/status.txt
+      timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+        --master-addr 127.0.0.1 --master-port 29512 bench.py --impl reference --gpus 2 --steps 3 \
+        --warmup 3 --cpu-sample 4096 > $OUT/bench_2rank_ref.txt 2>&1
+      echo "multirank ref rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
@@ -76,16 +85,16 @@ for p in $PARTS; do
     bench_exact) timeout 900 python bench.py --arith exact --no-cpu > $OUT/bench_exact.txt 2>&1; echo "bench_exact rc=$?" >> $OUT/status.txt ;;
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-        --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --num 1048576 \
-        --rkc-num 262144 --no-e2e --no-cpu > $OUT/ncu_launches_bench.txt 2>&1
+        --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --systems 1048576 \
+        --rkc-systems 262144 --no-e2e --no-cpu > $OUT/ncu_launches_bench.txt 2>&1
       echo "ncu_launches rc=$?" >> $OUT/status.txt
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:Pleiades \
-        -s 1 -c 1 -o $OUT/prof_rkck python bench.py --steps 1 --warmup 1 --num 262144 \
+        -s 1 -c 1 -o $OUT/prof_rkck python bench.py --steps 1 --warmup 1 --systems 262144 \
         --no-secondary --no-e2e --no-cpu > $OUT/ncu_full_rkck.txt 2>&1
       echo "ncu_full_rkck rc=$?" >> $OUT/status.txt
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:Heat \
-        -s 1 -c 1 -o $OUT/prof_rkc python bench.py --steps 2 --warmup 1 --num 4096 \
-        --rkc-num 131072 --no-e2e --no-cpu > $OUT/ncu_full_rkc.txt 2>&1
+        -s 1 -c 1 -o $OUT/prof_rkc python bench.py --steps 2 --warmup 1 --systems 4096 \
+        --rkc-systems 131072 --no-e2e --no-cpu > $OUT/ncu_full_rkc.txt 2>&1
       echo "ncu_full_rkc rc=$?" >> $OUT/status.txt ;;
   esac
 done
