@@ -78,6 +78,8 @@ for p in $PARTS; do
         --master-addr 127.0.0.1 --master-port 29512 bench.py --impl reference --gpus 2 --steps 3 \
         --warmup 3 --cpu-sample 4096 > $OUT/bench_2rank_ref.txt 2>&1
       echo "multirank ref rc=$?" >> $OUT/status.txt ;;
+    texact) timeout 1500 python -m pytest tests -x -q -m gpu -k "exact or golden or kats or pleiades or stride or variant or cpp" > $OUT/pytest_exact.txt 2>&1; echo "texact rc=$?" >> $OUT/status.txt ;;
+    qexact) timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1; echo "qexact rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
