@@ -137,8 +137,9 @@ __global__ void exact_math_kernel(const double* __restrict__ x, long long n, int
         if (i % 2) return;
         const double a = v, b = x[i + 1];
         ref = __ddiv_rn(a, b);
-        if (!bode::div_in_range(a, b, ref)) return;
-        got = bode::div_rn_bf(a, b);
+        bool fast;
+        got = bode::div_rn_nv(a, b, fast);
+        if (!fast) return;
     } else {
         if (!bode::in_safe_range(v)) return;
         got = op == 0 ? bode::sqrt_rn_bf(v) : bode::rcp_rn_bf(v);

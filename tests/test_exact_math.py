@@ -1,7 +1,7 @@
-"""The EXACT policy's branch-free sqrt / reciprocal (arith.cuh sqrt_rn_bf,
-rcp_rn_bf) must be bitwise the IEEE round-to-nearest results on their
-documented range [2^-400, 2^400]; outside it the kernels fall back to the
-intrinsics. Checked on random bit patterns, log-uniform values, the
+"""The EXACT policy's branch-free sqrt / reciprocal / division (arith.cuh
+sqrt_rn_bf, rcp_rn_bf on [2^-400, 2^400]; div_rn_nv wherever it reports the
+intrinsic's fast path) must be bitwise the IEEE round-to-nearest results;
+outside those domains the kernels fall back to the intrinsics. Checked on random bit patterns, log-uniform values, the
 Pleiades r^2 range and mantissa edge cases."""
 import ctypes
 
