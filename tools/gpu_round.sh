@@ -80,6 +80,9 @@ for p in $PARTS; do
       echo "multirank ref rc=$?" >> $OUT/status.txt ;;
     texact) timeout 1500 python -m pytest tests -x -q -m gpu -k "exact or golden or kats or pleiades or stride or variant or cpp" > $OUT/pytest_exact.txt 2>&1; echo "texact rc=$?" >> $OUT/status.txt ;;
     qexact) timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1; echo "qexact rc=$?" >> $OUT/status.txt ;;
+    ab_exact_lanes)
+      for L in 1 2; do BODE_LANES=$L timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/bench_exact_lanes$L.txt 2>&1; done
+      echo "ab_exact_lanes rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
