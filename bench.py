@@ -235,8 +235,12 @@ def _parse_cpulist(text):
     return cpus
 
 
-def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warmup, stream):
-    """K windows on HBM-resident state; per-launch CUDA events on `stream`."""
+def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warmup, stream,
+                   repack=False):
+    """K windows on HBM-resident state; per-launch CUDA events on `stream`.
+    repack: after the first timed window, re-pack the batch by the cost each
+    system showed (bode_repack_by_cost), and restore the caller's order after
+    the last (bode_unpack); both inside the timed region."""
     num = y0.size // dim
     yd = torch.from_numpy(y0).to("cuda")
     gd = torch.from_numpy(g0).to("cuda") if g0 is not None else None
@@ -250,16 +254,42 @@ def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warm
         P.int_driver_device(prob, solver, arith, t0, 0.0 + (k % 10 + 1) * 0.1, num, gp,
                             yd.data_ptr(), tol, st.data_ptr(), merge, stream.cuda_stream)
 
+    L = P.lib()
+    order = torch.empty(num, dtype=torch.int64, device="cuda") if repack else None
+    cprob = A.Problem(kind=prob.kind, dim=prob.dim, param_dim=prob.param_dim, reserved=0)
     with torch.cuda.stream(stream):
         for k in range(warmup):
             window(k, False)
+            if repack:  # warm the sort/gather kernels and the scratch allocation
+                P.api.check(L.bode_order_init(ctypes.c_void_p(order.data_ptr()), num,
+                                              ctypes.c_void_p(stream.cuda_stream)))
+                for fn in (L.bode_repack_by_cost, L.bode_unpack):
+                    P.api.check(fn(ctypes.byref(cprob), num, ctypes.c_void_p(yd.data_ptr()),
+                                   ctypes.c_void_p(gp), ctypes.c_void_p(st.data_ptr()),
+                                   ctypes.c_void_p(order.data_ptr()),
+                                   ctypes.c_void_p(stream.cuda_stream)))
         yd.copy_(torch.from_numpy(y0))
+        if gd is not None:
+            gd.copy_(torch.from_numpy(g0))
         torch.cuda.synchronize()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
         n0 = P.lib().bode_launch_count()
         ev[0].record(stream)
+        if repack:
+            P.api.check(L.bode_order_init(ctypes.c_void_p(order.data_ptr()), num,
+                                          ctypes.c_void_p(stream.cuda_stream)))
         for k in range(steps):
             window(k, k > 0)
+            if repack and k == 0 and steps > 1:
+                P.api.check(L.bode_repack_by_cost(
+                    ctypes.byref(cprob), num, ctypes.c_void_p(yd.data_ptr()),
+                    ctypes.c_void_p(gp), ctypes.c_void_p(st.data_ptr()),
+                    ctypes.c_void_p(order.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
+            if repack and k == steps - 1:
+                P.api.check(L.bode_unpack(
+                    ctypes.byref(cprob), num, ctypes.c_void_p(yd.data_ptr()),
+                    ctypes.c_void_p(gp), ctypes.c_void_p(st.data_ptr()),
+                    ctypes.c_void_p(order.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
             ev[k + 1].record(stream)
         torch.cuda.synchronize()
     launches = P.lib().bode_launch_count() - n0
@@ -375,9 +405,9 @@ def main():
                "h2d_bytes_per_step": num * 28 * 8, "d2h_bytes_per_step": num * (28 * 8 + 64),
                "ms_per_step": e2e_s / args.steps * 1e3, "pinned_host": True}
 
-    def secondary(problem, solver, arith, dim, y0s, g0s, label, steps):
+    def secondary(problem, solver, arith, dim, y0s, g0s, label, steps, repack=False):
         sec, perw, sts, _, _ = measure_device(P, A, torch, problem, solver, arith, dim, y0s, g0s,
-                                               steps, 1, stream)
+                                               steps, 1, stream, repack=repack)
         f = algorithmic_flops(problem, solver, dim, sts, steps)
         n = y0s.size // dim
         return {"workload": label, "value": world * n * steps / secs_max(sec),
@@ -409,6 +439,19 @@ def main():
             extra["rkc_stiff_expdecay"] = secondary(
                 "expdecay", "rkc", "exact", 1, ye0, g0,
                 f"RKC expDecay, g0 log-uniform in [1,1e4] (config 4), {args.rkc_num} systems, EXACT",
+                min(args.steps, 10))
+            # the same natural-order batch, re-packed by its window-1 cost
+            # (bode_repack_by_cost) and restored at the end, inside the timing
+            extra["rkc_stiff_expdecay_repacked"] = secondary(
+                "expdecay", "rkc", "exact", 1, ye0, g0,
+                f"RKC expDecay, config 4 batch (natural order) re-packed by cost after window "
+                f"1, {args.rkc_num} systems, EXACT", min(args.steps, 10), repack=True)
+            # the same batch with the systems sorted by stiffness (SURVEY 8d config 4:
+            # shuffled and sorted): warps then hold similar stage counts
+            order = np.argsort(g0, kind="stable")
+            extra["rkc_stiff_expdecay_sorted"] = secondary(
+                "expdecay", "rkc", "exact", 1, ye0[order], g0[order],
+                f"RKC expDecay, config 4 batch sorted by g0, {args.rkc_num} systems, EXACT",
                 min(args.steps, 10))
             yb0 = perturb(brusselator_ic(32), 0.01, 7 + rank, args.rkc_num)
             gb0 = brusselator_params(args.rkc_num, 0.02, 0.5)

@@ -95,6 +95,12 @@ def lib():
         "bode_launch_count": (c_i64, []),
         "bode_set_persistent": (ctypes.c_int, [c_i32]),
         "bode_register_kernels": (ctypes.c_int, [vp, c_i32, c_i32]),
+        "bode_order_init": (ctypes.c_int, [vp, c_i64, vp]),
+        "bode_repack_by_cost": (ctypes.c_int, [P(A.Problem), c_i64, vp, vp, vp, vp, vp]),
+        "bode_unpack": (ctypes.c_int, [P(A.Problem), c_i64, vp, vp, vp, vp, vp]),
+        "bode_lockstep_efficiency": (ctypes.c_int, [P(A.Problem), c_i32, c_i32, c_i64, vp, P(c_d),
+                                                    vp]),
+        "bode_set_repack_threshold": (ctypes.c_int, [c_d]),
         "bode_registered_count": (ctypes.c_int, []),
         "bode_integrate_fixed": (ctypes.c_int, [P(A.Problem), c_i32, c_i32, c_d, c_d, c_i64,
                                                 c_i32, c_d, c_i64, PD, PD]),

@@ -37,6 +37,7 @@ thread_local std::string g_last_error;
 std::atomic<long long> g_launches{0};
 std::atomic<int> g_block_override{0};
 std::atomic<int> g_persistent{0};  // dynamic-refill kernels where compiled (opt-in)
+std::atomic<double> g_repack_threshold{0.7};  // outer loop: re-pack below this efficiency
 
 int fail(int code, const std::string& msg) {
     g_last_error = msg;
@@ -337,6 +338,9 @@ struct DeviceBuffers {
     double* g = nullptr;
     DevStats* st = nullptr;
     size_t y_cap = 0, g_cap = 0, st_cap = 0;
+    long long* ord = nullptr;  // outer loop: position -> original index after re-packing
+    double* ysnap = nullptr;   // outer loop: snapshot in original order
+    size_t ord_cap = 0, ysnap_cap = 0;
     cudaStream_t streams[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
     cudaEvent_t events[2 * kMaxChunks] = {};                 // per chunk: H2D done, kernel done
 };
@@ -627,6 +631,65 @@ int bode_set_persistent(int32_t enable) {
     return BODE_OK;
 }
 
+int bode_set_repack_threshold(double threshold) {
+    if (!(threshold >= 0.0 && threshold <= 1.0))
+        return fail(BODE_E_INVALID_SHAPE, "repack threshold must lie in [0, 1]");
+    g_repack_threshold.store(threshold);
+    return BODE_OK;
+}
+
+int bode_order_init(int64_t* order_dev, int64_t num, void* stream) {
+    if (order_dev == nullptr || num < 1) return fail(BODE_E_INVALID_SHAPE, "order: bad arguments");
+    int rc = check_devices(1);
+    if (rc) return rc;
+    rc = bode::init_order(reinterpret_cast<long long*>(order_dev), num,
+                          static_cast<cudaStream_t>(stream));
+    return rc ? fail(rc, "order init failed") : BODE_OK;
+}
+
+int bode_repack_by_cost(const bode_problem_t* p, int64_t num, double* y_dev, double* g_dev,
+                        bode_stats_t* stats_dev, int64_t* order_dev, void* stream) {
+    int rc = check_problem_shape(p);
+    if (rc) return rc;
+    if (num < 1 || y_dev == nullptr || stats_dev == nullptr || order_dev == nullptr ||
+        (p->param_dim > 0 && g_dev == nullptr))
+        return fail(BODE_E_INVALID_SHAPE, "repack: bad arguments");
+    if ((rc = check_devices(1))) return rc;
+    rc = bode::repack_by_cost(p->dim, p->param_dim, num, y_dev, g_dev,
+                              reinterpret_cast<DevStats*>(stats_dev),
+                              reinterpret_cast<long long*>(order_dev),
+                              static_cast<cudaStream_t>(stream));
+    return rc ? fail(rc, "repack failed") : BODE_OK;
+}
+
+int bode_unpack(const bode_problem_t* p, int64_t num, double* y_dev, double* g_dev,
+                bode_stats_t* stats_dev, int64_t* order_dev, void* stream) {
+    int rc = check_problem_shape(p);
+    if (rc) return rc;
+    if (num < 1 || y_dev == nullptr || order_dev == nullptr)
+        return fail(BODE_E_INVALID_SHAPE, "unpack: bad arguments");
+    if ((rc = check_devices(1))) return rc;
+    rc = bode::unpack(p->dim, p->param_dim, num, y_dev, g_dev,
+                      reinterpret_cast<DevStats*>(stats_dev),
+                      reinterpret_cast<long long*>(order_dev), nullptr,
+                      static_cast<cudaStream_t>(stream));
+    return rc ? fail(rc, "unpack failed") : BODE_OK;
+}
+
+int bode_lockstep_efficiency(const bode_problem_t* p, int32_t solver, int32_t arith, int64_t num,
+                             const bode_stats_t* stats_dev, double* efficiency, void* stream) {
+    int rc = check_problem_shape(p);
+    if (rc) return rc;
+    if (num < 1 || stats_dev == nullptr || efficiency == nullptr)
+        return fail(BODE_E_INVALID_SHAPE, "lockstep efficiency: bad arguments");
+    const KernelEntry* e = find_entry(p, solver, arith);
+    if (e == nullptr) return fail(BODE_E_UNSUPPORTED, "no device kernel for this problem");
+    if ((rc = check_devices(1))) return rc;
+    rc = bode::lockstep_efficiency(reinterpret_cast<const DevStats*>(stats_dev), num,
+                                   32 / e->lanes, efficiency, static_cast<cudaStream_t>(stream));
+    return rc ? fail(rc, "lockstep efficiency failed") : BODE_OK;
+}
+
 int bode_int_driver_device(const bode_problem_t* p, int32_t solver, int32_t arith, double t,
                            double t_end, int64_t num, const double* g_dev, double* y_dev,
                            const bode_tol_t* tol, bode_stats_t* stats_dev, int32_t merge_stats,
@@ -677,8 +740,10 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
         if (r) return r;
         if (P > 0 && (r = ensure(&B.g, &B.g_cap, (size_t)sh.count * P))) return r;
         if ((r = ensure(&B.st, &B.st_cap, (size_t)sh.count))) return r;
+        if ((r = ensure(&B.ord, &B.ord_cap, (size_t)sh.count))) return r;
         if (!B.streams[0]) BODE_CUDA(cudaStreamCreateWithFlags(&B.streams[0], cudaStreamNonBlocking));
         cudaStream_t s = B.streams[0];
+        if ((r = bode::init_order(B.ord, sh.count, s))) return fail(r, "order init failed");
         BODE_CUDA(cudaMemcpy2DAsync(B.y, sh.count * sizeof(double), y + sh.begin,
                                     num * sizeof(double), sh.count * sizeof(double), N,
                                     cudaMemcpyHostToDevice, s));
@@ -692,6 +757,8 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
     if (rc) return rc;
 
     double t = t0;
+    std::vector<char> repacked(shards.size(), 0);
+    const double threshold = g_repack_threshold.load();
     for (int64_t k = 1; k <= nwin; ++k) {
         const double tk = (k == nwin) ? t_end : t0 + static_cast<double>(k) * h_outer;
         const bool snap = sink != nullptr || k == nwin;
@@ -700,13 +767,39 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
             DeviceBuffers& B = g_dev[sh.device];
             std::lock_guard<std::mutex> lock(B.m);
             cudaStream_t s = B.streams[0];
+            const size_t si = &sh - shards.data();
             int r = launch_window(e, s, P > 0 ? B.g : nullptr, B.y, B.st, sh.count, t, tk, dt,
                                   k > 1 ? 1 : 0);
             if (r) return r;
+            if (k == nwin && repacked[si]) {  // back to the caller's order, in place
+                if ((r = bode::unpack(N, P, sh.count, B.y, P > 0 ? B.g : nullptr, B.st, B.ord,
+                                      nullptr, s)))
+                    return fail(r, "unpack failed");
+                repacked[si] = 0;
+            }
+            const double* ysrc = B.y;
+            if (snap && repacked[si]) {  // snapshot in the caller's order
+                if ((r = ensure(&B.ysnap, &B.ysnap_cap, (size_t)sh.count * N))) return r;
+                if ((r = bode::unpack(N, P, sh.count, B.y, nullptr, nullptr, B.ord, B.ysnap, s)))
+                    return fail(r, "snapshot unpack failed");
+                ysrc = B.ysnap;
+            }
             if (snap)
-                BODE_CUDA(cudaMemcpy2DAsync(y + sh.begin, num * sizeof(double), B.y,
+                BODE_CUDA(cudaMemcpy2DAsync(y + sh.begin, num * sizeof(double), ysrc,
                                             sh.count * sizeof(double), sh.count * sizeof(double),
                                             N, cudaMemcpyDeviceToHost, s));
+            if (k < nwin && threshold > 0.0 && sh.count >= 1024) {
+                // re-pack when the cost history says warps idle behind stragglers
+                double eff = 1.0;
+                if ((r = bode::lockstep_efficiency(B.st, sh.count, 32 / e->lanes, &eff, s)))
+                    return fail(r, "lockstep efficiency failed");
+                if (eff < threshold) {
+                    if ((r = bode::repack_by_cost(N, P, sh.count, B.y, P > 0 ? B.g : nullptr,
+                                                  B.st, B.ord, s)))
+                        return fail(r, "repack failed");
+                    repacked[si] = 1;
+                }
+            }
             if (k == nwin && stats)
                 BODE_CUDA(cudaMemcpyAsync(stats + sh.begin, B.st, sh.count * sizeof(DevStats),
                                           cudaMemcpyDeviceToHost, s));

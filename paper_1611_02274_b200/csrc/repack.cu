@@ -1,0 +1,248 @@
+// repack.cu -- cost-aware re-packing of a device-resident batch.
+//
+// A warp advances its lane groups in lockstep, so a window costs each warp
+// its slowest system. When per-system cost varies a lot inside warps -- the
+// RKC stage count grows with sqrt(h * sigma), so a stiffness-varied batch in
+// natural order (BASELINE config 4) runs at ~0.3 lockstep efficiency --
+// sorting the systems by the cost they just showed (the window's RHS
+// evaluations, in the per-system stats) puts similar systems in the same
+// warps. Every system is integrated independently and deterministically
+// (batch_driver.hpp:16-21), so the results are bitwise the same in any order;
+// only the position of a system in the arrays changes, tracked by `order`
+// (position -> original index) and undone by bode_unpack.
+//
+// Sorting is CUB's device radix sort (32-bit saturated keys, stable); the
+// permutation is a gather into scratch plus a device copy back, so the caller's
+// buffers keep their addresses.
+#include <cuda_runtime.h>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include <mutex>
+#include <string>
+
+#include "../../include/bode.h"
+#include "dispatch.h"
+
+namespace {
+
+using bode::DevStats;
+
+struct Scratch {
+    std::mutex m;
+    void* p = nullptr;
+    size_t cap = 0;
+};
+Scratch g_scratch[64];
+
+int scratch(int dev, size_t bytes, void** out) {
+    Scratch& s = g_scratch[dev];
+    if (s.cap < bytes) {
+        if (s.p) cudaFree(s.p);
+        s.p = nullptr;
+        s.cap = 0;
+        if (cudaMalloc(&s.p, bytes) != cudaSuccess) return BODE_E_CUDA;
+        s.cap = bytes;
+    }
+    *out = s.p;
+    return BODE_OK;
+}
+
+__global__ void cost_keys(const DevStats* __restrict__ st, long long num,
+                          unsigned* __restrict__ key, unsigned* __restrict__ idx) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= num) return;
+    const long long c = st[i].rhs_evals;
+    key[i] = c < 0 ? 0u : c > 0xffffffffll ? 0xffffffffu : (unsigned)c;
+    idx[i] = (unsigned)i;
+}
+
+// dst[j*num + p] = src[j*num + from[p]] (SoA gather, coalesced writes)
+__global__ void gather_soa(const double* __restrict__ src, double* __restrict__ dst, int rows,
+                           long long num, const unsigned* __restrict__ from) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= num) return;
+    const long long f = from[p];
+    for (int j = 0; j < rows; ++j) dst[j * num + p] = src[j * num + f];
+}
+
+// dst[j*num + to[p]] = src[j*num + p] (SoA scatter)
+__global__ void scatter_soa(const double* __restrict__ src, double* __restrict__ dst, int rows,
+                            long long num, const long long* __restrict__ to) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= num) return;
+    const long long t = to[p];
+    for (int j = 0; j < rows; ++j) dst[j * num + t] = src[j * num + p];
+}
+
+__global__ void gather_stats_order(const DevStats* __restrict__ st, DevStats* __restrict__ st2,
+                                   const long long* __restrict__ ord, long long* __restrict__ ord2,
+                                   long long num, const unsigned* __restrict__ from) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= num) return;
+    const long long f = from[p];
+    if (st) st2[p] = st[f];
+    ord2[p] = ord[f];
+}
+
+__global__ void scatter_stats(const DevStats* __restrict__ st, DevStats* __restrict__ st2,
+                              long long num, const long long* __restrict__ to) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= num) return;
+    st2[to[p]] = st[p];
+}
+
+__global__ void identity_order(long long* __restrict__ ord, long long num) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < num) ord[p] = p;
+}
+
+// sums of per-group mean and max cost over groups of `group` consecutive systems
+__global__ void lockstep_sums(const DevStats* __restrict__ st, long long num, int group,
+                              unsigned long long* __restrict__ sums) {
+    const long long gidx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long b = gidx * group;
+    if (b >= num) return;
+    unsigned long long s = 0, m = 0;
+    for (int k = 0; k < group && b + k < num; ++k) {
+        const long long c = st[b + k].rhs_evals;
+        const unsigned long long u = c > 0 ? (unsigned long long)c : 0ull;
+        s += u;
+        m = u > m ? u : m;
+    }
+    const int n = (int)((num - b) < group ? (num - b) : group);
+    atomicAdd(&sums[0], s);
+    atomicAdd(&sums[1], m * (unsigned long long)n);
+}
+
+inline unsigned blocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
+
+int cuda_fail(cudaError_t e) {
+    (void)e;
+    return BODE_E_CUDA;
+}
+
+#define RP_CUDA(call)                                      \
+    do {                                                   \
+        cudaError_t e_ = (call);                           \
+        if (e_ != cudaSuccess) return cuda_fail(e_);       \
+    } while (0)
+
+}  // namespace
+
+namespace bode {
+
+// Sorts the systems by cost (stats[i].rhs_evals) and permutes y, g, stats and
+// order accordingly; all pointers are device pointers on the current device.
+int repack_by_cost(int N, int P, long long num, double* y, double* g, DevStats* st,
+                   long long* order, cudaStream_t s) {
+    if (num < 2 || st == nullptr || order == nullptr) return BODE_OK;
+    int dev = 0;
+    RP_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_scratch[dev].m);
+    size_t sort_bytes = 0;
+    RP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (unsigned*)nullptr,
+                                            (unsigned*)nullptr, (unsigned*)nullptr,
+                                            (unsigned*)nullptr, (int)num, 0, 32, s));
+    const size_t n = (size_t)num;
+    const int rows = N > P ? N : P;
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t bytes = 4 * al(n * sizeof(unsigned)) + al(sort_bytes) +
+                         al(n * rows * sizeof(double)) + al(n * sizeof(DevStats)) +
+                         al(n * sizeof(long long));
+    void* base = nullptr;
+    if (scratch(dev, bytes, &base) != BODE_OK) return BODE_E_CUDA;
+    char* c = static_cast<char*>(base);
+    unsigned* key = reinterpret_cast<unsigned*>(c);
+    c += al(n * sizeof(unsigned));
+    unsigned* key2 = reinterpret_cast<unsigned*>(c);
+    c += al(n * sizeof(unsigned));
+    unsigned* idx = reinterpret_cast<unsigned*>(c);
+    c += al(n * sizeof(unsigned));
+    unsigned* from = reinterpret_cast<unsigned*>(c);
+    c += al(n * sizeof(unsigned));
+    void* tmp = c;
+    c += al(sort_bytes);
+    double* buf = reinterpret_cast<double*>(c);
+    c += al(n * rows * sizeof(double));
+    DevStats* st2 = reinterpret_cast<DevStats*>(c);
+    c += al(n * sizeof(DevStats));
+    long long* ord2 = reinterpret_cast<long long*>(c);
+
+    cost_keys<<<blocks(num, 256), 256, 0, s>>>(st, num, key, idx);
+    RP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, key, key2, idx, from, (int)num, 0,
+                                            32, s));
+    gather_soa<<<blocks(num, 256), 256, 0, s>>>(y, buf, N, num, from);
+    RP_CUDA(cudaMemcpyAsync(y, buf, n * N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (P > 0 && g != nullptr) {
+        gather_soa<<<blocks(num, 256), 256, 0, s>>>(g, buf, P, num, from);
+        RP_CUDA(cudaMemcpyAsync(g, buf, n * P * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    gather_stats_order<<<blocks(num, 256), 256, 0, s>>>(st, st2, order, ord2, num, from);
+    RP_CUDA(cudaMemcpyAsync(st, st2, n * sizeof(DevStats), cudaMemcpyDeviceToDevice, s));
+    RP_CUDA(cudaMemcpyAsync(order, ord2, n * sizeof(long long), cudaMemcpyDeviceToDevice, s));
+    RP_CUDA(cudaGetLastError());
+    return BODE_OK;
+}
+
+// Scatters y (and g, stats) back to original positions and resets order.
+// With y_out != nullptr only y is scattered, into y_out (a snapshot), and
+// nothing else changes.
+int unpack(int N, int P, long long num, double* y, double* g, DevStats* st, long long* order,
+           double* y_out, cudaStream_t s) {
+    if (num < 1 || order == nullptr) return BODE_OK;
+    if (y_out != nullptr) {
+        scatter_soa<<<blocks(num, 256), 256, 0, s>>>(y, y_out, N, num, order);
+        RP_CUDA(cudaGetLastError());
+        return BODE_OK;
+    }
+    int dev = 0;
+    RP_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(g_scratch[dev].m);
+    const size_t n = (size_t)num;
+    const int rows = N > P ? N : P;
+    const size_t bytes = ((n * rows * sizeof(double) + 255) & ~size_t(255)) + n * sizeof(DevStats);
+    void* base = nullptr;
+    if (scratch(dev, bytes, &base) != BODE_OK) return BODE_E_CUDA;
+    double* buf = static_cast<double*>(base);
+    DevStats* st2 = reinterpret_cast<DevStats*>(static_cast<char*>(base) +
+                                                ((n * rows * sizeof(double) + 255) & ~size_t(255)));
+    scatter_soa<<<blocks(num, 256), 256, 0, s>>>(y, buf, N, num, order);
+    RP_CUDA(cudaMemcpyAsync(y, buf, n * N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (P > 0 && g != nullptr) {
+        scatter_soa<<<blocks(num, 256), 256, 0, s>>>(g, buf, P, num, order);
+        RP_CUDA(cudaMemcpyAsync(g, buf, n * P * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    if (st != nullptr) {
+        scatter_stats<<<blocks(num, 256), 256, 0, s>>>(st, st2, num, order);
+        RP_CUDA(cudaMemcpyAsync(st, st2, n * sizeof(DevStats), cudaMemcpyDeviceToDevice, s));
+    }
+    identity_order<<<blocks(num, 256), 256, 0, s>>>(order, num);
+    RP_CUDA(cudaGetLastError());
+    return BODE_OK;
+}
+
+int init_order(long long* order, long long num, cudaStream_t s) {
+    identity_order<<<blocks(num, 256), 256, 0, s>>>(order, num);
+    RP_CUDA(cudaGetLastError());
+    return BODE_OK;
+}
+
+// Lockstep efficiency of the stats' costs for warps of `group` systems:
+// sum(cost) / sum(group max * group size). Synchronises the stream.
+int lockstep_efficiency(const DevStats* st, long long num, int group, double* eff,
+                        cudaStream_t s) {
+    unsigned long long* d = nullptr;
+    RP_CUDA(cudaMallocAsync(&d, 2 * sizeof(unsigned long long), s));
+    RP_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), s));
+    const long long groups = (num + group - 1) / group;
+    lockstep_sums<<<blocks(groups, 256), 256, 0, s>>>(st, num, group, d);
+    unsigned long long h[2] = {0, 0};
+    RP_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
+    RP_CUDA(cudaFreeAsync(d, s));
+    RP_CUDA(cudaStreamSynchronize(s));
+    *eff = h[1] ? (double)h[0] / (double)h[1] : 1.0;
+    return BODE_OK;
+}
+
+}  // namespace bode

@@ -4,7 +4,8 @@
 Lockstep efficiency of a warp = mean(attempts) / max(attempts) over its 32
 consecutive systems (one system per lane), i.e. the fraction of issue slots
 doing useful attempts when every lane waits for the slowest system.
-    python tools/divergence.py [--problem pleiades|heat] [--num N] [--arith fast]
+    python tools/divergence.py [--problem pleiades|heat|expdecay|expdecay_sorted] [--num N]
+                               [--arith fast]
 """
 import argparse
 import json
@@ -30,12 +31,23 @@ def main():
     from paper_1611_02274_b200 import _abi as A
     from golden_cases import PLEIADES_IC, heat_ic, perturb
 
+    from paper_1611_02274_b200.api import stiffness_params
+    gh = None
     if args.problem == "pleiades":
         dim, solver, base, lanes = 28, "rkck", PLEIADES_IC, 1
-    else:
-        dim, solver, base, lanes = 64, "rkc", heat_ic(64), 4
-    prob = P.OdeProblem(A.PROBLEM_NAMES[args.problem], dim, 0)
-    y = torch.from_numpy(perturb(base, args.mag, 42, args.num)).cuda()
+    elif args.problem == "heat":
+        dim, solver, base, lanes = 64, "rkc", heat_ic(64), 8
+    else:  # config 4: expdecay (natural order) or expdecay_sorted (sorted by g0)
+        dim, solver, base, lanes = 1, "rkc", np.array([1.0]), 1
+        gh = stiffness_params(args.num)
+    y0 = perturb(base, args.mag, 42, args.num)
+    if args.problem == "expdecay_sorted":
+        order = np.argsort(gh, kind="stable")
+        gh, y0 = gh[order], y0[order]
+    kind = "expdecay" if args.problem.startswith("expdecay") else args.problem
+    prob = P.OdeProblem(A.PROBLEM_NAMES[kind], dim, 0 if gh is None else 1)
+    y = torch.from_numpy(y0).cuda()
+    g = torch.from_numpy(gh).cuda() if gh is not None else None
     st = torch.zeros(args.num * 8, dtype=torch.int64, device="cuda")
     tol = A.default_tol()
     s = torch.cuda.current_stream()
@@ -44,7 +56,8 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         P.int_driver_device(prob, solver, args.arith, 0.1 * k, 1.0 if k == 9 else 0.1 * (k + 1),
-                            args.num, 0, y.data_ptr(), tol, st.data_ptr(), False, s.cuda_stream)
+                            args.num, g.data_ptr() if g is not None else 0, y.data_ptr(), tol,
+                            st.data_ptr(), False, s.cuda_stream)
         e1.record()
         torch.cuda.synchronize()
         stats = st.cpu().numpy().view(A.STATS_DTYPE)

@@ -30,6 +30,8 @@ for p in $PARTS; do
     diverge)
       timeout 600 python tools/divergence.py --problem pleiades > $OUT/diverge_pleiades.txt 2>&1
       timeout 600 python tools/divergence.py --problem heat --num 262144 --arith exact > $OUT/diverge_heat.txt 2>&1
+      timeout 600 python tools/divergence.py --problem expdecay --num 1048576 --arith exact > $OUT/diverge_expdecay.txt 2>&1
+      timeout 600 python tools/divergence.py --problem expdecay_sorted --num 1048576 --arith exact > $OUT/diverge_expdecay_sorted.txt 2>&1
       echo "diverge rc=$?" >> $OUT/status.txt ;;
     ab_persist)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/bench_static.txt 2>&1
@@ -83,6 +85,7 @@ for p in $PARTS; do
     ab_exact_lanes)
       for L in 1 2; do BODE_LANES=$L timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/bench_exact_lanes$L.txt 2>&1; done
       echo "ab_exact_lanes rc=$?" >> $OUT/status.txt ;;
+    qrkc) timeout 900 python bench.py --no-e2e --no-cpu --steps 10 --systems 65536 > $OUT/quick_rkc.txt 2>&1; echo "qrkc rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
