@@ -42,7 +42,8 @@ def main():
     st = torch.zeros(num * 8, dtype=torch.int64, device="cuda")
     tol = A.default_tol()
     s = torch.cuda.current_stream()
-    tot = {"static": 0.0}
+    tot = {"static": 0.0, "sorted_by_prev": 0.0}
+    cum = np.zeros(num, np.int64)
     for k in range(10):
         P.int_driver_device(prob, "rkck", "fast", 0.1 * k, 1.0 if k == 9 else 0.1 * (k + 1), num, 0,
                             y.data_ptr(), tol, st.data_ptr(), False, s.cuda_stream)
@@ -52,6 +53,13 @@ def main():
         static = a.reshape(-1, 32).max(axis=1).sum()
         row = {"window": k, "useful": int(a.sum()), "static": int(static) * 32}
         tot["static"] += static
+        # order for this window = systems sorted by their cumulative cost so far
+        # (what bode_repack_by_cost would have done after the previous window)
+        order = np.argsort(cum, kind="stable") if k > 0 else np.arange(num)
+        sp = a[order].reshape(-1, 32).max(axis=1).sum()
+        row["sorted_by_prev"] = int(sp) * 32
+        tot["sorted_by_prev"] += sp
+        cum += a
         for T in (4, 8, 16, 24):
             c, n2 = two_pass(a, T)
             row[f"T{T}"] = int(c) * 32
