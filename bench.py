@@ -455,6 +455,11 @@ def main():
                 min(args.steps, 10))
             yb0 = perturb(brusselator_ic(32), 0.01, 7 + rank, args.rkc_num)
             gb0 = brusselator_params(args.rkc_num, 0.02, 0.5)
+            gbn = brusselator_params(args.rkc_num, 0.002, 0.02)
+            extra["rkck_brusselator_fast"] = secondary(
+                "brusselator", "rkck", "fast", 64, yb0, gbn,
+                f"RKCK FAST Brusselator n=32 (registered problem, generic RKCK kernel), alpha "
+                f"log-spaced in [0.002, 0.02], {args.rkc_num} systems", min(args.steps, 10))
             extra["rkc_brusselator"] = secondary(
                 "brusselator", "rkc", "exact", 64, yb0, gb0,
                 f"RKC Brusselator reaction-diffusion n=32 (dim 64, registered problem), alpha "

@@ -51,6 +51,24 @@ struct Brusselator {
 
 }  // namespace bode
 
-// n = 32 grid points (dim 64): RKCK with 4 lanes per system (stage slots in
-// shared memory), RKC with 8 lanes, 128 registers (16 warps/SM)
-BODE_REGISTER_PROBLEM_R(brusselator32, bode::Brusselator<32>, BODE_PROBLEM_BRUSSELATOR, 4, 8, 128)
+// n = 32 grid points (dim 64): RKC with 8 lanes per system at 128 registers
+// (16 warps/SM); RKCK candidates (lanes x register cap) registered in
+// preference order, selectable with BODE_LANES / BODE_MAXREG for A/B runs
+namespace {
+using Bru = bode::Brusselator<32>;
+const int bode_registered_brusselator32 = [] {
+    static const bode::KernelEntry e[] = {
+        bode::make_entry<Bru, bode::xd, 8, 1, false, 128>(BODE_PROBLEM_BRUSSELATOR, BODE_ARITH_EXACT),
+        bode::make_entry<Bru, double, 8, 1, false, 128>(BODE_PROBLEM_BRUSSELATOR, BODE_ARITH_FAST),
+        // RKCK FAST measured (2^20 systems, 5 windows, FP64 fraction): 8 lanes @128
+        // 0.490, 4 @255 0.483, 8 @255 0.437, 16 @128 0.410, 4 @128 0.326
+        bode::make_entry<Bru, double, 8, 0, true, 128>(BODE_PROBLEM_BRUSSELATOR, BODE_ARITH_FAST),
+        bode::make_entry<Bru, bode::xd, 8, 0, true, 128>(BODE_PROBLEM_BRUSSELATOR, BODE_ARITH_EXACT),
+        bode::make_entry<Bru, bode::xd, 4, 0, true, 0>(BODE_PROBLEM_BRUSSELATOR, BODE_ARITH_EXACT),
+        bode::make_entry<Bru, double, 4, 0, true, 0>(BODE_PROBLEM_BRUSSELATOR, BODE_ARITH_FAST),
+        bode::make_entry<Bru, double, 16, 0, true, 128>(BODE_PROBLEM_BRUSSELATOR, BODE_ARITH_FAST),
+    };
+    return bode_register_kernels(e, (int32_t)(sizeof(e) / sizeof(e[0])),
+                                 (int32_t)sizeof(bode::KernelEntry));
+}();
+}  // namespace

@@ -102,6 +102,7 @@ __device__ __forceinline__ bool rkck_adjust(R h, R err, bool nanFlag, R hMin, R 
         return false;
     }
     R hn = (err > R(tol.errcon)) ? R(tol.safety) * h * pow_(err, R(tol.pgrow), tol.powtab) : R(5.0) * h;
+    // (FAST: pow_ is ctrl_pow_fast, arith.cuh)
     hNew = fmax_(hMin, fmin_(hMax, hn));
     return true;
 }
@@ -136,38 +137,66 @@ __device__ __forceinline__ void rkck_system(const Group<L>& G, double t_in, doub
             haveF = true;
         }
         // ---- rkck::step (rkck.cpp:42-64): five stage evaluations ----
+        // The newest stage derivative is the last term of every stage sum, so
+        // it is read from the RHS output registers (`out`) rather than reloaded
+        // -- the reference's summation order is unchanged. FAST folds h into
+        // the weights (one FMA per term).
+        const R hh = h;
+        auto stage_arg = [&](int c, double w1, const double* wk, int nk, R newest, double wn) -> R {
+            if constexpr (is_exact<R>::value) {
+                R s = R(w1) * f0[c];
+                for (int m = 0; m < nk; ++m) s = s + R(wk[m]) * K.get(m, c);
+                s = s + R(wn) * newest;
+                return y[c] + hh * s;
+            } else {
+                double s = fma(val(hh) * w1, val(f0[c]), val(y[c]));
+                for (int m = 0; m < nk; ++m) s = fma(val(hh) * wk[m], val(K.get(m, c)), s);
+                return R(fma(val(hh) * wn, val(newest), s));
+            }
+        };
         // stage 2: y + h*b21*f0
 #pragma unroll
         for (int c = 0; c < C; ++c) arg[c] = y[c] + h * R(b21) * f0[c];
         P::template rhs<R, L>(G, t + R(a2) * h, arg, g, out);
-#pragma unroll
-        for (int c = 0; c < C; ++c) K.set(0, c, out[c]);
         // stage 3
+        {
+            const double w[1] = {0.0};
 #pragma unroll
-        for (int c = 0; c < C; ++c) arg[c] = y[c] + h * (R(b31) * f0[c] + R(b32) * K.get(0, c));
+            for (int c = 0; c < C; ++c) {
+                arg[c] = stage_arg(c, b31, w, 0, out[c], b32);
+                K.set(0, c, out[c]);
+            }
+        }
         P::template rhs<R, L>(G, t + R(a3) * h, arg, g, out);
-#pragma unroll
-        for (int c = 0; c < C; ++c) K.set(1, c, out[c]);
         // stage 4
+        {
+            const double w[1] = {b42};
 #pragma unroll
-        for (int c = 0; c < C; ++c)
-            arg[c] = y[c] + h * (R(b41) * f0[c] + R(b42) * K.get(0, c) + R(b43) * K.get(1, c));
+            for (int c = 0; c < C; ++c) {
+                arg[c] = stage_arg(c, b41, w, 1, out[c], b43);
+                K.set(1, c, out[c]);
+            }
+        }
         P::template rhs<R, L>(G, t + R(a4) * h, arg, g, out);
-#pragma unroll
-        for (int c = 0; c < C; ++c) K.set(2, c, out[c]);
         // stage 5
+        {
+            const double w[2] = {b52, b53};
 #pragma unroll
-        for (int c = 0; c < C; ++c)
-            arg[c] = y[c] + h * (R(b51) * f0[c] + R(b52) * K.get(0, c) + R(b53) * K.get(1, c) +
-                                 R(b54) * K.get(2, c));
+            for (int c = 0; c < C; ++c) {
+                arg[c] = stage_arg(c, b51, w, 2, out[c], b54);
+                K.set(2, c, out[c]);
+            }
+        }
         P::template rhs<R, L>(G, t + R(a5) * h, arg, g, out);
-#pragma unroll
-        for (int c = 0; c < C; ++c) K.set(3, c, out[c]);
         // stage 6
+        {
+            const double w[3] = {b62, b63, b64};
 #pragma unroll
-        for (int c = 0; c < C; ++c)
-            arg[c] = y[c] + h * (R(b61) * f0[c] + R(b62) * K.get(0, c) + R(b63) * K.get(1, c) +
-                                 R(b64) * K.get(2, c) + R(b65) * K.get(3, c));
+            for (int c = 0; c < C; ++c) {
+                arg[c] = stage_arg(c, b61, w, 3, out[c], b65);
+                K.set(3, c, out[c]);
+            }
+        }
         P::template rhs<R, L>(G, t + R(a6) * h, arg, g, out);  // out = k6
         st.rhs_evals += 5;
         st.stages_total += 6;
@@ -175,18 +204,50 @@ __device__ __forceinline__ void rkck_system(const Group<L>& G, double t_in, doub
         // ---- yErr folded into errorNorm (rkck.cpp:75-76, :88-98) ----
         R err(0.0);
         bool nanFlag = false;
+        if constexpr (is_exact<R>::value) {
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            const R yErr = h * (R(d1) * f0[c] + R(d3) * K.get(1, c) + R(d4) * K.get(2, c) +
-                                R(d5) * K.get(3, c) + R(d6) * out[c]);
-            if (!isfinite_(yErr)) nanFlag = true;
-            err = fmax_(err, fabs_(yErr / (fabs_(y[c]) + fabs_(h * f0[c]) + tiny)));
+            for (int c = 0; c < C; ++c) {
+                const R yErr = h * (R(d1) * f0[c] + R(d3) * K.get(1, c) + R(d4) * K.get(2, c) +
+                                    R(d5) * K.get(3, c) + R(d6) * out[c]);
+                if (!isfinite_(yErr)) nanFlag = true;
+                err = fmax_(err, fabs_(yErr / (fabs_(y[c]) + fabs_(h * f0[c]) + tiny)));
+            }
+            if constexpr (L > 1) {
+                err = R(G.max_all(val(err)));
+                nanFlag = G.any(nanFlag);
+            }
+            err = err / eps;
+        } else {
+            // FAST: argmax of |e|/d by cross-multiplication, one reciprocal; the
+            // candidate yNext goes into arg (free now), in the same pass
+            const double hv = val(h);
+            const double hd1 = hv * d1, hd3 = hv * d3, hd4 = hv * d4, hd5 = hv * d5, hd6 = hv * d6;
+            const double hc1 = hv * c1, hc3 = hv * c3, hc4 = hv * c4, hc6 = hv * c6;
+            double ma = 0.0, mb = 1.0;
+            int bad = 0;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const double k3 = val(K.get(1, c)), k4 = val(K.get(2, c)), k6 = val(out[c]);
+                const double e = fma(hd6, k6, fma(hd5, val(K.get(3, c)),
+                                 fma(hd4, k4, fma(hd3, k3, hd1 * val(f0[c])))));
+                arg[c] = R(fma(hc6, k6, fma(hc4, k4, fma(hc3, k3, fma(hc1, val(f0[c]), val(y[c]))))));
+                bad |= (__double2hiint(e) & 0x7ff00000) == 0x7ff00000;
+                const double d = fma(hv, fabs(val(f0[c])), fabs(val(y[c]))) + val(tiny);
+                if (fabs(e) * mb > ma * d) { ma = fabs(e); mb = d; }
+            }
+            if constexpr (L > 1) {
+#pragma unroll
+                for (int o = L / 2; o > 0; o /= 2) {
+                    const double oa = __shfl_xor_sync(G.mask, ma, o, L);
+                    const double ob = __shfl_xor_sync(G.mask, mb, o, L);
+                    if (oa * mb > ma * ob) { ma = oa; mb = ob; }
+                }
+                nanFlag = G.any(bad != 0);
+            } else {
+                nanFlag = bad != 0;
+            }
+            err = R(ma * rcp_fast(mb * val(eps)));
         }
-        if constexpr (L > 1) {
-            err = R(G.max_all(val(err)));
-            nanFlag = G.any(nanFlag);
-        }
-        err = err / eps;
 
         R hNew;
         const bool accepted = rkck_adjust(h, err, nanFlag, hMin, hMax, tol, hNew);
@@ -194,10 +255,15 @@ __device__ __forceinline__ void rkck_system(const Group<L>& G, double t_in, doub
             t += h;
             stats_accept(st, val(h));
             // yNext (rkck.cpp:74), written over y once the step is accepted
+            if constexpr (is_exact<R>::value) {
 #pragma unroll
-            for (int c = 0; c < C; ++c)
-                y[c] = y[c] + h * (R(c1) * f0[c] + R(c3) * K.get(1, c) + R(c4) * K.get(2, c) +
-                                   R(c6) * out[c]);
+                for (int c = 0; c < C; ++c)
+                    y[c] = y[c] + h * (R(c1) * f0[c] + R(c3) * K.get(1, c) + R(c4) * K.get(2, c) +
+                                       R(c6) * out[c]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < C; ++c) y[c] = arg[c];
+            }
             haveF = false;
             h = hNew;
         } else {

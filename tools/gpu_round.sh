@@ -86,6 +86,10 @@ for p in $PARTS; do
       for L in 1 2; do BODE_LANES=$L timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/bench_exact_lanes$L.txt 2>&1; done
       echo "ab_exact_lanes rc=$?" >> $OUT/status.txt ;;
     qrkc) timeout 900 python bench.py --no-e2e --no-cpu --steps 10 --systems 65536 > $OUT/quick_rkc.txt 2>&1; echo "qrkc rc=$?" >> $OUT/status.txt ;;
+    ab_bru)
+      for V in "4 255" "4 128" "8 255" "8 128" "16 128"; do set -- $V
+        BODE_LANES=$1 BODE_MAXREG=$2 timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 65536 --rkc-systems 1048576 > $OUT/bench_bru_L$1_R$2.txt 2>&1; done
+      echo "ab_bru rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
