@@ -248,7 +248,7 @@ struct NystromRkck {
         // stages 3..6: store the newest acceleration A_{j-1} (slot j-3), then
         // form Q_j from A_1..A_{j-2}
 #pragma unroll 1
-        for (int j = 3; j <= 6; ++j) {
+        for (int j = 3; j <= 6; ++j) {  // rolled: fully unrolled measured 13% slower
 #pragma unroll
             for (int i = 0; i < M; ++i) ks[(j - 3) * M + i] = Acc[i];
             const double ha = hh * c_rkn_node[j - 3];
