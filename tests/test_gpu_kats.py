@@ -99,3 +99,39 @@ def test_launch_counter_advances(gpu):
     n0 = B.lib().bode_launch_count()
     B.integrate_batch(B.problems.zero(2), B.pack([[1.0, 2.0]]), 0.0, 1.0)
     assert B.lib().bode_launch_count() > n0
+
+
+@pytest.mark.parametrize("arith", ["exact", "fast"])
+@pytest.mark.parametrize("problem", ["pleiades", "expdecay"])
+def test_nan_freeze_all_paths(gpu, arith, problem):
+    """rkck.cpp:150-154 on every RKCK kernel path: the Nystrom/RKN Pleiades
+    kernels (FAST, 1 lane), the lane-pair kernel (EXACT) and the generic one
+    (expDecay). A NaN system freezes with the underflow flag; every other
+    system is bitwise what it is without the NaN neighbour."""
+    import numpy as np
+    from paper_1611_02274_b200 import _abi as A
+    from golden_cases import PLEIADES_IC, perturb
+    num = 64
+    if problem == "pleiades":
+        prob, base, g = A.make_problem(A.PLEIADES), PLEIADES_IC, None
+    else:
+        prob, base = A.make_problem(A.EXPDECAY), np.array([1.0])
+        g = np.linspace(0.5, 5.0, num)
+    y0 = perturb(base, 0.01, 5, num)
+    bad = y0.copy()
+    bad[7 + num * min(3, prob.dim - 1)] = float("nan")  # one component of system 7
+
+    def run(y):
+        b = B.BatchStates(num, prob.dim, prob.param_dim, y.copy(),
+                          g.copy() if g is not None else np.zeros(0))
+        return B.integrate_batch(B.OdeProblem(prob.kind, prob.dim, prob.param_dim), b, 0.0, 0.1,
+                                 solver="rkck", arith=arith)
+
+    ref, got = run(y0), run(bad)
+    assert got.stats["underflow"][7] == 1
+    ys = got.states.values.reshape(prob.dim, num)
+    assert np.array_equal(ys[:, 7].view(np.uint64), bad.reshape(prob.dim, num)[:, 7].view(np.uint64))
+    others = np.arange(num) != 7
+    assert np.array_equal(ys[:, others].view(np.uint64),
+                          ref.states.values.reshape(prob.dim, num)[:, others].view(np.uint64))
+    assert not got.stats["underflow"][others].any()
