@@ -19,6 +19,12 @@
 //   };
 //   BODE_REGISTER_PROBLEM(my_problem, MyProblem, BODE_PROBLEM_USER_BASE + 0, 1, 1)
 //
+// Second-order systems (q' = v, v' = a(t, q; g)) derive from
+// bode::SecondOrderProblem<Self, dim(q), P> and provide only
+//   template <class R> __device__ static void accel(R t, const R* q, const R* g, R* a);
+// RKCK then runs the Nystrom kernels (one lane per system; FAST in
+// Runge-Kutta-Nystrom form, the fastest path in this library).
+//
 // R is bode::xd under the EXACT policy -- every + - * / is one IEEE binary64
 // operation, so written in the host code's expression order the device result
 // is bitwise the host's -- and double under FAST (FMA contraction allowed).

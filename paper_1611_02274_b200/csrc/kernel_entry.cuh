@@ -25,7 +25,7 @@ namespace bode {
 template <class P, int L>
 __device__ __forceinline__ int comp_index(int lane, int c) {
     constexpr int C = P::N / L;
-    if constexpr (is_second_order<P>::value && L == 2)
+    if constexpr (is_pleiades<P> && L == 2)
         return c < 7 ? 7 * lane + c : 14 + 7 * lane + (c - 7);
     else
         return lane * C + c;
@@ -51,10 +51,10 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
 #pragma unroll
     for (int p = 0; p < PP; ++p) g[p] = R(P::P > 0 ? g_soa[sys + num * (long long)p] : 0.0);
     DevStats st;
-    if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 2)
+    if constexpr (SOLVER == 0 && is_pleiades<P> && L == 2)
         rkck_pleiades2_system<R>(G, t, tEnd, y, tol, st);
-    else if constexpr (SOLVER == 0 && is_second_order<P>::value)
-        rkck_nystrom_system<P, R>(t, tEnd, y, tol, st);
+    else if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1)
+        rkck_nystrom_system<P, R>(t, tEnd, y, g, tol, st);
     else if constexpr (SOLVER == 0)
         rkck_system<P, R, L, KSMEM>(G, t, tEnd, y, g, tol, st);
     else
@@ -116,7 +116,7 @@ static KernelEntry make_entry(int kind, int arith) {
         return (int)err;
     };
     e.build_rkc_table = nullptr;
-    if constexpr (!(SOLVER == 0 && is_second_order<P>::value && L == 2)) {
+    if constexpr (!(SOLVER == 0 && is_pleiades<P> && L == 2)) {
         e.ffn = (const void*)&fixed_kernel<P, R, L, SOLVER>;
         e.launch_fixed = [](const void* fn, dim3 grid, dim3 block, cudaStream_t s,
                             const double* g, double* y, long long num, double t0, double tEnd,
@@ -127,7 +127,7 @@ static KernelEntry make_entry(int kind, int arith) {
             return (int)cudaGetLastError();
         };
     }
-    if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1) {
+    if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1 && P::P == 0) {
         // (routing static launches through this instance with counter == nullptr
         // removes the spills but measured 9% slower: the any_sync loop costs more)
         e.pfn = (const void*)&persistent_kernel<P, R>;

@@ -89,11 +89,12 @@ __device__ __forceinline__ R seq_sum(const Group<L>& G, const R (&terms)[C], R i
 // i outer, j inner; action/reaction share one distance evaluation.
 struct Pleiades {
     static constexpr int N = 28, P = 0;
+    static constexpr bool second_order = true;  // out[0..14) = w[14..28) (problems.cpp:17)
     static constexpr const char* name = "pleiades";
     // Accelerations a(q) for positions q = (x_1..x_7, y_1..y_7): the out[14..27]
     // half of the reference RHS, accumulated in the reference's order.
     template <class R>
-    __device__ __forceinline__ static void accel(const R* w, R* a) {
+    __device__ __forceinline__ static void accel(R, const R* w, const R*, R* a) {
         // EXACT: 1/(r2 sqrt(r2)) for all pairs first, straight-line (arith.cuh
         // sqrt_rn_bf / rcp_rn_bf), with one cold fallback to the intrinsics
         double inv[21];
@@ -157,7 +158,28 @@ struct Pleiades {
         static_assert(L == 1, "Pleiades couples all components: one lane per system");
 #pragma unroll
         for (int i = 0; i < 14; ++i) out[i] = w[14 + i];
-        accel<R>(w, out + 14);
+        accel<R>(R(0.0), w, nullptr, out + 14);
+    }
+};
+
+// Second-order systems y = (q, v), q' = v, v' = a(t, q; g): derive from this
+// with the problem struct itself as D and M = dim(q), and provide
+//   template <class R> __device__ static void accel(R t, const R* q, const R* g, R* a);
+// RKCK then runs the Nystrom kernels (rkck_nystrom.cuh: the reference's step
+// on velocity-copy storage under EXACT, the Runge-Kutta-Nystrom form under
+// FAST); RKC and the fixed-step harnesses use the rhs() below, which is the
+// reference-style full right-hand side (velocities first, then a).
+template <class D, int M_, int P_ = 0>
+struct SecondOrderProblem {
+    static constexpr int N = 2 * M_, P = P_;
+    static constexpr bool second_order = true;
+    template <class R, int L>
+    __device__ __forceinline__ static void rhs(const Group<L>&, R t, const R (&w)[N / L],
+                                               const R* g, R (&out)[N / L]) {
+        static_assert(L == 1, "second-order problems run one lane per system");
+#pragma unroll
+        for (int i = 0; i < M_; ++i) out[i] = w[M_ + i];
+        D::template accel<R>(t, w, g, out + M_);
     }
 };
 

@@ -26,14 +26,22 @@
 
 namespace bode {
 
-template <class P>
+// Problems that declare `static constexpr bool second_order = true` and an
+// accel(t, q, g, a) (problems.cuh SecondOrderProblem) take the Nystrom kernels.
+template <class P, class = void>
 struct is_second_order {
     static constexpr bool value = false;
 };
-template <>
-struct is_second_order<Pleiades> {
-    static constexpr bool value = true;
+template <class P>
+struct is_second_order<P, decltype((void)P::second_order)> {
+    static constexpr bool value = P::second_order;
 };
+template <class P>
+constexpr bool is_pleiades = false;
+template <>
+constexpr bool is_pleiades<Pleiades> = true;
+// stage nodes a3..a6 (rkck.cpp:9), for the rolled stage loop
+__constant__ double c_ck_a[4] = {3.0 / 10.0, 3.0 / 5.0, 1.0, 7.0 / 8.0};
 
 #define BODE_FENCE() asm volatile("" ::: "memory")
 
@@ -98,8 +106,12 @@ struct NystromRkck {
     R t, tEnd, hMax, h;
     bool haveF, live;
     DevStats st;
-    double* ks;  // this lane's shared-memory row (k2..k5 / k6)
+    double* ks;         // this lane's shared-memory row (k2..k5 / k6)
+    const R* gp = nullptr;  // the system's parameters (problems with P > 0)
 
+    __device__ __forceinline__ const double* gpd() const {  // params as doubles (FAST form)
+        return reinterpret_cast<const double*>(gp);
+    }
     __device__ __forceinline__ R kget(int m, int c) const { return R(ks[m * P::N + c]); }
     __device__ __forceinline__ void kset(int m, int c, R v) { ks[m * P::N + c] = val(v); }
 
@@ -130,7 +142,7 @@ struct NystromRkck {
         const R uround(tol.uround), eps(tol.eps), tiny(tol.tiny);
         h = fmin_(tEnd - t, h);
         if (UNIFORM_F0 || !haveF) {  // rejected retries reuse f(t, y) (rkck.cpp:133-137)
-            P::template accel<R>(q, A0);
+            P::template accel<R>(t, q, gp, A0);
             if (!haveF) ++st.rhs_evals;
             haveF = true;
         }
@@ -146,7 +158,7 @@ struct NystromRkck {
 #pragma unroll
             for (int i = 0; i < M; ++i) Q[i] = q[i] + hb * v[i];
             BODE_FENCE();
-            P::template accel<R>(Q, Acc);
+            P::template accel<R>(t + R(a2) * h, Q, gp, Acc);
 #pragma unroll
             for (int i = 0; i < M; ++i) kset(0, M + i, Acc[i]);
             BODE_FENCE();
@@ -220,7 +232,7 @@ struct NystromRkck {
 #pragma unroll
             for (int i = 0; i < M; ++i) kset(out, i, Acc[i]);
             BODE_FENCE();
-            P::template accel<R>(Q, Acc);
+            P::template accel<R>(t + R(c_ck_a[j - 3]) * h, Q, gp, Acc);
             // FAST reads A6 from registers (finish_attempt), so its slot is never stored
             if (is_exact<R>::value || j != 6) {
 #pragma unroll
@@ -243,7 +255,7 @@ struct NystromRkck {
             const double ha = hh * a2;  // Q_2 = q + h b21 v (b21 = a2)
 #pragma unroll
             for (int i = 0; i < M; ++i) Q[i] = fma(ha, v[i], q[i]);
-            P::template accel<double>(Q, Acc);
+            P::template accel<double>(val(t) + ha, Q, gpd(), Acc);
         }
         // stages 3..6: store the newest acceleration A_{j-1} (slot j-3), then
         // form Q_j from A_1..A_{j-2}
@@ -264,7 +276,7 @@ struct NystromRkck {
                     if (l <= j - 3) s = fma(hb[l], ks[(l - 1) * M + i], s);
                 Q[i] = s;
             }
-            P::template accel<double>(Q, Acc);
+            P::template accel<double>(val(t) + ha, Q, gpd(), Acc);
         }
         st.rhs_evals += 5;
         st.stages_total += 6;
@@ -472,9 +484,10 @@ struct NystromRkck {
 
 template <class P, class R>
 __device__ __forceinline__ void rkck_nystrom_system(double t_in, double tEnd_in,
-                                                    R (&y)[P::N], const DevTol& tol,
+                                                    R (&y)[P::N], const R* g, const DevTol& tol,
                                                     DevStats& st) {
     NystromRkck<P, R> s;
+    s.gp = g;
 #pragma unroll
     for (int c = 0; c < P::N; ++c) s.y[c] = y[c];
     s.start(t_in, tEnd_in, tol);

@@ -97,3 +97,46 @@ def test_out_of_tree_problem_fast(user_lib, ref):
     rc, yo, so, _ = ref.outer_loop_fn(rhs, 40, 1, A.SOLVER_RKCK, 0.0, 0.5, 0.1, y0, g)
     # chaotic flow: FMA-level differences grow, but stay far inside 1e-3 * eps
     assert sysrel(y, yo, num, 40).max() <= 1e-13
+
+
+NBODY = A.USER_BASE + 97
+
+
+def _nbody_inputs(num):
+    nb = 5
+    ang = 2 * np.pi * np.arange(nb) / nb
+    pos = np.stack([1.5 * np.cos(ang), 1.5 * np.sin(ang), 0.2 * np.sin(2 * ang)], axis=1).reshape(-1)
+    vel = np.stack([-0.9 * np.sin(ang), 0.9 * np.cos(ang), 0.05 * np.cos(ang)], axis=1).reshape(-1)
+    y0 = perturb(np.concatenate([pos, vel]), 0.01, 13, num)
+    m = 1.0 + 0.5 * np.sin(np.arange(num * nb) * 0.37).reshape(nb, num)  # SoA masses
+    return y0, m.reshape(-1)
+
+
+@pytest.mark.parametrize("solver", [A.SOLVER_RKCK, A.SOLVER_RKC])
+def test_second_order_user_problem_exact_bitwise(user_lib, ref, solver):
+    """An out-of-tree second-order problem (bode::SecondOrderProblem): RKCK runs
+    the Nystrom kernel, RKC the generic one; both bitwise the reference drivers."""
+    num = 512
+    prob = A.Problem(kind=NBODY, dim=30, param_dim=5, reserved=0)
+    y0, m = _nbody_inputs(num)
+    y, st = run(prob, solver, y0, m, "exact", t1=0.5)
+    rhs = ctypes.cast(user_lib.bode_example_nbody_rhs, ctypes.c_void_p).value
+    rc, yo, so, _ = ref.outer_loop_fn(rhs, 30, 5, solver, 0.0, 0.5, 0.1, y0, m)
+    assert rc == 0
+    assert np.array_equal(y.view(np.uint64), yo.view(np.uint64))
+    for k in COUNTS:
+        assert np.array_equal(st[k], so[k]), k
+
+
+def test_second_order_user_problem_fast_rkn(user_lib, ref):
+    """FAST RKCK on it runs in Runge-Kutta-Nystrom form: within 1e-3 * eps of
+    the reference with identical step counts."""
+    num = 512
+    prob = A.Problem(kind=NBODY, dim=30, param_dim=5, reserved=0)
+    y0, m = _nbody_inputs(num)
+    y, st = run(prob, A.SOLVER_RKCK, y0, m, "fast", t1=0.5)
+    rhs = ctypes.cast(user_lib.bode_example_nbody_rhs, ctypes.c_void_p).value
+    rc, yo, so, _ = ref.outer_loop_fn(rhs, 30, 5, A.SOLVER_RKCK, 0.0, 0.5, 0.1, y0, m)
+    assert sysrel(y, yo, num, 30).max() <= 1e-13
+    for k in ("steps_accepted", "steps_rejected", "rhs_evals"):
+        assert np.array_equal(st[k], so[k]), k
