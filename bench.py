@@ -404,6 +404,29 @@ def main():
         e2e = {"value": world * num * args.steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": num * 28 * 8, "d2h_bytes_per_step": num * (28 * 8 + 64),
                "ms_per_step": e2e_s / args.steps * 1e3, "pinned_host": True}
+        # the same 10-window protocol through bode_outer_loop (batchode::outerLoop's
+        # drop-in): host buffers in and out, the state resident in HBM between
+        # windows, so one H2D and one D2H per call instead of per window
+        steps_out = ctypes.c_int32(0)
+        P.api.check(L.bode_outer_loop(ctypes.byref(prob), 0, ar, 0.0, 0.2, 0.1, num, None, yp,
+                                      ctypes.byref(tol), ctypes.c_void_p(sth.data_ptr()), 1,
+                                      P.api.SINK(), None, ctypes.byref(steps_out)))  # warm-up
+        yh.copy_(torch.from_numpy(y0))
+        if dist:
+            dist.barrier()
+        t = time.perf_counter()
+        P.api.check(L.bode_outer_loop(ctypes.byref(prob), 0, ar, 0.0, 1.0, 0.1, num, None, yp,
+                                      ctypes.byref(tol), ctypes.c_void_p(sth.data_ptr()), 1,
+                                      P.api.SINK(), None, ctypes.byref(steps_out)))
+        ol_s = time.perf_counter() - t
+        if dist:
+            tt = torch.tensor([ol_s], device=red_dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ol_s = float(tt.item())
+        e2e["outer_loop"] = {"value": world * num * steps_out.value / ol_s, "unit": UNIT,
+                             "windows": steps_out.value, "ms_total": ol_s * 1e3,
+                             "h2d_bytes_per_call": num * 28 * 8,
+                             "d2h_bytes_per_call": num * (28 * 8 + 64)}
 
     def secondary(problem, solver, arith, dim, y0s, g0s, label, steps, repack=False):
         sec, perw, sts, _, _ = measure_device(P, A, torch, problem, solver, arith, dim, y0s, g0s,

@@ -13,6 +13,8 @@ struct DevTol {  // bode_tol_t, by value in the kernel parameters
     const double* powtab;    // host-libm pow tables on this device (arith.cuh), or null
     const double* rkc_coef;  // RKC coefficient table for this kappa/policy (rkc.cuh), or null
     int refill_min;          // persistent kernels: idle lanes that trigger a refill round
+    long long stride;        // SoA row stride of y and g in doubles (0: the launch's num),
+                             // so a launch can cover a column range of a larger batch
 };
 
 struct DevStats {  // bode_stats_t, per system (AoS, 64 bytes)

@@ -79,6 +79,7 @@ DevTol to_dev(const bode_tol_t* t) {
         return v < 1 ? 1 : v > 32 ? 32 : v;
     }();
     d.refill_min = refill_min;
+    d.stride = 0;
     return d;
 }
 
@@ -287,8 +288,9 @@ int block_for(const KernelEntry* e) {
 // Launch one window over `num` systems resident on the current device.
 int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double* y,
                   DevStats* st, long long num, double t, double tEnd, const DevTol& tol_in,
-                  int merge) {
+                  int merge, long long stride = 0) {
     DevTol tol = tol_in;
+    tol.stride = stride;
     tol.powtab = bode::device_powtab();
     tol.rkc_coef = nullptr;
     if (e->build_rkc_table != nullptr) {
@@ -731,7 +733,12 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
     const int N = p->dim, P = p->param_dim;
     const int64_t nwin = bode_num_windows(t0, t_end, h_outer);
 
-    // upload each shard once; y stays resident across windows
+    // Buffers per shard; y stays resident across windows.
+    // With pinned host memory the first window's upload and the last window's
+    // download are pipelined with its kernels in column chunks of the shard's
+    // SoA arrays (launches with a row stride): H2D on streams[0], kernels on
+    // streams[1], D2H on streams[2], chained by per-chunk events.
+    const bool pinned = host_pinned(y);
     rc = for_each_shard(shards, [&](const Shard& sh) {
         BODE_CUDA(cudaSetDevice(sh.device));
         DeviceBuffers& B = g_dev[sh.device];
@@ -741,17 +748,11 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
         if (P > 0 && (r = ensure(&B.g, &B.g_cap, (size_t)sh.count * P))) return r;
         if ((r = ensure(&B.st, &B.st_cap, (size_t)sh.count))) return r;
         if ((r = ensure(&B.ord, &B.ord_cap, (size_t)sh.count))) return r;
-        if (!B.streams[0]) BODE_CUDA(cudaStreamCreateWithFlags(&B.streams[0], cudaStreamNonBlocking));
-        cudaStream_t s = B.streams[0];
-        if ((r = bode::init_order(B.ord, sh.count, s))) return fail(r, "order init failed");
-        BODE_CUDA(cudaMemcpy2DAsync(B.y, sh.count * sizeof(double), y + sh.begin,
-                                    num * sizeof(double), sh.count * sizeof(double), N,
-                                    cudaMemcpyHostToDevice, s));
-        if (P > 0)
-            BODE_CUDA(cudaMemcpy2DAsync(B.g, sh.count * sizeof(double), g + sh.begin,
-                                        num * sizeof(double), sh.count * sizeof(double), P,
-                                        cudaMemcpyHostToDevice, s));
-        BODE_CUDA(cudaStreamSynchronize(s));
+        for (auto& st : B.streams)
+            if (!st) BODE_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        for (auto& ev : B.events)
+            if (!ev) BODE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        if ((r = bode::init_order(B.ord, sh.count, B.streams[1]))) return fail(r, "order init failed");
         return BODE_OK;
     });
     if (rc) return rc;
@@ -766,44 +767,100 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
             BODE_CUDA(cudaSetDevice(sh.device));
             DeviceBuffers& B = g_dev[sh.device];
             std::lock_guard<std::mutex> lock(B.m);
-            cudaStream_t s = B.streams[0];
+            cudaStream_t sh2d = B.streams[0], s = B.streams[1], sd2h = B.streams[2];
             const size_t si = &sh - shards.data();
-            int r = launch_window(e, s, P > 0 ? B.g : nullptr, B.y, B.st, sh.count, t, tk, dt,
-                                  k > 1 ? 1 : 0);
-            if (r) return r;
-            if (k == nwin && repacked[si]) {  // back to the caller's order, in place
-                if ((r = bode::unpack(N, P, sh.count, B.y, P > 0 ? B.g : nullptr, B.st, B.ord,
+            const long long cnt = sh.count;
+            const bool first = k == 1, last = k == nwin;
+            const int nch = pinned ? (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, cnt / (1 << 16)))
+                                   : 1;
+            // the final download can ride along per chunk unless the batch is re-packed
+            const bool chunked_out = last && !repacked[si] && nch > 1;
+            const bool chunked = (first && nch > 1) || chunked_out;
+            int r = BODE_OK;
+            if (first && !chunked) {  // upload in one piece
+                BODE_CUDA(cudaMemcpy2DAsync(B.y, cnt * sizeof(double), y + sh.begin,
+                                            num * sizeof(double), cnt * sizeof(double), N,
+                                            cudaMemcpyHostToDevice, s));
+                if (P > 0)
+                    BODE_CUDA(cudaMemcpy2DAsync(B.g, cnt * sizeof(double), g + sh.begin,
+                                                num * sizeof(double), cnt * sizeof(double), P,
+                                                cudaMemcpyHostToDevice, s));
+            }
+            if (chunked) {
+                const long long cb = cnt / nch, crem = cnt % nch;
+                long long off = 0;
+                for (int c = 0; c < nch; ++c) {
+                    const long long nk = cb + (c < crem ? 1 : 0);
+                    cudaEvent_t in_done = B.events[2 * c], k_done = B.events[2 * c + 1];
+                    if (first) {
+                        BODE_CUDA(cudaMemcpy2DAsync(B.y + off, cnt * sizeof(double),
+                                                    y + sh.begin + off, num * sizeof(double),
+                                                    nk * sizeof(double), N,
+                                                    cudaMemcpyHostToDevice, sh2d));
+                        if (P > 0)
+                            BODE_CUDA(cudaMemcpy2DAsync(B.g + off, cnt * sizeof(double),
+                                                        g + sh.begin + off, num * sizeof(double),
+                                                        nk * sizeof(double), P,
+                                                        cudaMemcpyHostToDevice, sh2d));
+                        BODE_CUDA(cudaEventRecord(in_done, sh2d));
+                        BODE_CUDA(cudaStreamWaitEvent(s, in_done, 0));
+                    }
+                    r = launch_window(e, s, P > 0 ? B.g + off : nullptr, B.y + off, B.st + off,
+                                      nk, t, tk, dt, first ? 0 : 1, cnt);
+                    if (r) return r;
+                    if (chunked_out) {
+                        BODE_CUDA(cudaEventRecord(k_done, s));
+                        BODE_CUDA(cudaStreamWaitEvent(sd2h, k_done, 0));
+                        BODE_CUDA(cudaMemcpy2DAsync(y + sh.begin + off, num * sizeof(double),
+                                                    B.y + off, cnt * sizeof(double),
+                                                    nk * sizeof(double), N,
+                                                    cudaMemcpyDeviceToHost, sd2h));
+                        if (stats)
+                            BODE_CUDA(cudaMemcpyAsync(stats + sh.begin + off, B.st + off,
+                                                      nk * sizeof(DevStats),
+                                                      cudaMemcpyDeviceToHost, sd2h));
+                    }
+                    off += nk;
+                }
+            } else {
+                r = launch_window(e, s, P > 0 ? B.g : nullptr, B.y, B.st, cnt, t, tk, dt,
+                                  first ? 0 : 1);
+                if (r) return r;
+            }
+            if (last && repacked[si]) {  // back to the caller's order, in place
+                if ((r = bode::unpack(N, P, cnt, B.y, P > 0 ? B.g : nullptr, B.st, B.ord,
                                       nullptr, s)))
                     return fail(r, "unpack failed");
                 repacked[si] = 0;
             }
-            const double* ysrc = B.y;
-            if (snap && repacked[si]) {  // snapshot in the caller's order
-                if ((r = ensure(&B.ysnap, &B.ysnap_cap, (size_t)sh.count * N))) return r;
-                if ((r = bode::unpack(N, P, sh.count, B.y, nullptr, nullptr, B.ord, B.ysnap, s)))
-                    return fail(r, "snapshot unpack failed");
-                ysrc = B.ysnap;
-            }
-            if (snap)
+            if (snap && !chunked_out) {
+                const double* ysrc = B.y;
+                if (repacked[si]) {  // snapshot in the caller's order
+                    if ((r = ensure(&B.ysnap, &B.ysnap_cap, (size_t)cnt * N))) return r;
+                    if ((r = bode::unpack(N, P, cnt, B.y, nullptr, nullptr, B.ord, B.ysnap, s)))
+                        return fail(r, "snapshot unpack failed");
+                    ysrc = B.ysnap;
+                }
                 BODE_CUDA(cudaMemcpy2DAsync(y + sh.begin, num * sizeof(double), ysrc,
-                                            sh.count * sizeof(double), sh.count * sizeof(double),
-                                            N, cudaMemcpyDeviceToHost, s));
-            if (k < nwin && threshold > 0.0 && sh.count >= 1024) {
+                                            cnt * sizeof(double), cnt * sizeof(double), N,
+                                            cudaMemcpyDeviceToHost, s));
+                if (last && stats)
+                    BODE_CUDA(cudaMemcpyAsync(stats + sh.begin, B.st, cnt * sizeof(DevStats),
+                                              cudaMemcpyDeviceToHost, s));
+            }
+            if (!last && threshold > 0.0 && cnt >= 1024) {
                 // re-pack when the cost history says warps idle behind stragglers
                 double eff = 1.0;
-                if ((r = bode::lockstep_efficiency(B.st, sh.count, 32 / e->lanes, &eff, s)))
+                if ((r = bode::lockstep_efficiency(B.st, cnt, 32 / e->lanes, &eff, s)))
                     return fail(r, "lockstep efficiency failed");
                 if (eff < threshold) {
-                    if ((r = bode::repack_by_cost(N, P, sh.count, B.y, P > 0 ? B.g : nullptr,
-                                                  B.st, B.ord, s)))
+                    if ((r = bode::repack_by_cost(N, P, cnt, B.y, P > 0 ? B.g : nullptr, B.st,
+                                                  B.ord, s)))
                         return fail(r, "repack failed");
                     repacked[si] = 1;
                 }
             }
-            if (k == nwin && stats)
-                BODE_CUDA(cudaMemcpyAsync(stats + sh.begin, B.st, sh.count * sizeof(DevStats),
-                                          cudaMemcpyDeviceToHost, s));
-            BODE_CUDA(cudaStreamSynchronize(s));
+            for (auto& st : B.streams) BODE_CUDA(cudaStreamSynchronize(st));
             return BODE_OK;
         });
         if (rc) return rc;

@@ -43,13 +43,14 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
     const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long sys = gt / L;
     if (sys >= num) return;  // whole lane groups retire together
+    const long long ld = tol.stride > 0 ? tol.stride : num;  // SoA row stride
     Group<L> G;
     R y[C];
     R g[PP];
 #pragma unroll
-    for (int c = 0; c < C; ++c) y[c] = R(y_soa[sys + num * (long long)comp_index<P, L>(G.lane, c)]);
+    for (int c = 0; c < C; ++c) y[c] = R(y_soa[sys + ld * (long long)comp_index<P, L>(G.lane, c)]);
 #pragma unroll
-    for (int p = 0; p < PP; ++p) g[p] = R(P::P > 0 ? g_soa[sys + num * (long long)p] : 0.0);
+    for (int p = 0; p < PP; ++p) g[p] = R(P::P > 0 ? g_soa[sys + ld * (long long)p] : 0.0);
     DevStats st;
     if constexpr (SOLVER == 0 && is_pleiades<P> && L == 2)
         rkck_pleiades2_system<R>(G, t, tEnd, y, tol, st);
@@ -60,7 +61,7 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
     else
         rkc_system<P, R, L>(G, t, tEnd, y, g, tol, st);
 #pragma unroll
-    for (int c = 0; c < C; ++c) y_soa[sys + num * (long long)comp_index<P, L>(G.lane, c)] = val(y[c]);
+    for (int c = 0; c < C; ++c) y_soa[sys + ld * (long long)comp_index<P, L>(G.lane, c)] = val(y[c]);
     if (stats != nullptr && G.lane == 0) {
         if (merge) {
             DevStats o = stats[sys];

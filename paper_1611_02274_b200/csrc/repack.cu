@@ -97,22 +97,30 @@ __global__ void identity_order(long long* __restrict__ ord, long long num) {
     if (p < num) ord[p] = p;
 }
 
-// sums of per-group mean and max cost over groups of `group` consecutive systems
+// sum over systems of cost, and of the cost of each system's warp group's
+// slowest member (groups of `group` consecutive systems, group | 32): one
+// thread per system, shuffle reductions, one atomic pair per warp
 __global__ void lockstep_sums(const DevStats* __restrict__ st, long long num, int group,
                               unsigned long long* __restrict__ sums) {
-    const long long gidx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long b = gidx * group;
-    if (b >= num) return;
-    unsigned long long s = 0, m = 0;
-    for (int k = 0; k < group && b + k < num; ++k) {
-        const long long c = st[b + k].rhs_evals;
-        const unsigned long long u = c > 0 ? (unsigned long long)c : 0ull;
-        s += u;
-        m = u > m ? u : m;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = i < num;
+    const long long c0 = valid ? st[i].rhs_evals : 0;
+    const unsigned long long c = c0 > 0 ? (unsigned long long)c0 : 0ull;
+    unsigned long long m = c;
+    for (int o = group / 2; o > 0; o /= 2) {
+        const unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+        m = t > m ? t : m;
     }
-    const int n = (int)((num - b) < group ? (num - b) : group);
-    atomicAdd(&sums[0], s);
-    atomicAdd(&sums[1], m * (unsigned long long)n);
+    unsigned long long s = c, w = valid ? m : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o /= 2) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        w += __shfl_xor_sync(0xffffffffu, w, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&sums[0], s);
+        atomicAdd(&sums[1], w);
+    }
 }
 
 inline unsigned blocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -232,16 +240,23 @@ int init_order(long long* order, long long num, cudaStream_t s) {
 // sum(cost) / sum(group max * group size). Synchronises the stream.
 int lockstep_efficiency(const DevStats* st, long long num, int group, double* eff,
                         cudaStream_t s) {
-    unsigned long long* d = nullptr;
-    RP_CUDA(cudaMallocAsync(&d, 2 * sizeof(unsigned long long), s));
-    RP_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), s));
-    const long long groups = (num + group - 1) / group;
-    lockstep_sums<<<blocks(groups, 256), 256, 0, s>>>(st, num, group, d);
-    unsigned long long h[2] = {0, 0};
-    RP_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, s));
-    RP_CUDA(cudaFreeAsync(d, s));
+    // per-device device/pinned-host counter pair, allocated once
+    static std::mutex m;
+    static unsigned long long* dsum[64] = {nullptr};
+    static unsigned long long* hsum[64] = {nullptr};
+    int dev = 0;
+    RP_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(m);
+    if (dsum[dev] == nullptr) {
+        RP_CUDA(cudaMalloc(&dsum[dev], 2 * sizeof(unsigned long long)));
+        RP_CUDA(cudaMallocHost(&hsum[dev], 2 * sizeof(unsigned long long)));
+    }
+    RP_CUDA(cudaMemsetAsync(dsum[dev], 0, 2 * sizeof(unsigned long long), s));
+    lockstep_sums<<<blocks(num, 256), 256, 0, s>>>(st, num, group, dsum[dev]);
+    RP_CUDA(cudaMemcpyAsync(hsum[dev], dsum[dev], 2 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s));
     RP_CUDA(cudaStreamSynchronize(s));
-    *eff = h[1] ? (double)h[0] / (double)h[1] : 1.0;
+    *eff = hsum[dev][1] ? (double)hsum[dev][0] / (double)hsum[dev][1] : 1.0;
     return BODE_OK;
 }
 

@@ -513,6 +513,7 @@ __device__ __forceinline__ void rkck_nystrom_persistent(const double* __restrict
                                                         unsigned long long* counter,
                                                         int refill_min) {
     constexpr unsigned kFull = 0xffffffffu;
+    const long long ld = tol.stride > 0 ? tol.stride : num;  // SoA row stride
     const unsigned lane = threadIdx.x & 31u;
     const unsigned lt_mask = (1u << lane) - 1u;
     NystromRkck<P, R> s;
@@ -523,14 +524,14 @@ __device__ __forceinline__ void rkck_nystrom_persistent(const double* __restrict
         sys = (long long)blockIdx.x * blockDim.x + threadIdx.x;
         if (sys < num) {
 #pragma unroll
-            for (int c = 0; c < P::N; ++c) s.y[c] = R(y_soa[sys + num * (long long)c]);
+            for (int c = 0; c < P::N; ++c) s.y[c] = R(y_soa[sys + ld * (long long)c]);
             s.start(t_in, tEnd_in, tol);
             has = true;
         }
     }
     auto retire = [&]() {  // store a finished (or frozen) system and free the lane
 #pragma unroll
-        for (int c = 0; c < P::N; ++c) y_soa[sys + num * (long long)c] = val(s.y[c]);
+        for (int c = 0; c < P::N; ++c) y_soa[sys + ld * (long long)c] = val(s.y[c]);
         if (stats != nullptr) {
             if (merge) {
                 DevStats o = stats[sys];
@@ -559,7 +560,7 @@ __device__ __forceinline__ void rkck_nystrom_persistent(const double* __restrict
                     if (mine < (unsigned long long)num) {
                         sys = (long long)mine;
 #pragma unroll
-                        for (int c = 0; c < P::N; ++c) s.y[c] = R(y_soa[sys + num * (long long)c]);
+                        for (int c = 0; c < P::N; ++c) s.y[c] = R(y_soa[sys + ld * (long long)c]);
                         s.start(t_in, tEnd_in, tol);
                         has = true;
                         if (!s.live) retire();  // empty interval: nothing to integrate

@@ -327,3 +327,32 @@ def test_heat64_lane_variants_bitwise(gpu, oracle, env):
     y0 = perturb(heat_ic(64), 0.01, 42, 2048)
     rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKC, 0.0, 1.0, 0.1, y0)
     assert np.array_equal(np.load(out).view(np.uint64), yo.view(np.uint64))
+
+
+@pytest.mark.parametrize("nwin_end", [0.1, 1.0])
+def test_outer_loop_pinned_chunked_pipeline(gpu, nwin_end):
+    """With pinned host buffers bode_outer_loop pipelines the first window's
+    upload and the last window's download in column chunks (strided launches);
+    the results equal the pageable (single-piece) path bit for bit."""
+    import ctypes
+    import torch
+    L = B.lib()
+    num = 1 << 18
+    prob = A.make_problem(A.PLEIADES)
+    y0 = perturb(PLEIADES_IC, 0.01, 42, num)
+    tol = A.default_tol()
+    outs = {}
+    for pinned in (False, True):
+        yh = torch.from_numpy(y0.copy())
+        sth = torch.zeros(num * 8, dtype=torch.int64)
+        if pinned:
+            yh, sth = yh.pin_memory(), sth.pin_memory()
+        n = ctypes.c_int32(0)
+        B.api.check(L.bode_outer_loop(ctypes.byref(prob), A.SOLVER_RKCK, A.ARITH_FAST, 0.0,
+                                      nwin_end, 0.1, num, None,
+                                      ctypes.cast(yh.data_ptr(), ctypes.POINTER(ctypes.c_double)),
+                                      ctypes.byref(tol), ctypes.c_void_p(sth.data_ptr()), 1,
+                                      B.api.SINK(), None, ctypes.byref(n)))
+        outs[pinned] = (yh.numpy().copy(), sth.numpy().copy())
+    assert np.array_equal(outs[False][0].view(np.uint64), outs[True][0].view(np.uint64))
+    assert np.array_equal(outs[False][1], outs[True][1])
