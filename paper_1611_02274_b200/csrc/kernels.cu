@@ -15,6 +15,7 @@ const KernelEntry* kernel_table(int* count) {
         // IEEE sqrt/reciprocal need more registers than one lane can spare
         // (FAST caps measured: 255 -> 5.59e8, 200 -> 4.99e8, 168 -> 4.07e8 system-windows/s)
         make_entry<Pleiades, double, 1, 0, true, 0>(0, 1),
+        // (EXACT caps measured: 168 -> 1.91e8, 200 -> 1.88e8, 128 -> 1.79e8 system-windows/s)
         make_entry<Pleiades, xd, 2, 0, true, 168>(0, 0),
         make_entry<Pleiades, double, 2, 0, true, 168>(0, 1),
         make_entry<Pleiades, xd, 1, 0, true, 0>(0, 0),

@@ -90,6 +90,9 @@ for p in $PARTS; do
       for V in "4 255" "4 128" "8 255" "8 128" "16 128"; do set -- $V
         BODE_LANES=$1 BODE_MAXREG=$2 timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 65536 --rkc-systems 1048576 > $OUT/bench_bru_L$1_R$2.txt 2>&1; done
       echo "ab_bru rc=$?" >> $OUT/status.txt ;;
+    ab_exactreg)
+      for R in 168 128 200; do BODE_MAXREG=$R timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/bench_exactreg$R.txt 2>&1; done
+      echo "ab_exactreg rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
