@@ -44,6 +44,9 @@ def main():
     s = torch.cuda.current_stream()
     tot = {"static": 0.0, "sorted_by_prev": 0.0}
     cum = np.zeros(num, np.int64)
+    # adaptive policy: re-pack (sort by cumulative cost) after a window whose
+    # cumulative-cost lockstep efficiency in the current order is below thr
+    pol = {thr: {"order": np.arange(num), "cost": 0.0, "repacks": 0} for thr in (0.9, 0.95, 0.97)}
     for k in range(10):
         P.int_driver_device(prob, "rkck", "fast", 0.1 * k, 1.0 if k == 9 else 0.1 * (k + 1), num, 0,
                             y.data_ptr(), tol, st.data_ptr(), False, s.cuda_stream)
@@ -59,7 +62,16 @@ def main():
         sp = a[order].reshape(-1, 32).max(axis=1).sum()
         row["sorted_by_prev"] = int(sp) * 32
         tot["sorted_by_prev"] += sp
+        for thr, st_ in pol.items():
+            st_["cost"] += a[st_["order"]].reshape(-1, 32).max(axis=1).sum()
         cum += a
+        for thr, st_ in pol.items():
+            cw = cum[st_["order"]].reshape(-1, 32)
+            eff = cw.sum() / (cw.max(axis=1).sum() * 32)
+            row[f"cum_eff_{thr}"] = float(eff)
+            if k < 9 and eff < thr:
+                st_["order"] = np.argsort(cum, kind="stable")
+                st_["repacks"] += 1
         for T in (4, 8, 16, 24):
             c, n2 = two_pass(a, T)
             row[f"T{T}"] = int(c) * 32
@@ -70,6 +82,9 @@ def main():
     # total attempts, instead of the sum over windows of per-window maxima
     fused = cum.reshape(-1, 32).max(axis=1).sum()
     tot["fused_windows"] = float(fused)
+    for thr, st_ in pol.items():
+        tot[f"adaptive_{thr}"] = st_["cost"]
+        tot[f"adaptive_{thr}_repacks"] = st_["repacks"] * tot["static"]
     print(json.dumps({k: v / tot["static"] for k, v in tot.items()}))
 
 
