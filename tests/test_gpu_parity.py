@@ -356,3 +356,21 @@ def test_outer_loop_pinned_chunked_pipeline(gpu, nwin_end):
         outs[pinned] = (yh.numpy().copy(), sth.numpy().copy())
     assert np.array_equal(outs[False][0].view(np.uint64), outs[True][0].view(np.uint64))
     assert np.array_equal(outs[False][1], outs[True][1])
+
+
+@pytest.mark.parametrize("num", [1, 3, 33, 1001])
+def test_ragged_batch_sizes_bitwise(gpu, oracle, num):
+    """Batches that fill neither a warp nor a lane group evenly (1, 3, 33, 1001
+    systems) on every default kernel shape: Pleiades RKCK (lane pair, EXACT),
+    heat64 RKC (8 lanes per system), expDecay RKC (1 lane): bitwise the oracle."""
+    cases = [(A.make_problem(A.PLEIADES), A.SOLVER_RKCK, PLEIADES_IC, None),
+             (A.make_problem(A.HEAT, 64), A.SOLVER_RKC, heat_ic(64), None),
+             (A.make_problem(A.EXPDECAY), A.SOLVER_RKC, np.array([1.0]),
+              np.linspace(1.0, 1e3, num))]
+    for prob, solver, base, g in cases:
+        y0 = perturb(base, 0.01, 17, num)
+        y, st = run_gpu(prob, solver, y0, g, "exact")
+        rc, yo, so, _ = oracle.outer_loop(prob, solver, 0.0, 1.0, 0.1, y0, g)
+        assert np.array_equal(y.view(np.uint64), yo.view(np.uint64)), (prob.kind, num)
+        for k in COUNTS:
+            assert np.array_equal(st[k], so[k]), (prob.kind, num, k)
