@@ -374,17 +374,35 @@ struct Shard {
     int64_t begin, count;
 };
 
+// Contiguous shards (batch_driver.cpp:68-73) over `gpus` devices starting at
+// the calling thread's current device, so a one-process-per-GPU caller (torchrun
+// rank r with cuda:r current) and num_gpus = 1 stays on its own GPU.
 std::vector<Shard> make_shards(int64_t num, int gpus) {
     std::vector<Shard> v;
+    int cur = 0, n = 1;
+    if (cudaGetDevice(&cur) != cudaSuccess) cur = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) n = 1;
     const int64_t base = num / gpus, rem = num % gpus;
     int64_t b = 0;
     for (int d = 0; d < gpus; ++d) {
         const int64_t len = base + (d < rem ? 1 : 0);
-        if (len > 0) v.push_back({d, b, len});
+        if (len > 0) v.push_back({(cur + d) % n, b, len});
         b += len;
     }
     return v;
 }
+
+// Restores the calling thread's current device when a host entry point
+// returns (the shard loop switches devices).
+struct DeviceRestore {
+    int dev = -1;
+    DeviceRestore() {
+        if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+    }
+    ~DeviceRestore() {
+        if (dev >= 0) cudaSetDevice(dev);
+    }
+};
 
 int check_devices(int gpus) {
     int n = 0;
@@ -712,6 +730,7 @@ int bode_int_driver(const bode_problem_t* p, int32_t solver, int32_t arith, doub
     if (rc) return rc;
     if ((rc = check_devices(num_gpus))) return rc;
     const DevTol dt = to_dev(tol);
+    DeviceRestore restore;
     const auto shards = make_shards(num, num_gpus);
     return for_each_shard(shards, [&](const Shard& sh) {
         return run_shard_window(e, p, sh, num, g, y, stats, t, t_end, dt);
@@ -729,6 +748,7 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
     if (rc) return rc;
     if ((rc = check_devices(num_gpus))) return rc;
     const DevTol dt = to_dev(tol);
+    DeviceRestore restore;
     const auto shards = make_shards(num, num_gpus);
     const int N = p->dim, P = p->param_dim;
     const int64_t nwin = bode_num_windows(t0, t_end, h_outer);
@@ -897,7 +917,8 @@ int bode_integrate_fixed(const bode_problem_t* p, int32_t solver, int32_t arith,
     if (e->launch_fixed == nullptr)
         return fail(BODE_E_UNSUPPORTED, "no fixed-step kernel for this problem/solver");
     if ((rc = check_devices(1))) return rc;
-    BODE_CUDA(cudaSetDevice(0));
+    int dev = 0;  // the calling thread's current device
+    BODE_CUDA(cudaGetDevice(&dev));
     const int N = p->dim, P = p->param_dim;
     double *dy = nullptr, *dg = nullptr;
     BODE_CUDA(cudaMalloc(&dy, (size_t)num * N * sizeof(double)));
@@ -906,7 +927,7 @@ int bode_integrate_fixed(const bode_problem_t* p, int32_t solver, int32_t arith,
     if (P > 0) BODE_CUDA(cudaMemcpy(dg, g, (size_t)num * P * sizeof(double), cudaMemcpyHostToDevice));
     const int block = 128;
     const long long grid = (num * e->lanes + block - 1) / block;
-    BODE_CUDA((cudaError_t)e->prepare(e->ffn, 0, 0));
+    BODE_CUDA((cudaError_t)e->prepare(e->ffn, dev, 0));
     BODE_CUDA((cudaError_t)e->launch_fixed(e->ffn, dim3((unsigned)grid), dim3(block), 0, dg, dy,
                                            num, t0, t_end, num_steps, stages, kappa));
     g_launches.fetch_add(1);
