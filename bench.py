@@ -508,6 +508,11 @@ def main():
                               "sample": f"{max(1024, args.cpu_sample // 16)} systems x 10 "
                                         f"windows, {dt1:.2f} s"}}
 
+    clocks = clk.summary()
+    # nominal FP64 FMA peak at the SM clock observed during the timed region:
+    # 64 DFMA/clk/SM x 2 flop x SMs (37.2 TF at 1965 MHz)
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    nominal = 64 * 2 * sms * (clocks["sm_mhz"] or 1965.0) * 1e6
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
@@ -523,11 +528,12 @@ def main():
                      "traffic_source": traffic_src, "ncu": ncu_evidence,
                      "algorithmic_bytes_per_launch": num * (28 * 8 * 2 + 64),
                      "peak_source": "DFMA microbenchmark on this device in this run "
-                                    "(MEASURED_PEAKS.json has no FP64 entry); nominal 37.2",
+                                    "(MEASURED_PEAKS.json has no FP64 entry)",
+                     "peak_nominal": nominal / 1e12, "frac_of_nominal": achieved / nominal,
                      "flop_per_system_window": flops / (num * args.steps),
                      "kernel_ms_per_launch": sum(per) / len(per)},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-        "clocks": clk.summary(), **extra,
+        "clocks": clocks, **extra,
         "kernel_ms_per_window": [round(x, 4) for x in per],
         "systems_per_s_full_protocol": value / 10.0,
         "work_per_system_window": {
