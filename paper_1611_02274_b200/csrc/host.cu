@@ -412,6 +412,7 @@ int check_devices(int gpus) {
     }
     if (gpus < 1) return fail(BODE_E_INVALID_SHAPE, "num_gpus must be positive");
     if (gpus > n) return fail(BODE_E_NO_DEVICE, "num_gpus exceeds the visible device count");
+    if (n > 64) return fail(BODE_E_UNSUPPORTED, "more than 64 visible devices");
     return BODE_OK;
 }
 

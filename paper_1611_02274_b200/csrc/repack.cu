@@ -36,6 +36,7 @@ struct Scratch {
 Scratch g_scratch[64];
 
 int scratch(int dev, size_t bytes, void** out) {
+    if (dev < 0 || dev >= 64) return BODE_E_UNSUPPORTED;
     Scratch& s = g_scratch[dev];
     if (s.cap < bytes) {
         if (s.p) cudaFree(s.p);
@@ -147,6 +148,7 @@ int repack_by_cost(int N, int P, long long num, double* y, double* g, DevStats* 
     if (num < 2 || st == nullptr || order == nullptr) return BODE_OK;
     int dev = 0;
     RP_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return BODE_E_UNSUPPORTED;
     std::lock_guard<std::mutex> lock(g_scratch[dev].m);
     size_t sort_bytes = 0;
     RP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (unsigned*)nullptr,
@@ -206,6 +208,7 @@ int unpack(int N, int P, long long num, double* y, double* g, DevStats* st, long
     }
     int dev = 0;
     RP_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return BODE_E_UNSUPPORTED;
     std::lock_guard<std::mutex> lock(g_scratch[dev].m);
     const size_t n = (size_t)num;
     const int rows = N > P ? N : P;
@@ -246,6 +249,7 @@ int lockstep_efficiency(const DevStats* st, long long num, int group, double* ef
     static unsigned long long* hsum[64] = {nullptr};
     int dev = 0;
     RP_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return BODE_E_UNSUPPORTED;
     std::lock_guard<std::mutex> lock(m);
     if (dsum[dev] == nullptr) {
         RP_CUDA(cudaMalloc(&dsum[dev], 2 * sizeof(unsigned long long)));
