@@ -32,6 +32,7 @@ const KernelEntry* kernel_table(int* count) {
         // the default -- measured 16% over 4 lanes at 254 registers (8 warps/SM)
         BODE_BOTH_ARITH_R(Heat<64>, 8, 1, false, 1, 128),
         BODE_BOTH_ARITH(Heat<64>, 4, 1, false, 1),
+        BODE_BOTH_ARITH_R(Heat<64>, 4, 1, false, 1, 168),
         BODE_BOTH_ARITH_R(Heat<64>, 8, 1, false, 1, 168),
         BODE_BOTH_ARITH_R(Heat<64>, 8, 1, false, 1, 96),
         BODE_BOTH_ARITH_R(Heat<64>, 16, 1, false, 1, 96),

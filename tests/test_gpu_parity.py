@@ -306,7 +306,7 @@ def test_very_stiff_generator_path_bitwise(gpu, oracle):
     assert per_step.max() > 160, per_step.max()
 
 
-@pytest.mark.parametrize("env", [("4", "255"), ("8", "168"), ("8", "128"), ("8", "96"), ("16", "96"), ("16", "128")])
+@pytest.mark.parametrize("env", [("4", "255"), ("4", "168"), ("8", "168"), ("8", "128"), ("8", "96"), ("16", "96"), ("16", "128")])
 def test_heat64_lane_variants_bitwise(gpu, oracle, env):
     """Every compiled heat64 RKC instance (lanes per system x register cap,
     selected with BODE_LANES / BODE_MAXREG) gives the oracle's bits."""

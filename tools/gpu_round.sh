@@ -44,7 +44,8 @@ for p in $PARTS; do
       for B in 32 64; do timeout 600 python bench.py --no-e2e --no-cpu --no-secondary --block $B --persistent > $OUT/bench_pblock$B.txt 2>&1; done
       echo "ab_block rc=$?" >> $OUT/status.txt ;;
     ab_rkc)
-      for V in "8 128" "8 96" "16 96" "16 128"; do set -- $V
+      IFS=';' read -ra VS <<< "${AB_RKC_VARIANTS:-8 128;8 96;16 96;16 128}"
+      for V in "${VS[@]}"; do set -- $V
         BODE_LANES=$1 BODE_MAXREG=$2 timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 1048576 --rkc-systems 1048576 > $OUT/bench_rkc_L$1_R$2.txt 2>&1; done
       for R in 96 80; do BODE_LANES=1 BODE_MAXREG=$R timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 1048576 --rkc-systems 1048576 > $OUT/bench_rkc_exp$R.txt 2>&1; done
       echo "ab_rkc rc=$?" >> $OUT/status.txt ;;
