@@ -339,6 +339,38 @@ def int_driver_device(problem: OdeProblem, solver, arith, t: float, t_end: float
                                        ctypes.c_void_p(stream or None)))
 
 
+def order_init(order_ptr: int, num: int, stream: int = 0):
+    """Identity position -> system map for re-packing (bode_order_init)."""
+    check(lib().bode_order_init(ctypes.c_void_p(order_ptr), num, ctypes.c_void_p(stream or None)))
+
+
+def repack_by_cost(problem: OdeProblem, num: int, y_ptr: int, g_ptr: int, stats_ptr: int,
+                   order_ptr: int, stream: int = 0):
+    """Sort a device-resident batch by last-window RHS cost so similar systems
+    share warps (bode_repack_by_cost); results stay bitwise identical."""
+    check(lib().bode_repack_by_cost(ctypes.byref(problem.c()), num, ctypes.c_void_p(y_ptr),
+                                    ctypes.c_void_p(g_ptr or None), ctypes.c_void_p(stats_ptr),
+                                    ctypes.c_void_p(order_ptr), ctypes.c_void_p(stream or None)))
+
+
+def unpack(problem: OdeProblem, num: int, y_ptr: int, g_ptr: int, stats_ptr: int,
+           order_ptr: int, stream: int = 0):
+    """Restore the caller's order after repack_by_cost (bode_unpack)."""
+    check(lib().bode_unpack(ctypes.byref(problem.c()), num, ctypes.c_void_p(y_ptr),
+                            ctypes.c_void_p(g_ptr or None), ctypes.c_void_p(stats_ptr or None),
+                            ctypes.c_void_p(order_ptr), ctypes.c_void_p(stream or None)))
+
+
+def lockstep_efficiency(problem: OdeProblem, solver, arith, num: int, stats_ptr: int,
+                        stream: int = 0) -> float:
+    """SIMT lockstep efficiency implied by device stats (bode_lockstep_efficiency)."""
+    eff = ctypes.c_double()
+    check(lib().bode_lockstep_efficiency(ctypes.byref(problem.c()), _solver(solver),
+                                         _arith(arith), num, ctypes.c_void_p(stats_ptr),
+                                         ctypes.byref(eff), ctypes.c_void_p(stream or None)))
+    return eff.value
+
+
 # ------------------------------------------------------------- problems ----
 class problems:
     """problems.hpp:19-63."""

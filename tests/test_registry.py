@@ -56,3 +56,17 @@ def test_register_rejects_bad_tables():
     assert L.bode_register_kernels(None, 1, 8) == A.E_INVALID_SHAPE
     buf = (ctypes.c_char * 4096)()
     assert L.bode_register_kernels(buf, 1, 7) == A.E_UNSUPPORTED  # layout mismatch
+
+
+def test_repack_api_validation_without_device():
+    """Argument checks come first; without a device the calls fail loudly
+    (NO_DEVICE), never silently."""
+    import pytest as _pt
+    p = B.problems.pleiades()
+    with _pt.raises(B.api.InvalidShape):
+        B.api.repack_by_cost(p, 0, 1, 0, 1, 1)
+    if B.lib().bode_device_count() == 0:
+        with _pt.raises(B.api.NoDevice):
+            B.api.repack_by_cost(p, 16, 1, 0, 1, 1)
+        with _pt.raises(B.api.NoDevice):
+            B.api.order_init(1, 16)
