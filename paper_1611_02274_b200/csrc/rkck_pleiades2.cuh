@@ -130,83 +130,85 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
 #pragma unroll 1
     while (__any_sync(0xffffffffu, live)) {
         if (live) h = fmin_(tEnd - t, h);
-        if (__any_sync(0xffffffffu, live && !haveF)) {  // rkck.cpp:133-137
-            R Af[M];
-            pleiades_accel_pair<R>(G, q, Af);
-            if (live && !haveF) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) A0[i] = Af[i];
-                ++st.rhs_evals;
-                haveF = true;
-            }
-        }
+        // One call site for the pair RHS: j = 1 is f(t, y) when any lane
+        // needs it (rkck.cpp:133-137), j = 2..6 the stages (rkck.cpp:42-64).
+        // A single inlined copy keeps the kernel small enough for the
+        // instruction cache.
         R Q[M], Acc[M];
-        {  // stage 2 (rkck.cpp:42-44)
-            const R hb = h * R(b21);
-#pragma unroll
-            for (int i = 0; i < M; ++i) kset(0, i, v[i] + hb * A0[i]);
-#pragma unroll
-            for (int i = 0; i < M; ++i) Q[i] = q[i] + hb * v[i];
-            pleiades_accel_pair<R>(G, Q, Acc);
-#pragma unroll
-            for (int i = 0; i < M; ++i) kset(0, M + i, Acc[i]);
-        }
 #pragma unroll 1
-        for (int j = 3; j <= 6; ++j) {  // stages 3..6 (rkck.cpp:46-64)
-            const double b0 = c_ck_b[j - 3][0];
-            double bm[4];  // b_j2..b_j5 (zero past the stage's last term)
-#pragma unroll
-            for (int m = 0; m < 4; ++m) bm[m] = c_ck_b[j - 3][m + 1];
-            const int nk = j - 2;
+        for (int j = __any_sync(0xffffffffu, live && !haveF) ? 1 : 2; j <= 6; ++j) {
             const int out = (j == 6) ? 0 : j - 2;  // k6 reuses k2's slot
-            // the newest acceleration A_{j-1} is still in Acc; it is the last
-            // term of every stage sum, so reading it from registers keeps the
-            // reference's summation order
-            const double blast = c_ck_b[j - 3][nk];
-            if constexpr (is_exact<R>::value) {
+            if (j == 1) {
 #pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    R s = R(b0) * A0[i];
+                for (int i = 0; i < M; ++i) Q[i] = q[i];
+            } else if (j == 2) {  // stage 2: y + h*b21*f0
+                const R hb = h * R(b21);
 #pragma unroll
-                    for (int m = 0; m < 3; ++m)  // predicated: constant offsets, no loop
-                        if (m < nk - 1) s = s + R(bm[m]) * kget(m, M + i);
-                    s = s + R(blast) * Acc[i];
-                    Acc[i] = v[i] + h * s;
+                for (int i = 0; i < M; ++i) kset(0, i, v[i] + hb * A0[i]);
+#pragma unroll
+                for (int i = 0; i < M; ++i) Q[i] = q[i] + hb * v[i];
+            } else {
+                const double b0 = c_ck_b[j - 3][0];
+                double bm[4];  // b_j2..b_j5 (zero past the stage's last term)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) bm[m] = c_ck_b[j - 3][m + 1];
+                const int nk = j - 2;
+                // the newest acceleration A_{j-1} is still in Acc; it is the last
+                // term of every stage sum, so reading it from registers keeps the
+                // reference's summation order
+                const double blast = c_ck_b[j - 3][nk];
+                if constexpr (is_exact<R>::value) {
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        R s = R(b0) * A0[i];
+#pragma unroll
+                        for (int m = 0; m < 3; ++m)  // predicated: constant offsets, no loop
+                            if (m < nk - 1) s = s + R(bm[m]) * kget(m, M + i);
+                        s = s + R(blast) * Acc[i];
+                        Acc[i] = v[i] + h * s;
+                    }
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        R s = R(b0) * v[i];
+#pragma unroll
+                        for (int m = 0; m < 4; ++m)
+                            if (m < nk) s = s + R(bm[m]) * kget(m, i);
+                        Q[i] = q[i] + h * s;
+                    }
+                } else {  // FAST: h folded into the stage weights (rkck_nystrom.cuh)
+                    const double hb0 = val(h) * b0;
+                    double hbm[4];
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) hbm[m] = val(h) * bm[m];
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        double s = fma(hb0, val(A0[i]), val(v[i]));
+#pragma unroll
+                        for (int m = 0; m < 3; ++m)
+                            if (m < nk - 1) s = fma(hbm[m], val(kget(m, M + i)), s);
+                        Acc[i] = R(fma(val(h) * blast, val(Acc[i]), s));
+                    }
+#pragma unroll
+                    for (int i = 0; i < M; ++i) {
+                        double s = fma(hb0, val(v[i]), val(q[i]));
+#pragma unroll
+                        for (int m = 0; m < 4; ++m)
+                            if (m < nk) s = fma(hbm[m], val(kget(m, i)), s);
+                        Q[i] = R(s);
+                    }
                 }
 #pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    R s = R(b0) * v[i];
-#pragma unroll
-                    for (int m = 0; m < 4; ++m)
-                        if (m < nk) s = s + R(bm[m]) * kget(m, i);
-                    Q[i] = q[i] + h * s;
-                }
-            } else {  // FAST: h folded into the stage weights (rkck_nystrom.cuh)
-                const double hb0 = val(h) * b0;
-                double hbm[4];
-#pragma unroll
-                for (int m = 0; m < 4; ++m) hbm[m] = val(h) * bm[m];
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    double s = fma(hb0, val(A0[i]), val(v[i]));
-#pragma unroll
-                    for (int m = 0; m < 3; ++m)
-                        if (m < nk - 1) s = fma(hbm[m], val(kget(m, M + i)), s);
-                    Acc[i] = R(fma(val(h) * blast, val(Acc[i]), s));
-                }
-#pragma unroll
-                for (int i = 0; i < M; ++i) {
-                    double s = fma(hb0, val(v[i]), val(q[i]));
-#pragma unroll
-                    for (int m = 0; m < 4; ++m)
-                        if (m < nk) s = fma(hbm[m], val(kget(m, i)), s);
-                    Q[i] = R(s);
-                }
+                for (int i = 0; i < M; ++i) kset(out, i, Acc[i]);
             }
-#pragma unroll
-            for (int i = 0; i < M; ++i) kset(out, i, Acc[i]);
             pleiades_accel_pair<R>(G, Q, Acc);
-            if (j != 6) {  // A6 stays in Acc for the error norm and yNext
+            if (j == 1) {
+                if (live && !haveF) {
+#pragma unroll
+                    for (int i = 0; i < M; ++i) A0[i] = Acc[i];
+                    ++st.rhs_evals;
+                    haveF = true;
+                }
+            } else if (j != 6) {  // A6 stays in Acc for the error norm and yNext
 #pragma unroll
                 for (int i = 0; i < M; ++i) kset(out, M + i, Acc[i]);
             }
