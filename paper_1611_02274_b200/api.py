@@ -353,9 +353,10 @@ def repack_by_cost(problem: OdeProblem, num: int, y_ptr: int, g_ptr: int, stats_
                                     ctypes.c_void_p(order_ptr), ctypes.c_void_p(stream or None)))
 
 
-def unpack(problem: OdeProblem, num: int, y_ptr: int, g_ptr: int, stats_ptr: int,
-           order_ptr: int, stream: int = 0):
-    """Restore the caller's order after repack_by_cost (bode_unpack)."""
+def unpack_order(problem: OdeProblem, num: int, y_ptr: int, g_ptr: int, stats_ptr: int,
+                 order_ptr: int, stream: int = 0):
+    """Restore the caller's order after repack_by_cost (bode_unpack). (Not to be
+    confused with unpack(batch), the reference's BatchStates helper.)"""
     check(lib().bode_unpack(ctypes.byref(problem.c()), num, ctypes.c_void_p(y_ptr),
                             ctypes.c_void_p(g_ptr or None), ctypes.c_void_p(stats_ptr or None),
                             ctypes.c_void_p(order_ptr), ctypes.c_void_p(stream or None)))
