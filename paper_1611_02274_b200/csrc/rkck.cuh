@@ -95,14 +95,18 @@ struct KStore<R, C, true> {
 template <class R>
 __device__ __forceinline__ bool rkck_adjust(R h, R err, bool nanFlag, R hMin, R hMax,
                                             const DevTol& tol, R& hNew) {
-    if (err > R(1.0) || !isfinite_(err) || nanFlag) {
-        hNew = (!isfinite_(err) || nanFlag)
-                   ? R(tol.p1) * h
-                   : fmax_(R(tol.safety) * h * pow_(err, R(tol.pshrnk), tol.powtab), R(tol.p1) * h);
+    // one pow call site (it is large under EXACT: glibc's algorithm inline)
+    // with the exponent of whichever branch needs it: the same bits as two
+    const bool reject = err > R(1.0) || !isfinite_(err) || nanFlag;
+    const bool bad = !isfinite_(err) || nanFlag;
+    R pw(1.0);
+    if ((reject && !bad) || (!reject && err > R(tol.errcon)))
+        pw = pow_(err, R(reject ? tol.pshrnk : tol.pgrow), tol.powtab);  // FAST: ctrl_pow_fast
+    if (reject) {
+        hNew = bad ? R(tol.p1) * h : fmax_(R(tol.safety) * h * pw, R(tol.p1) * h);
         return false;
     }
-    R hn = (err > R(tol.errcon)) ? R(tol.safety) * h * pow_(err, R(tol.pgrow), tol.powtab) : R(5.0) * h;
-    // (FAST: pow_ is ctrl_pow_fast, arith.cuh)
+    const R hn = (err > R(tol.errcon)) ? R(tol.safety) * h * pw : R(5.0) * h;
     hNew = fmax_(hMin, fmin_(hMax, hn));
     return true;
 }
