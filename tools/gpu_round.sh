@@ -94,6 +94,10 @@ for p in $PARTS; do
     ab_exactreg)
       for R in 168 128 200; do BODE_MAXREG=$R timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/bench_exactreg$R.txt 2>&1; done
       echo "ab_exactreg rc=$?" >> $OUT/status.txt ;;
+    ab_heatblk)
+      for V in "128 128" "112 64" "112 128" "128 64"; do set -- $V
+        BODE_LANES=8 BODE_MAXREG=$1 timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 65536 --rkc-systems 1048576 --block $2 > $OUT/bench_heat_R$1_B$2.txt 2>&1; done
+      echo "ab_heatblk rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
