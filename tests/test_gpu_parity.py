@@ -374,3 +374,43 @@ def test_ragged_batch_sizes_bitwise(gpu, oracle, num):
         assert np.array_equal(y.view(np.uint64), yo.view(np.uint64)), (prob.kind, num)
         for k in COUNTS:
             assert np.array_equal(st[k], so[k]), (prob.kind, num, k)
+
+
+def test_outer_loop_pinned_params_and_repack(gpu):
+    """Pinned buffers with per-system parameters (config 4, P = 1): chunked
+    strided upload of y and g, automatic re-packing after window 1, unpack and
+    whole download at the end -- bitwise the pageable path and the oracle."""
+    import ctypes
+    import torch
+    L = B.lib()
+    num = 1 << 18
+    case = dict(CASES["cfg4_expdecay_rkc_stiff"])
+    prob, solver, y0, g = build_inputs(case, num)
+    tol = A.default_tol()
+    outs = {}
+    for pinned in (False, True):
+        yh = torch.from_numpy(y0.copy())
+        gh = torch.from_numpy(g.copy())
+        sth = torch.zeros(num * 8, dtype=torch.int64)
+        if pinned:
+            yh, gh, sth = yh.pin_memory(), gh.pin_memory(), sth.pin_memory()
+        n = ctypes.c_int32(0)
+        dp = lambda t: ctypes.cast(t.data_ptr(), ctypes.POINTER(ctypes.c_double))
+        B.api.check(L.bode_outer_loop(ctypes.byref(prob), solver, A.ARITH_EXACT, 0.0, 1.0, 0.1,
+                                      num, dp(gh), dp(yh), ctypes.byref(tol),
+                                      ctypes.c_void_p(sth.data_ptr()), 1, B.api.SINK(), None,
+                                      ctypes.byref(n)))
+        outs[pinned] = (yh.numpy().copy(), sth.numpy().copy())
+    assert np.array_equal(outs[False][0].view(np.uint64), outs[True][0].view(np.uint64))
+    assert np.array_equal(outs[False][1], outs[True][1])
+    idx = np.arange(0, num, 97)
+    rc, yo, so, _ = oracle_outer_sample(prob, solver, y0, g, num, idx)
+    assert np.array_equal(outs[True][0].reshape(1, num)[:, idx].reshape(-1).view(np.uint64),
+                          yo.view(np.uint64))
+
+
+def oracle_outer_sample(prob, solver, y0, g, num, idx):
+    from oracle_lib import Oracle
+    sub_y = np.ascontiguousarray(y0.reshape(prob.dim, num)[:, idx]).reshape(-1)
+    sub_g = np.ascontiguousarray(g.reshape(prob.param_dim, num)[:, idx]).reshape(-1)
+    return Oracle().outer_loop(prob, solver, 0.0, 1.0, 0.1, sub_y, sub_g)
