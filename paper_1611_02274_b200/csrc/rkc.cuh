@@ -25,6 +25,24 @@
 
 namespace bode {
 
+// Phase timing (tools/phase_probe.cu builds with BODE_PHASE_TIMING): clock64()
+// deltas per rkc_system phase, summed over lane groups into g_phase[0..4] =
+// power method, initial step, stage loop, f_trial + error norm, controller.
+#ifdef BODE_PHASE_TIMING
+__device__ unsigned long long* g_phase = nullptr;
+#define BODE_PHASE_DECL long long ph_acc[5] = {0, 0, 0, 0, 0}, ph_t = 0, ph_last = -1;
+#define BODE_PHASE_MARK(k) do { const long long n_ = clock64(); if ((k) >= 0) ph_acc[k] += n_ - ph_t; ph_t = n_; } while (0)
+#define BODE_PHASE_CTRL_BEGIN ph_last = clock64();
+#define BODE_PHASE_CTRL_END if (ph_last >= 0) { ph_acc[4] += clock64() - ph_last; ph_last = -1; }
+#define BODE_PHASE_FLUSH if (g_phase && G.lane == 0) for (int k_ = 0; k_ < 5; ++k_) atomicAdd(&g_phase[k_], (unsigned long long)ph_acc[k_]);
+#else
+#define BODE_PHASE_DECL
+#define BODE_PHASE_MARK(k)
+#define BODE_PHASE_CTRL_BEGIN
+#define BODE_PHASE_CTRL_END
+#define BODE_PHASE_FLUSH
+#endif
+
 // Running Chebyshev triple (T_j, T'_j, T''_j) at x (rkc.cpp:18-25).
 template <class R>
 struct Cheb {
@@ -410,14 +428,17 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, double t_in, doubl
 
     int state = kTop;
     R hMin(0.0), hNewRej(0.0);
+    BODE_PHASE_DECL
 #pragma unroll 1
     for (;;) {
+        BODE_PHASE_CTRL_END
         if (state == kTop) {
             if (!(tEnd - t > uround * fabs_(tEnd))) break;
             hMin = R(10.0) * uround * fmax_(fabs_(t), hMax);
             if (R(1.1) * wsH >= fabs_(tEnd - t)) wsH = fabs_(tEnd - t);
             state = (numStep % 25 == 0) ? kSrThenAttempt : kAttempt;
         }
+        BODE_PHASE_MARK(-1);
         if (state == kSrThenAttempt || state == kSrThenRejectTail) {
             R sig;
             const int it = power_method<P, R, L>(G, t, ys, g, f0, hMax, eig, sig);
@@ -435,6 +456,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, double t_in, doubl
             state = kTop;
             continue;
         }
+        BODE_PHASE_MARK(0);
         // ---- state == kAttempt ----
         R wa[C], wb[C];
         if (wsH < uround) {  // initialStep (rkc.cpp:146-171), one RHS
@@ -469,6 +491,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, double t_in, doubl
             }
         }
         const R h = wsH;
+        BODE_PHASE_MARK(1);
         // ---- rkc::step (rkc.cpp:82-117) with coefficients (rkc.cpp:29-69)
         // from the per-device table for s <= kRkcTableMaxS, else generated ----
         const double* crow = (tol.rkc_coef != nullptr && s <= kRkcTableMaxS)
@@ -526,6 +549,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, double t_in, doubl
         }
         st.rhs_evals += s - 1;
         st.stages_total += s;
+        BODE_PHASE_MARK(2);
         P::template rhs<R, L>(G, t + h, wa, g, wb);  // f_trial (rkc.cpp:247)
         ++st.rhs_evals;
         // errorNorm (rkc.cpp:119-129)
@@ -539,6 +563,8 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, double t_in, doubl
             for (int c = 0; c < C; ++c) terms[c] = terms[c] * terms[c];
             err = sqrt_(rkc_seq_sum<R, L, C>(G, terms, R(0.0)) / R(double(P::N)));
         }
+        BODE_PHASE_MARK(3);
+        BODE_PHASE_CTRL_BEGIN
         const bool accepted = err <= R(1.0);
         // one cbrt call site (glibc's algorithm inline under EXACT) for both
         // controllers (rkc.cpp:177-190): cbrt(err) whenever err is finite
@@ -577,6 +603,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, double t_in, doubl
     }
 #pragma unroll
     for (int c = 0; c < C; ++c) y[c] = ys[c];
+    BODE_PHASE_FLUSH
     st_out = st;
 }
 

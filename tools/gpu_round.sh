@@ -98,6 +98,11 @@ for p in $PARTS; do
       for V in "128 128" "112 64" "112 128" "128 64"; do set -- $V
         BODE_LANES=8 BODE_MAXREG=$1 timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 65536 --rkc-systems 1048576 --block $2 > $OUT/bench_heat_R$1_B$2.txt 2>&1; done
       echo "ab_heatblk rc=$?" >> $OUT/status.txt ;;
+    phase)
+      nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Ipaper_1611_02274_b200/csrc \
+        -DBODE_PHASE_TIMING tools/phase_probe.cu -o /tmp/phase_probe > $OUT/phase_build.txt 2>&1
+      timeout 300 /tmp/phase_probe > $OUT/phase.txt 2>&1
+      echo "phase rc=$?" >> $OUT/status.txt ;;
     quick)
       timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/quick_fast.txt 2>&1
       timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/quick_exact.txt 2>&1
