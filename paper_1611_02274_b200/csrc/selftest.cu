@@ -140,6 +140,15 @@ __global__ void exact_math_kernel(const double* __restrict__ x, long long n, int
         bool fast;
         got = bode::div_rn_nv(a, b, fast);
         if (!fast) return;
+    } else if (op == 3) {  // the EXACT policy's sqrt_ on every input (fallback included)
+        ref = __dsqrt_rn(v);
+        got = val(bode::sqrt_(bode::xd(v)));
+        if (ref != ref && got != got) return;  // NaN payloads aside
+    } else if (op == 4) {  // the EXACT policy's operator/ on every pair (fallback included)
+        if (i % 2) return;
+        ref = __ddiv_rn(v, x[i + 1]);
+        got = val(bode::xd(v) / bode::xd(x[i + 1]));
+        if (ref != ref && got != got) return;
     } else {
         if (!bode::in_safe_range(v)) return;
         got = op == 0 ? bode::sqrt_rn_bf(v) : bode::rcp_rn_bf(v);

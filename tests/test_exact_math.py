@@ -25,6 +25,30 @@ def cases(n, seed):
     return np.concatenate([rand_bits, edges, pleiades, pleiades * np.sqrt(pleiades)])
 
 
+def full_range_cases(n, seed):
+    """Every exponent (subnormals, Inf, NaN included), random and edge
+    significands, both signs: the EXACT sqrt_ / operator/ wrappers must equal
+    the intrinsics everywhere, through their fallback where needed."""
+    rng = np.random.default_rng(seed)
+    bits = rng.integers(0, 1 << 63, n, dtype=np.uint64) | (rng.integers(0, 2, n, dtype=np.uint64) << np.uint64(63))
+    x = bits.view(np.float64)
+    edge = np.array([0.0, -0.0, 5e-324, -5e-324, 2.2250738585072014e-308, np.inf, -np.inf,
+                     np.nan, 1.0, -1.0, 1.7976931348623157e308, 2.0 ** -970, 2.0 ** -971,
+                     2.0 ** 1023])
+    return np.concatenate([x, np.repeat(edge, 2), np.tile(edge, 2)])
+
+
+@pytest.mark.parametrize("op", [3, 4], ids=["sqrt_policy", "div_policy"])
+def test_policy_ops_match_ieee_everywhere(gpu, op):
+    from paper_1611_02274_b200 import _abi as A
+    bad, first = ctypes.c_int64(), ctypes.c_int64()
+    for seed in range(4):
+        x = full_range_cases(5_000_000, 50 + seed)
+        gpu.api.check(gpu.lib().bode_selftest_exact_math(A.dptr(x), x.size, op,
+                                                         ctypes.byref(bad), ctypes.byref(first)))
+        assert bad.value == 0, f"{bad.value} mismatches, first x = {x[first.value]!r}"
+
+
 @pytest.mark.parametrize("op", [0, 1, 2], ids=["sqrt", "rcp", "div"])
 def test_branch_free_matches_ieee(gpu, op):
     from paper_1611_02274_b200 import _abi as A
