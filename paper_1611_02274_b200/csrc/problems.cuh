@@ -60,7 +60,6 @@ __device__ __forceinline__ R grp_from(const Group<L>& G, R v, int src) {
     return R(G.from(val(v), src));
 }
 
-constexpr bool kSeqSumGather = false;  // measured: -18% (heat64), -13% (Brusselator)
 // Sequential sum in global component order: lane 0 sums its C terms, hands
 // the partial to lane 1, ... exactly the reference's `sum += term` loop
 // (rkc.cpp:122-127, spectral_radius.cpp:11-13). Result valid on every lane.
@@ -70,16 +69,6 @@ __device__ __forceinline__ R seq_sum(const Group<L>& G, const R (&terms)[C], R i
         R s = init;
 #pragma unroll
         for (int c = 0; c < C; ++c) s = s + terms[c];
-        return s;
-    } else if constexpr (kSeqSumGather) {
-        // every lane receives the group's terms in component order (shuffles,
-        // off the dependency chain) and runs the same sequential sum: the chain
-        // is the N adds alone, with no lane-to-lane hand-offs
-        R s = init;
-#pragma unroll
-        for (int k = 0; k < L; ++k)
-#pragma unroll
-            for (int c = 0; c < C; ++c) s = s + R(G.from(val(terms[c]), k));
         return s;
     } else {
         R s = init;

@@ -112,17 +112,12 @@ struct RkcCoefGen {
     }
 };
 
-// Shared-memory row per lane: the eigenvector, f0, the lane's stats, (with
-// kRkcYInSmem) the state y, and (with kRkcSumSmem) a C-double scratch for the
-// group's sequential sums (3C + 8 or 4C + 8 doubles, odd stride).
-constexpr bool kRkcSumSmemFlag = false;  // measured: heat64 -4%, Brusselator -8% at 8 lanes
-constexpr bool kRkcSumHandoffFlag = false;  // measured: heat64 -5%, Brusselator -9% at 8 lanes The stats are touched a few times per attempt;
+// Shared-memory row per lane: the eigenvector, f0, the lane's stats and (with
+// kRkcYInSmem) the state y (3C + 8 doubles, odd stride). The stats are touched a few times per attempt;
 // keeping their 15 registers out of the stage loop removes most spills at
 // the 128-register cap.
 template <int C>
-__host__ __device__ constexpr int kRkcSmemStride() {
-    return ((kRkcSumSmemFlag ? 4 : 3) * C + 8 + (kRkcSumHandoffFlag ? 2 : 0)) | 1;
-}
+__host__ __device__ constexpr int kRkcSmemStride() { return (3 * C + 8) | 1; }
 
 // Per-device coefficient table for s = 2..kRkcTableMaxS: row(s) holds
 // muTilde_1 followed by (mu_j, nu_j, muTilde_j, gammaTilde_j, c_{j-1}) for
@@ -240,57 +235,12 @@ __device__ __forceinline__ void elementwise_quotients(Num num, Den den, R (&out)
 }
 
 // The reference's sequential sums (rkc.cpp:122-127, spectral_radius.cpp:11-13)
-// for a lane group. With kRkcSumSmem every lane parks its C terms in its
-// shared-memory scratch and the group's lane 0 runs the whole chain in
-// component order -- the same adds as seq_sum, without a shuffle hand-off
-// (and its convergence checks) between every C of them.
-constexpr bool kRkcSumSmem = kRkcSumSmemFlag;
-constexpr bool kRkcSumHandoff = kRkcSumHandoffFlag;
+// for a lane group: seq_sum's shuffle hand-off. (Measured alternatives, all
+// slower: lane 0 running the chain from shared memory, -4%; a shared-memory
+// hand-off with __syncwarp, -5%; gathering every term by shuffles, -18%.)
 template <class R, int L, int C>
 __device__ __forceinline__ R rkc_seq_sum(const Group<L>& G, const R (&terms)[C], R init) {
-    if constexpr (L > 1 && kRkcSumHandoff && !kRkcSumSmem) {
-        // seq_sum's lane-to-lane hand-off through two shared-memory slots of
-        // the group's lane 0 (alternating, so one __syncwarp per hand-off is
-        // race-free) instead of a shuffle with a run-time member mask, whose
-        // convergence check costs ~6 instructions per call
-        extern __shared__ double bode_smem[];
-        constexpr int S = kRkcSmemStride<C>();
-        double* const slot = bode_smem + (threadIdx.x - G.lane) * S + (S - 3);
-        R s = init;
-#pragma unroll 1
-        for (int k = 0; k < L; ++k) {
-            if (G.lane == k) {
-#pragma unroll
-                for (int c = 0; c < C; ++c) s = s + terms[c];
-                slot[k & 1] = val(s);
-            }
-            __syncwarp(G.mask);
-            s = R(slot[k & 1]);
-        }
-        return s;
-    } else if constexpr (L == 1 || !kRkcSumSmem) {
-        return seq_sum<R, L, C>(G, terms, init);
-    } else {
-        extern __shared__ double bode_smem[];
-        constexpr int S = kRkcSmemStride<C>();
-        double* const mine = bode_smem + threadIdx.x * S + 3 * C + 8;
-        double* const lead = mine - G.lane * S;  // the group's lane 0
-#pragma unroll
-        for (int c = 0; c < C; ++c) mine[c] = val(terms[c]);
-        __syncwarp(G.mask);
-        if (G.lane == 0) {
-            R s = init;
-#pragma unroll
-            for (int k = 0; k < L; ++k)
-#pragma unroll
-                for (int c = 0; c < C; ++c) s = s + R(lead[k * S + c]);
-            lead[0] = val(s);  // after its own reads, in program order
-        }
-        __syncwarp(G.mask);
-        const R out = R(lead[0]);
-        __syncwarp(G.mask);  // everyone has read before the scratch is reused
-        return out;
-    }
+    return seq_sum<R, L, C>(G, terms, init);
 }
 
 // Power method (spectral_radius.cpp:17-85). Returns sigma (with the 1.2

@@ -96,7 +96,6 @@ __host__ __device__ constexpr int nystrom_smem_doubles() {
 // Per-lane solver state: one system, advanced one attempt at a time, so a
 // persistent kernel can hand a lane a new system as soon as its own finishes.
 constexpr bool kRkckUnrollStages = false;  // measured: unrolling adds spills, -16%
-constexpr bool kRefillUniformF0 = false;   // persistent refill: f0 on every attempt
 
 template <class P, class R>
 struct NystromRkck {
@@ -129,11 +128,6 @@ struct NystromRkck {
     }
 
     // one pass of the while loop of rkck.cpp:131-157
-    // UNIFORM_F0: evaluate f(t, y) on every attempt, so lanes of a warp that
-    // are at different points of their integrations (refill) never diverge on
-    // it. A rejected retry recomputes the same bits it would have reused, and
-    // only the evaluations the reference performs are counted.
-    template <bool UNIFORM_F0 = false>
     __device__ __forceinline__ void attempt(const DevTol& tol) {
         using namespace ck;
         R* const q = y;
@@ -141,9 +135,9 @@ struct NystromRkck {
         const R hMin(tol.h_min_floor);
         const R uround(tol.uround), eps(tol.eps), tiny(tol.tiny);
         h = fmin_(tEnd - t, h);
-        if (UNIFORM_F0 || !haveF) {  // rejected retries reuse f(t, y) (rkck.cpp:133-137)
+        if (!haveF) {  // rejected retries reuse f(t, y) (rkck.cpp:133-137)
             P::template accel<R>(t, q, gp, A0);
-            if (!haveF) ++st.rhs_evals;
+            ++st.rhs_evals;
             haveF = true;
         }
         if constexpr (!is_exact<R>::value) {
@@ -577,7 +571,7 @@ __device__ __forceinline__ void rkck_nystrom_persistent(const double* __restrict
         // slower, so the attempt stays guarded by `has`)
 #pragma unroll 1
         do {
-            if (has && s.live) s.template attempt<kRefillUniformF0>(tol);
+            if (has && s.live) s.attempt(tol);
             if (has && !s.live) retire();
         } while (__popc(__ballot_sync(kFull, !has)) < stop);
     }
