@@ -49,9 +49,6 @@ for p in $PARTS; do
         BODE_LANES=$1 BODE_MAXREG=$2 timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 1048576 --rkc-systems 1048576 > $OUT/bench_rkc_L$1_R$2.txt 2>&1; done
       for R in 96 80; do BODE_LANES=1 BODE_MAXREG=$R timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 1048576 --rkc-systems 1048576 > $OUT/bench_rkc_exp$R.txt 2>&1; done
       echo "ab_rkc rc=$?" >> $OUT/status.txt ;;
-    ab_stagger)
-      I=0; for S in ${AB_STAGGER:-0 1000 4000 16000 0}; do I=$((I+1)); BODE_RKC_STAGGER=$S timeout 600 python bench.py --no-e2e --no-cpu --steps 5 > $OUT/bench_stagger${I}_$S.txt 2>&1; done
-      echo "ab_stagger rc=$?" >> $OUT/status.txt ;;
     ncu_late)
       for W in 0 9; do
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:Pleiades, double" \
