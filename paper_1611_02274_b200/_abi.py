@@ -119,4 +119,5 @@ def vptr(a: np.ndarray):
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "lib", "libbode.so")
+# BODE_LIB_PATH: another in-tree build of the same library, for A/B timing
+LIB_PATH = os.environ.get("BODE_LIB_PATH") or os.path.join(PKG_DIR, "lib", "libbode.so")

@@ -42,15 +42,21 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
     constexpr int PP = P::P > 0 ? P::P : 1;
     const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long sys = gt / L;
-    if (sys >= num) return;  // whole lane groups retire together
+    // RKC on lane groups runs warp-uniform (rkc.cuh): lanes past the batch's
+    // end stay with their warp as idle groups; elsewhere lanes retire here
+    constexpr bool kUniform = SOLVER == 1 && L > 1;
+    const bool inRange = sys < num;
+    if (kUniform ? !__any_sync(0xffffffffu, inRange) : !inRange) return;
     const long long ld = tol.stride > 0 ? tol.stride : num;  // SoA row stride
-    Group<L> G;
+    Group<L> G(kUniform);
     R y[C];
     R g[PP];
 #pragma unroll
-    for (int c = 0; c < C; ++c) y[c] = R(y_soa[sys + ld * (long long)comp_index<P, L>(G.lane, c)]);
+    for (int c = 0; c < C; ++c)
+        y[c] = R(inRange ? y_soa[sys + ld * (long long)comp_index<P, L>(G.lane, c)] : 0.0);
 #pragma unroll
-    for (int p = 0; p < PP; ++p) g[p] = R(P::P > 0 ? g_soa[sys + ld * (long long)p] : 0.0);
+    for (int p = 0; p < PP; ++p)
+        g[p] = R(P::P > 0 && inRange ? g_soa[sys + ld * (long long)p] : 0.0);
     DevStats st;
     if constexpr (SOLVER == 0 && is_pleiades<P> && L == 2)
         rkck_pleiades2_system<R>(G, t, tEnd, y, tol, st);
@@ -58,8 +64,11 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
         rkck_nystrom_system<P, R>(t, tEnd, y, g, tol, st);
     else if constexpr (SOLVER == 0)
         rkck_system<P, R, L, KSMEM>(G, t, tEnd, y, g, tol, st);
+    else if constexpr (L == 1)
+        rkc_system_lane<P, R>(G, t, tEnd, y, g, tol, st);
     else
-        rkc_system<P, R, L>(G, t, tEnd, y, g, tol, st);
+        rkc_system<P, R, L>(G, inRange, t, tEnd, y, g, tol, st);
+    if (!inRange) return;
 #pragma unroll
     for (int c = 0; c < C; ++c) y_soa[sys + ld * (long long)comp_index<P, L>(G.lane, c)] = val(y[c]);
     if (stats != nullptr && G.lane == 0) {

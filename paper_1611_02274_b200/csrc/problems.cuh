@@ -13,15 +13,19 @@
 
 namespace bode {
 
-// Lane group of L lanes (L divides 32) inside a warp.
+// Lane group of L lanes (L divides 32) inside a warp. The shuffles name the
+// group's own lanes by default; a warp-uniform caller (every lane of the warp
+// reaches every shuffle, as the RKC driver guarantees) passes full = true, and
+// the constant full mask lets ptxas drop its per-shuffle convergence check
+// (MATCH.ANY / REDUX / VOTE and a divergent-path branch).
 template <int L>
 struct Group {
     int lane;       // 0..L-1
-    unsigned mask;  // the group's lanes in the warp
-    __device__ __forceinline__ Group() {
+    unsigned mask;  // the lanes taking part in each shuffle
+    __device__ __forceinline__ explicit Group(bool full = false) {
         const int wl = threadIdx.x & 31;
         lane = wl & (L - 1);
-        mask = (L == 32) ? 0xffffffffu : (((1u << L) - 1u) << (wl & ~(L - 1)));
+        mask = (L == 32 || full) ? 0xffffffffu : (((1u << L) - 1u) << (wl & ~(L - 1)));
     }
     // value held by group lane `src`
     __device__ __forceinline__ double from(double v, int src) const {
@@ -47,7 +51,7 @@ template <>
 struct Group<1> {
     int lane = 0;
     unsigned mask = 0u;
-    __device__ __forceinline__ Group() {}
+    __device__ __forceinline__ explicit Group(bool = false) {}
     __device__ __forceinline__ double from(double v, int) const { return v; }
     __device__ __forceinline__ double from_prev(double v) const { return v; }
     __device__ __forceinline__ double from_next(double v) const { return v; }

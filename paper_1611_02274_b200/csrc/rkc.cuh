@@ -16,7 +16,9 @@
 //  * The driver loop is a small state machine (TOP -> [SPECRAD] -> ATTEMPT,
 //    reject -> SPECRAD -> REJECT_TAIL) so the power method, the initial step
 //    and the stage recurrence each have one call site in the kernel. The
-//    event order per system is exactly the reference's.
+//    event order per system is exactly the reference's. The loop is
+//    warp-uniform: each phase runs for the whole warp when any group needs
+//    it, so the lane-group shuffles use the full warp mask.
 //  * Sums that the reference accumulates sequentially (error norm, 2-norms)
 //    stay sequential in component order across the lane group (seq_sum).
 #pragma once
@@ -243,11 +245,25 @@ __device__ __forceinline__ R rkc_seq_sum(const Group<L>& G, const R (&terms)[C],
     return seq_sum<R, L, C>(G, terms, init);
 }
 
-// Power method (spectral_radius.cpp:17-85). Returns sigma (with the 1.2
-// safety factor) and the number of iterations (= RHS evaluations); eig is the
-// warm start on entry and v - y on exit.
+// For lane groups (L > 1) every lane of the warp reaches every shuffle of the
+// driver below (see rkc_system); this is the warp-wide vote that keeps its
+// phases uniform. With one lane per system there are no shuffles and each
+// lane branches on its own state.
+template <int L>
+__device__ __forceinline__ bool phase_any(bool b) {
+    if constexpr (L > 1)
+        return __any_sync(0xffffffffu, b);
+    else
+        return b;
+}
+
+// Power method (spectral_radius.cpp:17-85) for the groups with `on` set; the
+// other groups of the warp run alongside on their own state and discard the
+// result. Returns sigma (with the 1.2 safety factor) and the number of
+// iterations (= RHS evaluations); eig is the warm start on entry and v - y
+// on exit.
 template <class P, class R, int L, class Y, class F0>
-__device__ __forceinline__ int power_method(const Group<L>& G, R t, const Y& y,
+__device__ __forceinline__ int power_method(const Group<L>& G, bool on, R t, const Y& y,
                                             const R* g, const F0& f0, R hMax, double* eig,
                                             R& sigmaOut) {
     constexpr int C = P::N / L;
@@ -282,46 +298,57 @@ __device__ __forceinline__ int power_method(const Group<L>& G, R t, const Y& y,
     }
     R sigma(0.0);
     int iters = 0;
+    bool run = on;
 #pragma unroll 1
     for (int iter = 1; iter <= kItMax; ++iter) {
+        if constexpr (L > 1)
+            if (!phase_any<L>(run)) break;
         R fv[C];
         P::template rhs<R, L>(G, t, v, g, fv);
-        iters = iter;
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             const R d = fv[c] - f0[c];
             tmp[c] = d * d;
         }
         const R diffNrm = sqrt_(rkc_seq_sum<R, L, C>(G, tmp, R(0.0)));
-        const R sigmaOld = sigma;
-        sigma = diffNrm / dynrm;
-        if (iter >= 2 && fabs_(sigma - sigmaOld) <= fmax_(sigma, small) * R(0.01)) break;
-        if (diffNrm != R(0.0)) {
+        if (L == 1 || run) {  // one lane per system: always on (rkc_system_lane)
+            iters = iter;
+            const R sigmaOld = sigma;
+            sigma = diffNrm / dynrm;
+            if (iter >= 2 && fabs_(sigma - sigmaOld) <= fmax_(sigma, small) * R(0.01)) {
+                if constexpr (L == 1) break;
+                run = false;
+            } else if (diffNrm != R(0.0)) {
 #pragma unroll
-            for (int c = 0; c < C; ++c) v[c] = y[c] + (fv[c] - f0[c]) * (dynrm / diffNrm);
-        } else {  // degenerate direction: flip one component about y
-            const int ind = iter % P::N;
+                for (int c = 0; c < C; ++c) v[c] = y[c] + (fv[c] - f0[c]) * (dynrm / diffNrm);
+            } else {  // degenerate direction: flip one component about y
+                const int ind = iter % P::N;
 #pragma unroll
-            for (int c = 0; c < C; ++c)
-                if (G.lane * C + c == ind) v[c] = y[c] - (v[c] - y[c]);
+                for (int c = 0; c < C; ++c)
+                    if (G.lane * C + c == ind) v[c] = y[c] - (v[c] - y[c]);
+            }
         }
     }
     sigmaOut = R(1.2) * sigma;
+    if (on) {
 #pragma unroll
-    for (int c = 0; c < C; ++c) eig[c] = val(v[c] - y[c]);
+        for (int c = 0; c < C; ++c) eig[c] = val(v[c] - y[c]);
+    }
     return iters;
 }
 
 // One RKC stage j >= 2 (rkc.cpp:99-112): dst <- w_j from src = w_{j-1} and
 // dst = w_{j-2} on entry (ignored when first, i.e. w_{j-2} = y).
+// Groups with `act` clear evaluate the RHS with the warp and keep dst.
 template <class P, class R, int L, class Y, class F0>
-__device__ __forceinline__ void rkc_stage(const Group<L>& G, R tj, const Y& y,
+__device__ __forceinline__ void rkc_stage(const Group<L>& G, bool act, R tj, const Y& y,
                                           const F0& f0, const R* g,
                                           const R (&src)[P::N / L], R (&dst)[P::N / L], R muj,
                                           R nuj, R mujh, R gjh, bool first) {
     constexpr int C = P::N / L;
     R f[C];
     P::template rhs<R, L>(G, tj, src, g, f);
+    if (!act) return;
     if (first) {
 #pragma unroll
         for (int c = 0; c < C; ++c)
@@ -336,12 +363,16 @@ __device__ __forceinline__ void rkc_stage(const Group<L>& G, R tj, const Y& y,
 
 enum RkcState { kTop = 0, kSrThenAttempt = 1, kAttempt = 2, kSrThenRejectTail = 3, kRejectTail = 4 };
 
-// rkc::driver (rkc.cpp:193-281) for this lane group's system.
-template <class P, class R, int L>
-__device__ __forceinline__ void rkc_system(const Group<L>& G, double t_in, double tEnd_in,
-                                           R (&y)[P::N / L], const R* g, const DevTol& tol,
-                                           DevStats& st_out) {
-    constexpr int C = P::N / L;
+// rkc::driver (rkc.cpp:193-281) with one lane per system: the same state
+// machine as rkc_system below, each lane branching on its own state. (The
+// warp-uniform form measured 5% slower here: with no shuffles to save, its
+// extra predication only costs.)
+template <class P, class R>
+__device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, double tEnd_in,
+                                                R (&y)[P::N], const R* g, const DevTol& tol,
+                                                DevStats& st_out) {
+    constexpr int L = 1;
+    constexpr int C = P::N;
     extern __shared__ double bode_smem[];
     DevStats& st = *reinterpret_cast<DevStats*>(bode_smem + threadIdx.x * kRkcSmemStride<C>() + 2 * C);
     stats_init(st);
@@ -391,7 +422,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, double t_in, doubl
         BODE_PHASE_MARK(-1);
         if (state == kSrThenAttempt || state == kSrThenRejectTail) {
             R sig;
-            const int it = power_method<P, R, L>(G, t, ys, g, f0, hMax, eig, sig);
+            const int it = power_method<P, R, L>(G, true, t, ys, g, f0, hMax, eig, sig);
             wsSpecRad = sig;
             ++st.spec_rad_evals;
             st.rhs_evals += it;
@@ -488,9 +519,9 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, double t_in, doubl
             }
             const R tj = t + cjm1 * h;
             if (inA)
-                rkc_stage<P, R, L>(G, tj, ys, f0, g, wa, wb, muj, nuj, muTj * h, gTj * h, j == 2);
+                rkc_stage<P, R, L>(G, true, tj, ys, f0, g, wa, wb, muj, nuj, muTj * h, gTj * h, j == 2);
             else
-                rkc_stage<P, R, L>(G, tj, ys, f0, g, wb, wa, muj, nuj, muTj * h, gTj * h, false);
+                rkc_stage<P, R, L>(G, true, tj, ys, f0, g, wb, wa, muj, nuj, muTj * h, gTj * h, false);
             inA = !inA;
         }
         if (!inA) {  // y_trial = w_s -> wa
@@ -515,6 +546,256 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, double t_in, doubl
         }
         BODE_PHASE_MARK(3);
         BODE_PHASE_CTRL_BEGIN
+        const bool accepted = err <= R(1.0);
+        // one cbrt call site (glibc's algorithm inline under EXACT) for both
+        // controllers (rkc.cpp:177-190): cbrt(err) whenever err is finite
+        const R cb = isfinite_(err) ? cbrt_(err) : R(1.0);
+        if (!accepted) {
+            ++st.steps_rejected;
+            hNewRej = isfinite_(err) ? R(0.8) * h / cb : R(tol.p1) * h;
+            state = kSrThenRejectTail;
+        } else {
+            t += h;
+            ++numStep;
+            stats_accept(st, val(h));
+            const bool firstAccepted = wsHOld < uround;
+            // nextStepAccepted (rkc.cpp:173-187); cbrt(errOld) is the previous
+            // accepted step's cbrt(err) unless errOld was floored at uround
+            R fac(10.0);
+            if (firstAccepted) {
+                if (R(0.8) < fac * cb) fac = R(0.8) / cb;
+            } else {
+                const R t1 = R(0.8) * h * cbErrOld;
+                const R t2 = wsHOld * cb * cb;
+                if (t1 < fac * t2) fac = t1 / t2;
+            }
+            const R hNew = fmax_(hMin, fmin_(hMax, h * fmax_(R(0.1), fac)));
+            wsErrOld = fmax_(err, uround);
+            cbErrOld = (err > uround) ? cb : cbrtU;  // errOld floored at uround
+            wsHOld = h;
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                ys.set(c, wa[c]);
+                f0.set(c, wb[c]);  // FSAL swap (rkc.cpp:276)
+            }
+            wsH = hNew;
+            state = kTop;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) y[c] = ys[c];
+    BODE_PHASE_FLUSH
+    st_out = st;
+}
+
+// rkc::driver (rkc.cpp:193-281) for a lane group's system (L > 1),
+// warp-uniform: every lane of the warp runs every phase that holds a shuffle
+// (power method, initial step, stage loop, error norm), each group doing or
+// discarding the work by its own state. Groups with `live` clear (finished,
+// frozen, or past the batch's end) ride along; G carries the full warp mask.
+template <class P, class R, int L>
+__device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double t_in,
+                                           double tEnd_in, R (&y)[P::N / L], const R* g,
+                                           const DevTol& tol, DevStats& st_out) {
+    static_assert(L > 1, "one lane per system: rkc_system_lane");
+    constexpr int C = P::N / L;
+    extern __shared__ double bode_smem[];
+    DevStats& st = *reinterpret_cast<DevStats*>(bode_smem + threadIdx.x * kRkcSmemStride<C>() + 2 * C);
+    stats_init(st);
+    const R tEnd(tEnd_in);
+    R t(t_in);
+    const R uround(tol.uround), absTol(tol.abs_tol), relTol(tol.rel_tol), kappa(tol.kappa);
+    const R hMax = fabs_(tEnd - t);
+    // stageCount's mMax (rkc.cpp:132-133), a per-call constant
+    long long mMax = llround(val(sqrt_(relTol / (R(10.0) * uround))));
+    if (mMax < 2) mMax = 2;
+
+    R wsErrOld(0.0), wsHOld(0.0), wsH(0.0), wsSpecRad(0.0);  // Workspace::reset
+    R cbErrOld(0.0);  // cbrt(wsErrOld), valid once a step was accepted
+    const R cbrtU = cbrt_(uround);  // cbrt(errOld) when errOld is floored at uround
+    long long numStep = 0;
+    // f0 and the power-method eigenvector live in this lane's shared-memory
+    // row (stride kRkcSmemStride<C>, odd => conflict-free): f0 is read once
+    // per element per stage, eig only by the power method; registers go to
+    // y and the two stage vectors.
+    double* const eig = bode_smem + threadIdx.x * kRkcSmemStride<C>();
+    F0Store<R, C, kRkcF0InSmem> f0(eig + C);
+    F0Store<R, C, kRkcYInSmem && (C >= 4)> ys(eig + 2 * C + 8);
+    {
+        R f[C];
+        P::template rhs<R, L>(G, t, y, g, f);
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            f0.set(c, f[c]);
+            eig[c] = val(f[c]);  // rkc.cpp:212
+            ys.set(c, y[c]);
+        }
+    }
+    ++st.rhs_evals;
+
+    int state = kTop;
+    R hMin(0.0), hNewRej(0.0);
+    // The scalar transitions (no shuffles): the tail of a rejection
+    // (rkc.cpp:255-264) and the top of the loop (rkc.cpp:223-229).
+    auto advance = [&]() {
+        if (live && state == kRejectTail) {
+            if (hNewRej < hMin) {  // freeze at the last accepted state (rkc.cpp:260-263)
+                st.underflow = 1;
+                live = false;
+            } else {
+                wsH = hNewRej;
+                state = kTop;
+            }
+        }
+        if (live && state == kTop) {
+            if (!(tEnd - t > uround * fabs_(tEnd))) {
+                live = false;
+            } else {
+                hMin = R(10.0) * uround * fmax_(fabs_(t), hMax);
+                if (R(1.1) * wsH >= fabs_(tEnd - t)) wsH = fabs_(tEnd - t);
+                state = (numStep % 25 == 0) ? kSrThenAttempt : kAttempt;
+            }
+        }
+    };
+    BODE_PHASE_DECL
+#pragma unroll 1
+    for (;;) {
+        BODE_PHASE_CTRL_END
+        advance();
+        if (!phase_any<L>(live)) break;
+        BODE_PHASE_MARK(-1);
+        const bool sr = live && (state == kSrThenAttempt || state == kSrThenRejectTail);
+        if (phase_any<L>(sr)) {
+            R sig;
+            const int it = power_method<P, R, L>(G, sr, t, ys, g, f0, hMax, eig, sig);
+            if (sr) {
+                wsSpecRad = sig;
+                ++st.spec_rad_evals;
+                st.rhs_evals += it;
+                state = (state == kSrThenAttempt) ? kAttempt : kRejectTail;
+            }
+            advance();  // a rejection's tail and the next top, in the same pass
+        }
+        BODE_PHASE_MARK(0);
+        const bool att = live && state == kAttempt;
+        if (!phase_any<L>(att)) continue;
+        // ---- attempt (groups with att set) ----
+        R wa[C], wb[C];
+        const bool init = att && wsH < uround;
+        if (phase_any<L>(init)) {  // initialStep (rkc.cpp:146-171), one RHS
+            R h = hMax;
+            if (wsSpecRad * h > R(1.0)) h = R(1.0) / wsSpecRad;
+            h = fmax_(h, hMin);
+#pragma unroll
+            for (int c = 0; c < C; ++c) wa[c] = ys[c] + h * f0[c];
+            P::template rhs<R, L>(G, t + h, wa, g, wb);
+            elementwise_quotients<R, C>([&](int c) { return wb[c] - f0[c]; },
+                                        [&](int c) { return absTol + relTol * fabs_(ys[c]); }, wa);
+#pragma unroll
+            for (int c = 0; c < C; ++c) wa[c] = wa[c] * wa[c];
+            const R sum = rkc_seq_sum<R, L, C>(G, wa, R(0.0));
+            if (init) {
+                const R err = h * sqrt_(sum / R(double(P::N)));
+                if (R(0.1) * h < hMax * sqrt_(err))
+                    h = fmax_(R(0.1) * h / sqrt_(err), hMin);
+                else
+                    h = hMax;
+                ++st.rhs_evals;
+                wsH = h;
+            }
+        }
+        // stageCount (rkc.cpp:131-144); s = 1 (no stages) for idle groups
+        long long s = 1;
+        if (att) {
+            const R sigma = isfinite_(wsSpecRad) ? wsSpecRad : R(0.0);
+            const R raw = sqrt_(R(1.54) * wsH * sigma + R(1.0));
+            s = (raw < R(double(mMax))) ? 1 + (long long)val(raw) : mMax + 1;
+            if (s > mMax) {
+                s = mMax;
+                wsH = (R(double(s)) * R(double(s)) - R(1.0)) / (R(1.54) * sigma);
+            }
+        }
+        const R h = wsH;
+        BODE_PHASE_MARK(1);
+        // ---- rkc::step (rkc.cpp:82-117) with coefficients (rkc.cpp:29-69)
+        // from the per-device table for s <= kRkcTableMaxS, else generated ----
+        const double* crow = (att && tol.rkc_coef != nullptr && s <= kRkcTableMaxS)
+                                 ? tol.rkc_coef + rkc_table_row(s)
+                                 : nullptr;
+        RkcCoefGen<R> gen;                // generator path only (local memory)
+        double chunk[5 * kRkcGenChunk];  // generator path only (local memory)
+        R mu1(0.0);
+        if (att) {
+            if (crow != nullptr) {
+                mu1 = R(crow[0]);
+            } else {
+                double m;
+                rkc_gen_start<R>(&gen, s, val(kappa), &m);
+                mu1 = R(m);
+            }
+        }
+        {
+            const R mu1h = mu1 * h;  // muTilde_1 * h
+#pragma unroll
+            for (int c = 0; c < C; ++c) wa[c] = ys[c] + mu1h * f0[c];
+        }
+        // the warp runs max(s) - 1 stages; w_j alternates between wa and wb
+        const long long sMax = (long long)__reduce_max_sync(0xffffffffu, (unsigned)s);
+        bool inA = true;  // current w_{j-1} lives in wa
+        int jc = 0;       // generator path: position in the current chunk
+#pragma unroll 1
+        for (long long j = 2; j <= sMax; ++j) {
+            const bool act = j <= s;
+            R muj(0.0), nuj(0.0), muTj(0.0), gTj(0.0), cjm1(0.0);
+            if (act) {
+                const double* e;
+                if (crow != nullptr) {
+                    e = crow + 1 + 5 * (j - 2);
+                } else {
+                    if (jc == 0)
+                        rkc_gen_chunk<R>(&gen, j,
+                                         j + kRkcGenChunk - 1 < s ? j + kRkcGenChunk - 1 : s,
+                                         chunk);
+                    e = chunk + 5 * jc;
+                    jc = (jc + 1 == kRkcGenChunk) ? 0 : jc + 1;
+                }
+                muj = R(e[0]);
+                nuj = R(e[1]);
+                muTj = R(e[2]);
+                gTj = R(e[3]);
+                cjm1 = R(e[4]);
+            }
+            const R tj = t + cjm1 * h;
+            if (inA)
+                rkc_stage<P, R, L>(G, act, tj, ys, f0, g, wa, wb, muj, nuj, muTj * h, gTj * h,
+                                   j == 2);
+            else
+                rkc_stage<P, R, L>(G, act, tj, ys, f0, g, wb, wa, muj, nuj, muTj * h, gTj * h,
+                                   false);
+            inA = !inA;
+        }
+        if ((s & 1) == 0) {  // the last stage (j = s even) wrote wb: y_trial -> wa
+#pragma unroll
+            for (int c = 0; c < C; ++c) wa[c] = wb[c];
+        }
+        BODE_PHASE_MARK(2);
+        P::template rhs<R, L>(G, t + h, wa, g, wb);  // f_trial (rkc.cpp:247)
+        // errorNorm (rkc.cpp:119-129)
+        R err;
+        {
+            R terms[C];
+            elementwise_quotients<R, C>(
+                [&](int c) { return R(0.8) * (ys[c] - wa[c]) + R(0.4) * h * (f0[c] + wb[c]); },
+                [&](int c) { return absTol + relTol * fmax_abs(ys[c], wa[c]); }, terms);
+#pragma unroll
+            for (int c = 0; c < C; ++c) terms[c] = terms[c] * terms[c];
+            err = sqrt_(rkc_seq_sum<R, L, C>(G, terms, R(0.0)) / R(double(P::N)));
+        }
+        BODE_PHASE_MARK(3);
+        BODE_PHASE_CTRL_BEGIN
+        if (!att) continue;
+        st.rhs_evals += s;  // s - 1 stages and f_trial
+        st.stages_total += s;
         const bool accepted = err <= R(1.0);
         // one cbrt call site (glibc's algorithm inline under EXACT) for both
         // controllers (rkc.cpp:177-190): cbrt(err) whenever err is finite

@@ -49,6 +49,11 @@ for p in $PARTS; do
         BODE_LANES=$1 BODE_MAXREG=$2 timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 1048576 --rkc-systems 1048576 > $OUT/bench_rkc_L$1_R$2.txt 2>&1; done
       for R in 96 80; do BODE_LANES=1 BODE_MAXREG=$R timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 1048576 --rkc-systems 1048576 > $OUT/bench_rkc_exp$R.txt 2>&1; done
       echo "ab_rkc rc=$?" >> $OUT/status.txt ;;
+    ab_lib)  # this build against paper_1611_02274_b200/lib/ab/libbode_base.so, alternating
+      I=0; for L in base new base new; do I=$((I+1))
+        if [ $L = base ]; then LP=$PWD/paper_1611_02274_b200/lib/ab/libbode_base.so; else LP=; fi
+        BODE_LIB_PATH=$LP timeout 600 python bench.py --no-e2e --no-cpu --steps 5 > $OUT/bench_ab${I}_$L.txt 2>&1; done
+      echo "ab_lib rc=$?" >> $OUT/status.txt ;;
     ncu_late)
       for W in 0 9; do
       timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:Pleiades, double" \
