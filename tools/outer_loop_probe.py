@@ -39,9 +39,12 @@ def main():
         return (time.perf_counter() - t) * 1e3
 
     ol(0.2, 0.7)
-    for thr in (0.7, 0.0):
-        out[f"outer10_thr{thr}_ms"] = ol(1.0, thr)
-        out[f"outer1_thr{thr}_ms"] = ol(0.1, thr)
+    thrs = [float(x) for x in os.environ.get("PROBE_THRESHOLDS", "0.7 0.0").split()]
+    for rep in range(int(os.environ.get("PROBE_REPS", "1"))):
+        for thr in thrs:
+            out.setdefault(f"outer10_thr{thr}_ms", []).append(ol(1.0, thr))
+            if rep == 0:
+                out[f"outer1_thr{thr}_ms"] = ol(0.1, thr)
     print(json.dumps(out))
 
 
