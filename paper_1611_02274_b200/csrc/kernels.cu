@@ -34,6 +34,7 @@ const KernelEntry* kernel_table(int* count) {
         BODE_BOTH_ARITH(Heat<64>, 4, 1, false, 1),
         BODE_BOTH_ARITH_R(Heat<64>, 4, 1, false, 1, 168),
         BODE_BOTH_ARITH_R(Heat<64>, 8, 1, false, 1, 168),
+        BODE_BOTH_ARITH_R(Heat<64>, 8, 1, false, 1, 112),
         BODE_BOTH_ARITH_R(Heat<64>, 8, 1, false, 1, 96),
         BODE_BOTH_ARITH_R(Heat<64>, 16, 1, false, 1, 96),
         BODE_BOTH_ARITH_R(Heat<64>, 16, 1, false, 1, 128),

@@ -748,22 +748,26 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
             const bool act = j <= s;
             R muj(0.0), nuj(0.0), muTj(0.0), gTj(0.0), cjm1(0.0);
             if (act) {
-                const double* e;
-                if (crow != nullptr) {
-                    e = crow + 1 + 5 * (j - 2);
-                } else {
+                if (crow != nullptr) {  // the device table: read-only global loads
+                    const double* e = crow + 1 + 5 * (j - 2);
+                    muj = R(__ldg(e));
+                    nuj = R(__ldg(e + 1));
+                    muTj = R(__ldg(e + 2));
+                    gTj = R(__ldg(e + 3));
+                    cjm1 = R(__ldg(e + 4));
+                } else {  // the generator's chunk in local memory
                     if (jc == 0)
                         rkc_gen_chunk<R>(&gen, j,
                                          j + kRkcGenChunk - 1 < s ? j + kRkcGenChunk - 1 : s,
                                          chunk);
-                    e = chunk + 5 * jc;
+                    const double* e = chunk + 5 * jc;
+                    muj = R(e[0]);
+                    nuj = R(e[1]);
+                    muTj = R(e[2]);
+                    gTj = R(e[3]);
+                    cjm1 = R(e[4]);
                     jc = (jc + 1 == kRkcGenChunk) ? 0 : jc + 1;
                 }
-                muj = R(e[0]);
-                nuj = R(e[1]);
-                muTj = R(e[2]);
-                gTj = R(e[3]);
-                cjm1 = R(e[4]);
             }
             const R tj = t + cjm1 * h;
             if (inA)

@@ -306,7 +306,7 @@ def test_very_stiff_generator_path_bitwise(gpu, oracle):
     assert per_step.max() > 160, per_step.max()
 
 
-@pytest.mark.parametrize("env", [("4", "255"), ("4", "168"), ("8", "168"), ("8", "128"), ("8", "96"), ("16", "96"), ("16", "128")])
+@pytest.mark.parametrize("env", [("4", "255"), ("4", "168"), ("8", "168"), ("8", "128"), ("8", "112"), ("8", "96"), ("16", "96"), ("16", "128")])
 def test_heat64_lane_variants_bitwise(gpu, oracle, env):
     """Every compiled heat64 RKC instance (lanes per system x register cap,
     selected with BODE_LANES / BODE_MAXREG) gives the oracle's bits."""
@@ -414,3 +414,27 @@ def oracle_outer_sample(prob, solver, y0, g, num, idx):
     sub_y = np.ascontiguousarray(y0.reshape(prob.dim, num)[:, idx]).reshape(-1)
     sub_g = np.ascontiguousarray(g.reshape(prob.param_dim, num)[:, idx]).reshape(-1)
     return Oracle().outer_loop(prob, solver, 0.0, 1.0, 0.1, sub_y, sub_g)
+
+
+def test_heat64_mixed_groups_per_warp_bitwise(gpu, oracle):
+    """The lane-group RKC driver is warp-uniform (rkc.cuh rkc_system): the four
+    heat64 systems sharing a warp run every phase together and keep or drop
+    the results by their own state. Neighbours here differ in amplitude (so in
+    step sizes, stage counts and rejections), include all-zero systems
+    (degenerate power method), a NaN system (underflow freeze) and a ragged
+    last warp; every system must still be bitwise the oracle's."""
+    num = 4 * 64 + 3
+    y0 = perturb(heat_ic(64), 0.01, 99, num).reshape(64, num)
+    scales = [1.0, 0.0, 1e-150, 1e3, 1e-6, -1.0, 5e2]
+    for i in range(num):
+        y0[:, i] *= scales[i % len(scales)]
+    y0[5, 10] = np.nan
+    y0 = np.ascontiguousarray(y0).reshape(-1)
+    prob = A.make_problem(A.HEAT, 64)
+    y, st = run_gpu(prob, A.SOLVER_RKC, y0, None, "exact")
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKC, 0.0, 1.0, 0.1, y0)
+    assert np.array_equal(y.view(np.uint64), yo.view(np.uint64))
+    for k in COUNTS + ("stages_total",):
+        assert np.array_equal(st[k], so[k]), k
+    assert st["underflow"][10] == 1
+    assert len(set(st["rhs_evals"].tolist())) > 3  # the groups really did differ
