@@ -13,6 +13,9 @@
 //       // this lane's slice dy[c] = f(t, y)[G.lane * (N / L) + c] of the RHS;
 //       // y[c] likewise; g[0..P) are the system's parameters. Lanes of the
 //       // group exchange halo values with G.from / G.from_prev / G.from_next.
+//       // Every lane must reach each of these calls (no data-dependent
+//       // branch around them): RKC on lane groups calls rhs warp-uniformly
+//       // with a full-warp shuffle mask (rkc.cuh).
 //       template <class R, int L>
 //       __device__ static void rhs(const bode::Group<L>& G, R t, const R (&y)[N / L],
 //                                  const R* g, R (&dy)[N / L]);

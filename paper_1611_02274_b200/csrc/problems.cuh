@@ -42,8 +42,11 @@ struct Group {
         for (int o = L / 2; o > 0; o /= 2) v = fmax(v, __shfl_xor_sync(mask, v, o, L));
         return v;
     }
+    // any lane of this group (the vote spans `mask`, the answer the group only)
     __device__ __forceinline__ bool any(bool b) const {
-        return (__ballot_sync(mask, b) & mask) != 0u;
+        const unsigned own = (L == 32) ? 0xffffffffu
+                                       : (((1u << L) - 1u) << ((threadIdx.x & 31) & ~(L - 1)));
+        return (__ballot_sync(mask, b) & own) != 0u;
     }
 };
 
