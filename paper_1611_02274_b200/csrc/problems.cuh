@@ -115,7 +115,7 @@ struct Pleiades {
                     const R dy = w[7 + j] - w[7 + i];
                     const double r2 = val(dx * dx + dy * dy);
                     const double d = __dmul_rn(r2, sqrt_rn_bf(r2));
-                    ok = ok && in_safe_range(r2) && in_safe_range(d);
+                    ok = ok & r3_in_safe_range(r2);
                     inv[p] = rcp_rn_bf(d);
                 }
             if (!ok) {  // rare: some operand outside [2^-400, 2^400] (or NaN/Inf)

@@ -60,7 +60,7 @@ __device__ __forceinline__ void pleiades_accel_pair(const Group<2>& G, const R* 
         if constexpr (is_exact<R>::value) {  // straight-line IEEE ops (arith.cuh)
             const double r2 = __dadd_rn(own, oth);
             const double d = __dmul_rn(r2, sqrt_rn_bf(r2));
-            ok = ok && in_safe_range(r2) && in_safe_range(d);
+            ok = ok & r3_in_safe_range(r2);
             r2s[k] = r2;
             mine[k] = rcp_rn_bf(d);
         } else {

@@ -438,3 +438,21 @@ def test_heat64_mixed_groups_per_warp_bitwise(gpu, oracle):
         assert np.array_equal(st[k], so[k]), k
     assert st["underflow"][10] == 1
     assert len(set(st["rhs_evals"].tolist())) > 3  # the groups really did differ
+
+
+@pytest.mark.parametrize("scale", [2.0 ** 140, 2.0 ** -140])
+def test_pleiades_exact_outside_fast_range_bitwise(gpu, oracle, scale):
+    """EXACT Pleiades evaluates 1/(r2 sqrt r2) on a straight-line path only
+    for r2 in [2^-266, 2^266) (arith.cuh r3_in_safe_range) and falls back to
+    the IEEE intrinsics otherwise. Positions scaled by 2^+-140 put every r2
+    outside that band; the results must still be the oracle's bits."""
+    num = 96
+    y0 = perturb(PLEIADES_IC, 0.01, 3, num).reshape(28, num)
+    y0[:14] *= scale
+    y0 = np.ascontiguousarray(y0).reshape(-1)
+    prob = A.make_problem(A.PLEIADES)
+    y, st = run_gpu(prob, A.SOLVER_RKCK, y0, None, "exact")
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKCK, 0.0, 1.0, 0.1, y0)
+    assert np.array_equal(y.view(np.uint64), yo.view(np.uint64))
+    for k in COUNTS:
+        assert np.array_equal(st[k], so[k]), k
