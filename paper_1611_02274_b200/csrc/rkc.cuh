@@ -257,6 +257,19 @@ __device__ __forceinline__ bool phase_any(bool b) {
         return b;
 }
 
+// x / N for the mean in the RMS norms (rkc.cpp:128, :164). For N a power of
+// two, x * 2^-k rounds the same real number, so the product is bitwise the
+// quotient (subnormals, infinities and NaN included) without a division.
+template <int N, class R>
+__device__ __forceinline__ R div_by_dim(R x) {
+    if constexpr (N == 1)
+        return x;
+    else if constexpr ((N & (N - 1)) == 0)
+        return x * R(1.0 / N);
+    else
+        return x / R(double(N));
+}
+
 // Power method (spectral_radius.cpp:17-85) for the groups with `on` set; the
 // other groups of the warp run alongside on their own state and discard the
 // result. Returns sigma (with the 1.2 safety factor) and the number of
@@ -452,7 +465,7 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
 #pragma unroll
             for (int c = 0; c < C; ++c) wa[c] = wa[c] * wa[c];
             const R sum = rkc_seq_sum<R, L, C>(G, wa, R(0.0));
-            const R err = h * sqrt_(sum / R(double(P::N)));
+            const R err = h * sqrt_(div_by_dim<P::N>(sum));
             if (R(0.1) * h < hMax * sqrt_(err))
                 h = fmax_(R(0.1) * h / sqrt_(err), hMin);
             else
@@ -542,7 +555,7 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
                 [&](int c) { return absTol + relTol * fmax_abs(ys[c], wa[c]); }, terms);
 #pragma unroll
             for (int c = 0; c < C; ++c) terms[c] = terms[c] * terms[c];
-            err = sqrt_(rkc_seq_sum<R, L, C>(G, terms, R(0.0)) / R(double(P::N)));
+            err = sqrt_(div_by_dim<P::N>(rkc_seq_sum<R, L, C>(G, terms, R(0.0))));
         }
         BODE_PHASE_MARK(3);
         BODE_PHASE_CTRL_BEGIN
@@ -695,7 +708,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
             for (int c = 0; c < C; ++c) wa[c] = wa[c] * wa[c];
             const R sum = rkc_seq_sum<R, L, C>(G, wa, R(0.0));
             if (init) {
-                const R err = h * sqrt_(sum / R(double(P::N)));
+                const R err = h * sqrt_(div_by_dim<P::N>(sum));
                 if (R(0.1) * h < hMax * sqrt_(err))
                     h = fmax_(R(0.1) * h / sqrt_(err), hMin);
                 else
@@ -793,7 +806,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
                 [&](int c) { return absTol + relTol * fmax_abs(ys[c], wa[c]); }, terms);
 #pragma unroll
             for (int c = 0; c < C; ++c) terms[c] = terms[c] * terms[c];
-            err = sqrt_(rkc_seq_sum<R, L, C>(G, terms, R(0.0)) / R(double(P::N)));
+            err = sqrt_(div_by_dim<P::N>(rkc_seq_sum<R, L, C>(G, terms, R(0.0))));
         }
         BODE_PHASE_MARK(3);
         BODE_PHASE_CTRL_BEGIN
