@@ -376,6 +376,102 @@ __device__ __forceinline__ void rkc_stage(const Group<L>& G, bool act, R tj, con
 
 enum RkcState { kTop = 0, kSrThenAttempt = 1, kAttempt = 2, kSrThenRejectTail = 3, kRejectTail = 4 };
 
+// initialStep (rkc.cpp:146-171): one RHS at t + h on y + h f0 and the RMS
+// of (f1 - f0) / (absTol + relTol |y|); wa and wb are scratch. Every lane of
+// a group (of the warp, for L > 1) must call it; groups with `on` clear skip
+// the scalar tail and get a meaningless value.
+template <class P, class R, int L, class Y, class F0>
+__device__ __forceinline__ R rkc_initial_step(const Group<L>& G, bool on, R t, const Y& ys,
+                                              const F0& f0, const R* g, R wsSpecRad, R hMin,
+                                              R hMax, R absTol, R relTol, R (&wa)[P::N / L],
+                                              R (&wb)[P::N / L]) {
+    constexpr int C = P::N / L;
+    R h = hMax;
+    if (wsSpecRad * h > R(1.0)) h = R(1.0) / wsSpecRad;
+    h = fmax_(h, hMin);
+#pragma unroll
+    for (int c = 0; c < C; ++c) wa[c] = ys[c] + h * f0[c];
+    P::template rhs<R, L>(G, t + h, wa, g, wb);
+    elementwise_quotients<R, C>([&](int c) { return wb[c] - f0[c]; },
+                                [&](int c) { return absTol + relTol * fabs_(ys[c]); }, wa);
+#pragma unroll
+    for (int c = 0; c < C; ++c) wa[c] = wa[c] * wa[c];
+    const R sum = rkc_seq_sum<R, L, C>(G, wa, R(0.0));
+    if (!on) return hMax;
+    const R err = h * sqrt_(div_by_dim<P::N>(sum));
+    if (R(0.1) * h < hMax * sqrt_(err))
+        return fmax_(R(0.1) * h / sqrt_(err), hMin);
+    return hMax;
+}
+
+// errorNorm (rkc.cpp:119-129) of the trial y1 = wa with f(t + h, y1) = wb.
+template <class P, class R, int L, class Y, class F0>
+__device__ __forceinline__ R rkc_error_norm(const Group<L>& G, const Y& ys, const R (&y1)[P::N / L],
+                                            const F0& f0, const R (&f1)[P::N / L], R h, R absTol,
+                                            R relTol) {
+    constexpr int C = P::N / L;
+    R terms[C];
+    elementwise_quotients<R, C>(
+        [&](int c) { return R(0.8) * (ys[c] - y1[c]) + R(0.4) * h * (f0[c] + f1[c]); },
+        [&](int c) { return absTol + relTol * fmax_abs(ys[c], y1[c]); }, terms);
+#pragma unroll
+    for (int c = 0; c < C; ++c) terms[c] = terms[c] * terms[c];
+    return sqrt_(div_by_dim<P::N>(rkc_seq_sum<R, L, C>(G, terms, R(0.0))));
+}
+
+// stageCount (rkc.cpp:131-144) for the spectral radius estimate wsSpecRad
+// (non-finite -> 0, rkc.cpp:240); shortens wsH when s would exceed mMax.
+template <class R>
+__device__ __forceinline__ long long rkc_stage_count(R wsSpecRad, long long mMax, R& wsH) {
+    const R sigma = isfinite_(wsSpecRad) ? wsSpecRad : R(0.0);
+    const R raw = sqrt_(R(1.54) * wsH * sigma + R(1.0));
+    long long s = (raw < R(double(mMax))) ? 1 + (long long)val(raw) : mMax + 1;
+    if (s > mMax) {
+        s = mMax;
+        wsH = (R(double(s)) * R(double(s)) - R(1.0)) / (R(1.54) * sigma);
+    }
+    return s;
+}
+
+// The accept/reject decision and both step-size controllers after an attempt
+// (rkc.cpp:252-275, nextStepAccepted/Rejected :173-191) on the driver's
+// Workspace (wsErrOld, wsHOld, wsH) plus cbErrOld = cbrt(wsErrOld). Returns
+// whether the step was accepted; the caller then advances y and f0 (FSAL).
+template <class R>
+__device__ __forceinline__ bool rkc_finish_attempt(R err, R h, R hMin, R hMax, R uround, R cbrtU,
+                                                   double p1, DevStats& st, R& t,
+                                                   long long& numStep, R& wsErrOld, R& cbErrOld,
+                                                   R& wsHOld, R& wsH, R& hNewRej) {
+    // one cbrt call site (glibc's algorithm inline under EXACT) for both
+    // controllers (rkc.cpp:177-190): cbrt(err) whenever err is finite
+    const R cb = isfinite_(err) ? cbrt_(err) : R(1.0);
+    if (!(err <= R(1.0))) {
+        ++st.steps_rejected;
+        hNewRej = isfinite_(err) ? R(0.8) * h / cb : R(p1) * h;
+        return false;
+    }
+    t += h;
+    ++numStep;
+    stats_accept(st, val(h));
+    const bool firstAccepted = wsHOld < uround;
+    // nextStepAccepted (rkc.cpp:173-187); cbrt(errOld) is the previous
+    // accepted step's cbrt(err) unless errOld was floored at uround
+    R fac(10.0);
+    if (firstAccepted) {
+        if (R(0.8) < fac * cb) fac = R(0.8) / cb;
+    } else {
+        const R t1 = R(0.8) * h * cbErrOld;
+        const R t2 = wsHOld * cb * cb;
+        if (t1 < fac * t2) fac = t1 / t2;
+    }
+    const R hNew = fmax_(hMin, fmin_(hMax, h * fmax_(R(0.1), fac)));
+    wsErrOld = fmax_(err, uround);
+    cbErrOld = (err > uround) ? cb : cbrtU;  // errOld floored at uround
+    wsHOld = h;
+    wsH = hNew;
+    return true;
+}
+
 // rkc::driver (rkc.cpp:193-281) with one lane per system: the same state
 // machine as rkc_system below, each lane branching on its own state. (The
 // warp-uniform form measured 5% slower here: with no shuffles to save, its
@@ -454,36 +550,11 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
         // ---- state == kAttempt ----
         R wa[C], wb[C];
         if (wsH < uround) {  // initialStep (rkc.cpp:146-171), one RHS
-            R h = hMax;
-            if (wsSpecRad * h > R(1.0)) h = R(1.0) / wsSpecRad;
-            h = fmax_(h, hMin);
-#pragma unroll
-            for (int c = 0; c < C; ++c) wa[c] = ys[c] + h * f0[c];
-            P::template rhs<R, L>(G, t + h, wa, g, wb);
-            elementwise_quotients<R, C>([&](int c) { return wb[c] - f0[c]; },
-                                        [&](int c) { return absTol + relTol * fabs_(ys[c]); }, wa);
-#pragma unroll
-            for (int c = 0; c < C; ++c) wa[c] = wa[c] * wa[c];
-            const R sum = rkc_seq_sum<R, L, C>(G, wa, R(0.0));
-            const R err = h * sqrt_(div_by_dim<P::N>(sum));
-            if (R(0.1) * h < hMax * sqrt_(err))
-                h = fmax_(R(0.1) * h / sqrt_(err), hMin);
-            else
-                h = hMax;
+            wsH = rkc_initial_step<P, R, L>(G, true, t, ys, f0, g, wsSpecRad, hMin, hMax, absTol,
+                                            relTol, wa, wb);
             ++st.rhs_evals;
-            wsH = h;
         }
-        const R sigma = isfinite_(wsSpecRad) ? wsSpecRad : R(0.0);
-        // stageCount (rkc.cpp:131-144)
-        long long s;
-        {
-            const R raw = sqrt_(R(1.54) * wsH * sigma + R(1.0));
-            s = (raw < R(double(mMax))) ? 1 + (long long)val(raw) : mMax + 1;
-            if (s > mMax) {
-                s = mMax;
-                wsH = (R(double(s)) * R(double(s)) - R(1.0)) / (R(1.54) * sigma);
-            }
-        }
+        const long long s = rkc_stage_count(wsSpecRad, mMax, wsH);
         const R h = wsH;
         BODE_PHASE_MARK(1);
         // ---- rkc::step (rkc.cpp:82-117) with coefficients (rkc.cpp:29-69)
@@ -546,53 +617,19 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
         BODE_PHASE_MARK(2);
         P::template rhs<R, L>(G, t + h, wa, g, wb);  // f_trial (rkc.cpp:247)
         ++st.rhs_evals;
-        // errorNorm (rkc.cpp:119-129)
-        R err;
-        {
-            R terms[C];
-            elementwise_quotients<R, C>(
-                [&](int c) { return R(0.8) * (ys[c] - wa[c]) + R(0.4) * h * (f0[c] + wb[c]); },
-                [&](int c) { return absTol + relTol * fmax_abs(ys[c], wa[c]); }, terms);
-#pragma unroll
-            for (int c = 0; c < C; ++c) terms[c] = terms[c] * terms[c];
-            err = sqrt_(div_by_dim<P::N>(rkc_seq_sum<R, L, C>(G, terms, R(0.0))));
-        }
+        const R err = rkc_error_norm<P, R, L>(G, ys, wa, f0, wb, h, absTol, relTol);
         BODE_PHASE_MARK(3);
         BODE_PHASE_CTRL_BEGIN
-        const bool accepted = err <= R(1.0);
-        // one cbrt call site (glibc's algorithm inline under EXACT) for both
-        // controllers (rkc.cpp:177-190): cbrt(err) whenever err is finite
-        const R cb = isfinite_(err) ? cbrt_(err) : R(1.0);
-        if (!accepted) {
-            ++st.steps_rejected;
-            hNewRej = isfinite_(err) ? R(0.8) * h / cb : R(tol.p1) * h;
-            state = kSrThenRejectTail;
-        } else {
-            t += h;
-            ++numStep;
-            stats_accept(st, val(h));
-            const bool firstAccepted = wsHOld < uround;
-            // nextStepAccepted (rkc.cpp:173-187); cbrt(errOld) is the previous
-            // accepted step's cbrt(err) unless errOld was floored at uround
-            R fac(10.0);
-            if (firstAccepted) {
-                if (R(0.8) < fac * cb) fac = R(0.8) / cb;
-            } else {
-                const R t1 = R(0.8) * h * cbErrOld;
-                const R t2 = wsHOld * cb * cb;
-                if (t1 < fac * t2) fac = t1 / t2;
-            }
-            const R hNew = fmax_(hMin, fmin_(hMax, h * fmax_(R(0.1), fac)));
-            wsErrOld = fmax_(err, uround);
-            cbErrOld = (err > uround) ? cb : cbrtU;  // errOld floored at uround
-            wsHOld = h;
+        if (rkc_finish_attempt<R>(err, h, hMin, hMax, uround, cbrtU, tol.p1, st, t, numStep,
+                                  wsErrOld, cbErrOld, wsHOld, wsH, hNewRej)) {
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 ys.set(c, wa[c]);
                 f0.set(c, wb[c]);  // FSAL swap (rkc.cpp:276)
             }
-            wsH = hNew;
             state = kTop;
+        } else {
+            state = kSrThenRejectTail;
         }
     }
 #pragma unroll
@@ -696,38 +733,15 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
         R wa[C], wb[C];
         const bool init = att && wsH < uround;
         if (phase_any<L>(init)) {  // initialStep (rkc.cpp:146-171), one RHS
-            R h = hMax;
-            if (wsSpecRad * h > R(1.0)) h = R(1.0) / wsSpecRad;
-            h = fmax_(h, hMin);
-#pragma unroll
-            for (int c = 0; c < C; ++c) wa[c] = ys[c] + h * f0[c];
-            P::template rhs<R, L>(G, t + h, wa, g, wb);
-            elementwise_quotients<R, C>([&](int c) { return wb[c] - f0[c]; },
-                                        [&](int c) { return absTol + relTol * fabs_(ys[c]); }, wa);
-#pragma unroll
-            for (int c = 0; c < C; ++c) wa[c] = wa[c] * wa[c];
-            const R sum = rkc_seq_sum<R, L, C>(G, wa, R(0.0));
+            const R h0 = rkc_initial_step<P, R, L>(G, init, t, ys, f0, g, wsSpecRad, hMin, hMax,
+                                                   absTol, relTol, wa, wb);
             if (init) {
-                const R err = h * sqrt_(div_by_dim<P::N>(sum));
-                if (R(0.1) * h < hMax * sqrt_(err))
-                    h = fmax_(R(0.1) * h / sqrt_(err), hMin);
-                else
-                    h = hMax;
                 ++st.rhs_evals;
-                wsH = h;
+                wsH = h0;
             }
         }
-        // stageCount (rkc.cpp:131-144); s = 1 (no stages) for idle groups
-        long long s = 1;
-        if (att) {
-            const R sigma = isfinite_(wsSpecRad) ? wsSpecRad : R(0.0);
-            const R raw = sqrt_(R(1.54) * wsH * sigma + R(1.0));
-            s = (raw < R(double(mMax))) ? 1 + (long long)val(raw) : mMax + 1;
-            if (s > mMax) {
-                s = mMax;
-                wsH = (R(double(s)) * R(double(s)) - R(1.0)) / (R(1.54) * sigma);
-            }
-        }
+        // s = 1 (no stages) for idle groups
+        const long long s = att ? rkc_stage_count(wsSpecRad, mMax, wsH) : 1;
         const R h = wsH;
         BODE_PHASE_MARK(1);
         // ---- rkc::step (rkc.cpp:82-117) with coefficients (rkc.cpp:29-69)
@@ -797,56 +811,22 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
         }
         BODE_PHASE_MARK(2);
         P::template rhs<R, L>(G, t + h, wa, g, wb);  // f_trial (rkc.cpp:247)
-        // errorNorm (rkc.cpp:119-129)
-        R err;
-        {
-            R terms[C];
-            elementwise_quotients<R, C>(
-                [&](int c) { return R(0.8) * (ys[c] - wa[c]) + R(0.4) * h * (f0[c] + wb[c]); },
-                [&](int c) { return absTol + relTol * fmax_abs(ys[c], wa[c]); }, terms);
-#pragma unroll
-            for (int c = 0; c < C; ++c) terms[c] = terms[c] * terms[c];
-            err = sqrt_(div_by_dim<P::N>(rkc_seq_sum<R, L, C>(G, terms, R(0.0))));
-        }
+        const R err = rkc_error_norm<P, R, L>(G, ys, wa, f0, wb, h, absTol, relTol);
         BODE_PHASE_MARK(3);
         BODE_PHASE_CTRL_BEGIN
         if (!att) continue;
         st.rhs_evals += s;  // s - 1 stages and f_trial
         st.stages_total += s;
-        const bool accepted = err <= R(1.0);
-        // one cbrt call site (glibc's algorithm inline under EXACT) for both
-        // controllers (rkc.cpp:177-190): cbrt(err) whenever err is finite
-        const R cb = isfinite_(err) ? cbrt_(err) : R(1.0);
-        if (!accepted) {
-            ++st.steps_rejected;
-            hNewRej = isfinite_(err) ? R(0.8) * h / cb : R(tol.p1) * h;
-            state = kSrThenRejectTail;
-        } else {
-            t += h;
-            ++numStep;
-            stats_accept(st, val(h));
-            const bool firstAccepted = wsHOld < uround;
-            // nextStepAccepted (rkc.cpp:173-187); cbrt(errOld) is the previous
-            // accepted step's cbrt(err) unless errOld was floored at uround
-            R fac(10.0);
-            if (firstAccepted) {
-                if (R(0.8) < fac * cb) fac = R(0.8) / cb;
-            } else {
-                const R t1 = R(0.8) * h * cbErrOld;
-                const R t2 = wsHOld * cb * cb;
-                if (t1 < fac * t2) fac = t1 / t2;
-            }
-            const R hNew = fmax_(hMin, fmin_(hMax, h * fmax_(R(0.1), fac)));
-            wsErrOld = fmax_(err, uround);
-            cbErrOld = (err > uround) ? cb : cbrtU;  // errOld floored at uround
-            wsHOld = h;
+        if (rkc_finish_attempt<R>(err, h, hMin, hMax, uround, cbrtU, tol.p1, st, t, numStep,
+                                  wsErrOld, cbErrOld, wsHOld, wsH, hNewRej)) {
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 ys.set(c, wa[c]);
                 f0.set(c, wb[c]);  // FSAL swap (rkc.cpp:276)
             }
-            wsH = hNew;
             state = kTop;
+        } else {
+            state = kSrThenRejectTail;
         }
     }
 #pragma unroll
