@@ -404,6 +404,25 @@ def main():
         e2e = {"value": world * num * args.steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": num * 28 * 8, "d2h_bytes_per_step": num * (28 * 8 + 64),
                "ms_per_step": e2e_s / args.steps * 1e3, "pinned_host": True}
+        # the paper's intDriver(t, tEnd, numODE, gGlobal, yGlobal) exactly: y in and
+        # out, no per-system stats requested (stats = NULL), same windows
+        yh.copy_(torch.from_numpy(y0))
+        if dist:
+            dist.barrier()
+        t = time.perf_counter()
+        for k in range(args.steps):
+            P.api.check(L.bode_int_driver(ctypes.byref(prob), 0, ar, 0.0 + (k % 10) * 0.1,
+                                          0.0 + (k % 10 + 1) * 0.1, num, None, yp,
+                                          ctypes.byref(tol), None, 1))
+        pp_s = time.perf_counter() - t
+        if dist:
+            tt = torch.tensor([pp_s], device=red_dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            pp_s = float(tt.item())
+        e2e["paper_protocol_no_stats"] = {
+            "value": world * num * args.steps / pp_s, "unit": UNIT,
+            "h2d_bytes_per_step": num * 28 * 8, "d2h_bytes_per_step": num * 28 * 8,
+            "ms_per_step": pp_s / args.steps * 1e3}
         # the same 10-window protocol through bode_outer_loop (batchode::outerLoop's
         # drop-in): host buffers in and out, the state resident in HBM between
         # windows, so one H2D and one D2H per call instead of per window
