@@ -51,13 +51,18 @@ struct Brusselator {
 
 }  // namespace bode
 
-// n = 32 grid points (dim 64): RKC with 8 lanes per system at 128 registers
-// (16 warps/SM); RKCK candidates (lanes x register cap) registered in
+// n = 32 grid points (dim 64): RKC with 4 lanes per system, uncapped (8 warps/SM);
+// RKCK candidates (lanes x register cap) registered in
 // preference order, selectable with BODE_LANES / BODE_MAXREG for A/B runs
 namespace {
 using Bru = bode::Brusselator<32>;
 const int bode_registered_brusselator32 = [] {
     static const bode::KernelEntry e[] = {
+        // RKC EXACT measured (2^20 systems, 5 windows, system-windows/s): 4 lanes
+        // uncapped 6.33e7, 8 @128 6.07e7, 4 @168 5.83e7, 8 @168 5.58e7 (r01cq);
+        // the heavier reaction RHS and 3 instead of 7 sum hand-offs favour 4 lanes
+        bode::make_entry<Bru, bode::xd, 4, 1, false, 0>(BODE_PROBLEM_BRUSSELATOR, BODE_ARITH_EXACT),
+        bode::make_entry<Bru, double, 4, 1, false, 0>(BODE_PROBLEM_BRUSSELATOR, BODE_ARITH_FAST),
         bode::make_entry<Bru, bode::xd, 8, 1, false, 128>(BODE_PROBLEM_BRUSSELATOR, BODE_ARITH_EXACT),
         bode::make_entry<Bru, double, 8, 1, false, 128>(BODE_PROBLEM_BRUSSELATOR, BODE_ARITH_FAST),
         // RKCK FAST measured (2^20 systems, 5 windows, FP64 fraction): 8 lanes @128

@@ -140,3 +140,30 @@ def test_second_order_user_problem_fast_rkn(user_lib, ref):
     assert sysrel(y, yo, num, 30).max() <= 1e-13
     for k in ("steps_accepted", "steps_rejected", "rhs_evals"):
         assert np.array_equal(st[k], so[k]), k
+
+
+@pytest.mark.parametrize("env", [("4", "255"), ("8", "128")])
+def test_brusselator_rkc_lane_variants_bitwise(gpu, ref, env):
+    """Both compiled RKC Brusselator shapes (4 lanes uncapped, the default, and
+    8 lanes at 128 registers; BODE_LANES / BODE_MAXREG) give the reference's bits."""
+    import os
+    import subprocess
+    import sys
+    num = 512
+    code = ("import sys; sys.path.insert(0, 'tests'); import numpy as np;"
+            "from test_gpu_user_problems import run; from golden_cases import brusselator_ic,"
+            " brusselator_params, perturb; from paper_1611_02274_b200 import _abi as A;"
+            "p = A.make_problem(A.BRUSSELATOR); y0 = perturb(brusselator_ic(32), 0.01, 11, %d);"
+            "g = brusselator_params(%d, 0.02, 0.5);"
+            "y, st = run(p, A.SOLVER_RKC, y0, g, 'exact'); np.save(sys.argv[1], y)" % (num, num))
+    out = os.path.join(os.environ.get("TMPDIR", "/tmp"), f"bru_variant_{env[0]}_{env[1]}.npy")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code, out], cwd=repo, capture_output=True, text=True,
+                       env=dict(os.environ, BODE_LANES=env[0], BODE_MAXREG=env[1]))
+    assert r.returncode == 0, r.stderr[-2000:]
+    prob = A.make_problem(A.BRUSSELATOR)
+    y0 = perturb(brusselator_ic(32), 0.01, 11, num)
+    g = brusselator_params(num, 0.02, 0.5)
+    rc, yo, so, _ = ref.outer_loop(prob, A.SOLVER_RKC, 0.0, 1.0, 0.1, y0, g)
+    assert rc == 0
+    assert np.array_equal(np.load(out).view(np.uint64), yo.view(np.uint64))
