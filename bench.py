@@ -236,11 +236,13 @@ def _parse_cpulist(text):
 
 
 def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warmup, stream,
-                   repack=False):
+                   repack=False, presort_row=None):
     """K windows on HBM-resident state; per-launch CUDA events on `stream`.
     repack: after the first timed window, re-pack the batch by the cost each
     system showed (bode_repack_by_cost), and restore the caller's order after
-    the last (bode_unpack); both inside the timed region."""
+    the last (bode_unpack); both inside the timed region. presort_row: sort by
+    |g[presort_row]| before the first window instead (bode_repack_by_param)."""
+    reorder = repack or presort_row is not None
     num = y0.size // dim
     yd = torch.from_numpy(y0).to("cuda")
     gd = torch.from_numpy(g0).to("cuda") if g0 is not None else None
@@ -255,12 +257,12 @@ def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warm
                             yd.data_ptr(), tol, st.data_ptr(), merge, stream.cuda_stream)
 
     L = P.lib()
-    order = torch.empty(num, dtype=torch.int64, device="cuda") if repack else None
+    order = torch.empty(num, dtype=torch.int64, device="cuda") if reorder else None
     cprob = A.Problem(kind=prob.kind, dim=prob.dim, param_dim=prob.param_dim, reserved=0)
     with torch.cuda.stream(stream):
         for k in range(warmup):
             window(k, False)
-            if repack:  # warm the sort/gather kernels and the scratch allocation
+            if reorder:  # warm the sort/gather kernels and the scratch allocation
                 P.api.check(L.bode_order_init(ctypes.c_void_p(order.data_ptr()), num,
                                               ctypes.c_void_p(stream.cuda_stream)))
                 for fn in (L.bode_repack_by_cost, L.bode_unpack):
@@ -275,9 +277,14 @@ def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warm
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
         n0 = P.lib().bode_launch_count()
         ev[0].record(stream)
-        if repack:
+        if reorder:
             P.api.check(L.bode_order_init(ctypes.c_void_p(order.data_ptr()), num,
                                           ctypes.c_void_p(stream.cuda_stream)))
+        if presort_row is not None:
+            P.api.check(L.bode_repack_by_param(
+                ctypes.byref(cprob), num, ctypes.c_void_p(yd.data_ptr()), ctypes.c_void_p(gp),
+                ctypes.c_void_p(st.data_ptr()), ctypes.c_void_p(order.data_ptr()), presort_row,
+                ctypes.c_void_p(stream.cuda_stream)))
         for k in range(steps):
             window(k, k > 0)
             if repack and k == 0 and steps > 1:
@@ -285,7 +292,7 @@ def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warm
                     ctypes.byref(cprob), num, ctypes.c_void_p(yd.data_ptr()),
                     ctypes.c_void_p(gp), ctypes.c_void_p(st.data_ptr()),
                     ctypes.c_void_p(order.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
-            if repack and k == steps - 1:
+            if reorder and k == steps - 1:
                 P.api.check(L.bode_unpack(
                     ctypes.byref(cprob), num, ctypes.c_void_p(yd.data_ptr()),
                     ctypes.c_void_p(gp), ctypes.c_void_p(st.data_ptr()),
@@ -447,9 +454,11 @@ def main():
                              "h2d_bytes_per_call": num * 28 * 8,
                              "d2h_bytes_per_call": num * (28 * 8 + 64)}
 
-    def secondary(problem, solver, arith, dim, y0s, g0s, label, steps, repack=False):
+    def secondary(problem, solver, arith, dim, y0s, g0s, label, steps, repack=False,
+                  presort_row=None):
         sec, perw, sts, _, _ = measure_device(P, A, torch, problem, solver, arith, dim, y0s, g0s,
-                                               steps, 1, stream, repack=repack)
+                                               steps, 1, stream, repack=repack,
+                                               presort_row=presort_row)
         f = algorithmic_flops(problem, solver, dim, sts, steps)
         n = y0s.size // dim
         return {"workload": label, "value": world * n * steps / secs_max(sec),
@@ -488,6 +497,13 @@ def main():
                 "expdecay", "rkc", "exact", 1, ye0, g0,
                 f"RKC expDecay, config 4 batch (natural order) re-packed by cost after window "
                 f"1, {args.rkc_num} systems, EXACT", min(args.steps, 10), repack=True)
+            # the same natural-order batch sorted by |g0| (its spectral radius, the
+            # reference's specRadHint) before window 1 (bode_repack_by_param) and
+            # restored at the end, inside the timing
+            extra["rkc_stiff_expdecay_presorted"] = secondary(
+                "expdecay", "rkc", "exact", 1, ye0, g0,
+                f"RKC expDecay, config 4 batch (natural order) sorted by |g0| before window 1, "
+                f"{args.rkc_num} systems, EXACT", min(args.steps, 10), presort_row=0)
             # the same batch with the systems sorted by stiffness (SURVEY 8d config 4:
             # shuffled and sorted): warps then hold similar stage counts
             order = np.argsort(g0, kind="stable")

@@ -101,6 +101,8 @@ def lib():
         "bode_lockstep_efficiency": (ctypes.c_int, [P(A.Problem), c_i32, c_i32, c_i64, vp, P(c_d),
                                                     vp]),
         "bode_set_repack_threshold": (ctypes.c_int, [c_d]),
+        "bode_repack_by_param": (ctypes.c_int, [P(A.Problem), c_i64, vp, vp, vp, vp, c_i32, vp]),
+        "bode_set_presort_param": (ctypes.c_int, [c_i32]),
         "bode_registered_count": (ctypes.c_int, []),
         "bode_integrate_fixed": (ctypes.c_int, [P(A.Problem), c_i32, c_i32, c_d, c_d, c_i64,
                                                 c_i32, c_d, c_i64, PD, PD]),
@@ -351,6 +353,16 @@ def repack_by_cost(problem: OdeProblem, num: int, y_ptr: int, g_ptr: int, stats_
     check(lib().bode_repack_by_cost(ctypes.byref(problem.c()), num, ctypes.c_void_p(y_ptr),
                                     ctypes.c_void_p(g_ptr or None), ctypes.c_void_p(stats_ptr),
                                     ctypes.c_void_p(order_ptr), ctypes.c_void_p(stream or None)))
+
+
+def repack_by_param(problem: OdeProblem, num: int, y_ptr: int, g_ptr: int, stats_ptr: int,
+                    order_ptr: int, param_row: int, stream: int = 0):
+    """Sort a device-resident batch by |g[param_row]|, a stiffness proxy known
+    before any window (bode_repack_by_param); results stay bitwise identical."""
+    check(lib().bode_repack_by_param(ctypes.byref(problem.c()), num, ctypes.c_void_p(y_ptr),
+                                     ctypes.c_void_p(g_ptr), ctypes.c_void_p(stats_ptr or None),
+                                     ctypes.c_void_p(order_ptr), param_row,
+                                     ctypes.c_void_p(stream or None)))
 
 
 def unpack_order(problem: OdeProblem, num: int, y_ptr: int, g_ptr: int, stats_ptr: int,

@@ -66,6 +66,8 @@ const KernelEntry* kernel_table(int* count);
 // repack.cu: cost-aware re-packing of a device-resident batch
 int repack_by_cost(int N, int P, long long num, double* y, double* g, DevStats* st,
                    long long* order, cudaStream_t s);
+int repack_by(int N, int P, long long num, double* y, double* g, DevStats* st, long long* order,
+              int param_row, cudaStream_t s);
 int unpack(int N, int P, long long num, double* y, double* g, DevStats* st, long long* order,
            double* y_out, cudaStream_t s);
 int init_order(long long* order, long long num, cudaStream_t s);

@@ -38,6 +38,14 @@ std::atomic<long long> g_launches{0};
 std::atomic<int> g_block_override{0};
 std::atomic<int> g_persistent{0};  // dynamic-refill kernels where compiled (opt-in)
 std::atomic<double> g_repack_threshold{0.7};  // outer loop: re-pack below this efficiency
+std::atomic<int> g_presort_param{-2};  // outer loop: sort by |g[row]| first (-1 off, -2 auto)
+
+// The parameter row that is a system's stiffness (its spectral radius up to a
+// constant) for the built-in problems: expDecay's g0 (the reference's
+// specRadHint, problems.cpp:140-142). -1: none known.
+int stiffness_param_row(const bode_problem_t* p) {
+    return p->kind == BODE_PROBLEM_EXPDECAY && p->param_dim >= 1 ? 0 : -1;
+}
 
 int fail(int code, const std::string& msg) {
     g_last_error = msg;
@@ -659,6 +667,12 @@ int bode_set_repack_threshold(double threshold) {
     return BODE_OK;
 }
 
+int bode_set_presort_param(int32_t param_row) {
+    if (param_row < -2) return fail(BODE_E_INVALID_SHAPE, "presort parameter row must be >= -2");
+    g_presort_param.store(param_row);
+    return BODE_OK;
+}
+
 int bode_order_init(int64_t* order_dev, int64_t num, void* stream) {
     if (order_dev == nullptr || num < 1) return fail(BODE_E_INVALID_SHAPE, "order: bad arguments");
     int rc = check_devices(1);
@@ -680,6 +694,22 @@ int bode_repack_by_cost(const bode_problem_t* p, int64_t num, double* y_dev, dou
                               reinterpret_cast<DevStats*>(stats_dev),
                               reinterpret_cast<long long*>(order_dev),
                               static_cast<cudaStream_t>(stream));
+    return rc ? fail(rc, "repack failed") : BODE_OK;
+}
+
+int bode_repack_by_param(const bode_problem_t* p, int64_t num, double* y_dev, double* g_dev,
+                         bode_stats_t* stats_dev, int64_t* order_dev, int32_t param_row,
+                         void* stream) {
+    int rc = check_problem_shape(p);
+    if (rc) return rc;
+    if (num < 1 || y_dev == nullptr || g_dev == nullptr || order_dev == nullptr ||
+        param_row < 0 || param_row >= p->param_dim)
+        return fail(BODE_E_INVALID_SHAPE, "repack_by_param: bad arguments");
+    if ((rc = check_devices(1))) return rc;
+    rc = bode::repack_by(p->dim, p->param_dim, num, y_dev, g_dev,
+                         reinterpret_cast<DevStats*>(stats_dev),
+                         reinterpret_cast<long long*>(order_dev), param_row,
+                         static_cast<cudaStream_t>(stream));
     return rc ? fail(rc, "repack failed") : BODE_OK;
 }
 
@@ -781,6 +811,8 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
     double t = t0;
     std::vector<char> repacked(shards.size(), 0);
     const double threshold = g_repack_threshold.load();
+    const int presort_sel = g_presort_param.load();
+    const int presort_row = presort_sel == -2 ? stiffness_param_row(p) : presort_sel;
     for (int64_t k = 1; k <= nwin; ++k) {
         const double tk = (k == nwin) ? t_end : t0 + static_cast<double>(k) * h_outer;
         const bool snap = sink != nullptr || k == nwin;
@@ -794,9 +826,12 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
             const bool first = k == 1, last = k == nwin;
             const int nch = pinned ? (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, cnt / (1 << 16)))
                                    : 1;
+            // sort by a stiffness parameter before the first window: needs the
+            // whole shard uploaded first, so that upload is not chunked
+            const bool presort = first && presort_row >= 0 && presort_row < P && cnt >= 1024;
             // the final download can ride along per chunk unless the batch is re-packed
-            const bool chunked_out = last && !repacked[si] && nch > 1;
-            const bool chunked = (first && nch > 1) || chunked_out;
+            const bool chunked_out = last && !repacked[si] && !presort && nch > 1;
+            const bool chunked = (first && !presort && nch > 1) || chunked_out;
             int r = BODE_OK;
             if (first && !chunked) {  // upload in one piece
                 BODE_CUDA(cudaMemcpy2DAsync(B.y, cnt * sizeof(double), y + sh.begin,
@@ -806,6 +841,11 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
                     BODE_CUDA(cudaMemcpy2DAsync(B.g, cnt * sizeof(double), g + sh.begin,
                                                 num * sizeof(double), cnt * sizeof(double), P,
                                                 cudaMemcpyHostToDevice, s));
+            }
+            if (presort) {
+                if ((r = bode::repack_by(N, P, cnt, B.y, B.g, B.st, B.ord, presort_row, s)))
+                    return fail(r, "presort failed");
+                repacked[si] = 1;
             }
             if (chunked) {
                 const long long cb = cnt / nch, crem = cnt % nch;

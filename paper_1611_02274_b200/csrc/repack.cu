@@ -58,6 +58,16 @@ __global__ void cost_keys(const DevStats* __restrict__ st, long long num,
     idx[i] = (unsigned)i;
 }
 
+// key = |g_row[i]| rounded to float: for non-negative floats the bit pattern
+// orders like the value (NaN sorts last)
+__global__ void param_keys(const double* __restrict__ g_row, long long num,
+                           unsigned* __restrict__ key, unsigned* __restrict__ idx) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= num) return;
+    key[i] = __float_as_uint(fabsf(__double2float_rn(g_row[i])));
+    idx[i] = (unsigned)i;
+}
+
 // dst[j*num + p] = src[j*num + from[p]] (SoA gather, coalesced writes)
 __global__ void gather_soa(const double* __restrict__ src, double* __restrict__ dst, int rows,
                            long long num, const unsigned* __restrict__ from) {
@@ -141,11 +151,16 @@ int cuda_fail(cudaError_t e) {
 
 namespace bode {
 
-// Sorts the systems by cost (stats[i].rhs_evals) and permutes y, g, stats and
-// order accordingly; all pointers are device pointers on the current device.
-int repack_by_cost(int N, int P, long long num, double* y, double* g, DevStats* st,
-                   long long* order, cudaStream_t s) {
-    if (num < 2 || st == nullptr || order == nullptr) return BODE_OK;
+// Sorts the systems by a key and permutes y, g, stats (may be null) and order
+// accordingly: the cost each system just showed (stats[i].rhs_evals) when
+// param_row < 0, else the magnitude of parameter row param_row (a stiffness
+// proxy such as expDecay's g0, known before the first window). All pointers
+// are device pointers on the current device.
+int repack_by(int N, int P, long long num, double* y, double* g, DevStats* st, long long* order,
+              int param_row, cudaStream_t s) {
+    if (num < 2 || order == nullptr) return BODE_OK;
+    if (param_row < 0 ? st == nullptr : (param_row >= P || g == nullptr))
+        return BODE_E_INVALID_SHAPE;
     int dev = 0;
     RP_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64) return BODE_E_UNSUPPORTED;
@@ -179,7 +194,10 @@ int repack_by_cost(int N, int P, long long num, double* y, double* g, DevStats* 
     c += al(n * sizeof(DevStats));
     long long* ord2 = reinterpret_cast<long long*>(c);
 
-    cost_keys<<<blocks(num, 256), 256, 0, s>>>(st, num, key, idx);
+    if (param_row < 0)
+        cost_keys<<<blocks(num, 256), 256, 0, s>>>(st, num, key, idx);
+    else
+        param_keys<<<blocks(num, 256), 256, 0, s>>>(g + (size_t)param_row * n, num, key, idx);
     RP_CUDA(cub::DeviceRadixSort::SortPairs(tmp, sort_bytes, key, key2, idx, from, (int)num, 0,
                                             32, s));
     gather_soa<<<blocks(num, 256), 256, 0, s>>>(y, buf, N, num, from);
@@ -189,10 +207,16 @@ int repack_by_cost(int N, int P, long long num, double* y, double* g, DevStats* 
         RP_CUDA(cudaMemcpyAsync(g, buf, n * P * sizeof(double), cudaMemcpyDeviceToDevice, s));
     }
     gather_stats_order<<<blocks(num, 256), 256, 0, s>>>(st, st2, order, ord2, num, from);
-    RP_CUDA(cudaMemcpyAsync(st, st2, n * sizeof(DevStats), cudaMemcpyDeviceToDevice, s));
+    if (st != nullptr)
+        RP_CUDA(cudaMemcpyAsync(st, st2, n * sizeof(DevStats), cudaMemcpyDeviceToDevice, s));
     RP_CUDA(cudaMemcpyAsync(order, ord2, n * sizeof(long long), cudaMemcpyDeviceToDevice, s));
     RP_CUDA(cudaGetLastError());
     return BODE_OK;
+}
+
+int repack_by_cost(int N, int P, long long num, double* y, double* g, DevStats* st,
+                   long long* order, cudaStream_t s) {
+    return repack_by(N, P, num, y, g, st, order, -1, s);
 }
 
 // Scatters y (and g, stats) back to original positions and resets order.

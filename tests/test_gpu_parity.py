@@ -376,10 +376,13 @@ def test_ragged_batch_sizes_bitwise(gpu, oracle, num):
             assert np.array_equal(st[k], so[k]), (prob.kind, num, k)
 
 
-def test_outer_loop_pinned_params_and_repack(gpu):
+@pytest.mark.parametrize("presort", [False, True])
+def test_outer_loop_pinned_params_and_repack(gpu, presort):
     """Pinned buffers with per-system parameters (config 4, P = 1): chunked
     strided upload of y and g, automatic re-packing after window 1, unpack and
-    whole download at the end -- bitwise the pageable path and the oracle."""
+    whole download at the end -- bitwise the pageable path and the oracle.
+    With presort, the batch is sorted by |g0| before window 1 instead (whole
+    upload, bode_set_presort_param)."""
     import ctypes
     import torch
     L = B.lib()
@@ -388,6 +391,7 @@ def test_outer_loop_pinned_params_and_repack(gpu):
     prob, solver, y0, g = build_inputs(case, num)
     tol = A.default_tol()
     outs = {}
+    B.api.check(L.bode_set_presort_param(0 if presort else -1))
     for pinned in (False, True):
         yh = torch.from_numpy(y0.copy())
         gh = torch.from_numpy(g.copy())
@@ -401,6 +405,7 @@ def test_outer_loop_pinned_params_and_repack(gpu):
                                       ctypes.c_void_p(sth.data_ptr()), 1, B.api.SINK(), None,
                                       ctypes.byref(n)))
         outs[pinned] = (yh.numpy().copy(), sth.numpy().copy())
+    B.api.check(L.bode_set_presort_param(-2))  # back to the default
     assert np.array_equal(outs[False][0].view(np.uint64), outs[True][0].view(np.uint64))
     assert np.array_equal(outs[False][1], outs[True][1])
     idx = np.arange(0, num, 97)

@@ -87,6 +87,7 @@ def test_outer_loop_repack_is_bitwise_invisible(gpu):
     num = 1 << 15
     prob, solver, y0, g = _config4(num)
     runs = {}
+    B.api.check(L.bode_set_presort_param(-1))  # the cost re-pack, not the g0 presort
     for thr in (0.0, 0.7):
         B.api.check(L.bode_set_repack_threshold(thr))
         snaps = []
@@ -96,6 +97,7 @@ def test_outer_loop_repack_is_bitwise_invisible(gpu):
                          sink=lambda t, b: snaps.append((t, b.values.copy())))
         runs[thr] = (r, snaps)
     B.api.check(L.bode_set_repack_threshold(0.7))
+    B.api.check(L.bode_set_presort_param(-2))
     (r0, s0), (r1, s1) = runs[0.0], runs[0.7]
     assert np.array_equal(r0.states.values.view(np.uint64), r1.states.values.view(np.uint64))
     for k in A.STATS_DTYPE.names:
@@ -103,3 +105,53 @@ def test_outer_loop_repack_is_bitwise_invisible(gpu):
     assert len(s0) == len(s1) == 10
     for (t0, a), (t1, b) in zip(s0, s1):
         assert t0 == t1 and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+@pytest.mark.parametrize("with_sink", [False, True])
+def test_outer_loop_presort_by_param_is_bitwise_invisible(gpu, with_sink):
+    """bode_set_presort_param(0): config 4 sorted by |g0| before the first
+    window (bode_repack_by_param), snapshots and the result in the caller's
+    order, bitwise the unsorted run's."""
+    L = B.lib()
+    num = 1 << 15
+    prob, solver, y0, g = _config4(num)
+    runs = {}
+    for row in (-1, 0):
+        B.api.check(L.bode_set_presort_param(row))
+        snaps = []
+        batch = B.BatchStates(num, prob.dim, prob.param_dim, y0.copy(), g.copy())
+        sink = (lambda t, b: snaps.append((t, b.values.copy()))) if with_sink else None
+        r = B.outer_loop(B.OdeProblem(prob.kind, prob.dim, prob.param_dim), batch, 0.0, 1.0, 0.1,
+                         solver="rkc", arith="exact", sink=sink)
+        runs[row] = (r, snaps)
+    B.api.check(L.bode_set_presort_param(-2))  # back to the default
+    (r0, s0), (r1, s1) = runs[-1], runs[0]
+    assert np.array_equal(r0.states.values.view(np.uint64), r1.states.values.view(np.uint64))
+    for k in A.STATS_DTYPE.names:
+        assert np.array_equal(r0.stats[k], r1.stats[k]), k
+    assert len(s0) == len(s1)
+    for (t0, a), (t1, b) in zip(s0, s1):
+        assert t0 == t1 and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def test_repack_by_param_sorts_and_unpacks(gpu):
+    """bode_repack_by_param orders the batch by |g0| (stable), moves y and the
+    order map with it, and bode_unpack restores the caller's order."""
+    import torch
+    num = 5000
+    prob, solver, y0, g = _config4(num)
+    y = torch.from_numpy(y0.copy()).cuda()
+    gd = torch.from_numpy(g.copy()).cuda()
+    order = torch.zeros(num, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    p = B.OdeProblem(prob.kind, prob.dim, prob.param_dim)
+    B.api.order_init(order.data_ptr(), num, s)
+    B.api.repack_by_param(p, num, y.data_ptr(), gd.data_ptr(), 0, order.data_ptr(), 0, s)
+    torch.cuda.synchronize()
+    perm = np.argsort(np.abs(g).astype(np.float32), kind="stable")
+    assert np.array_equal(order.cpu().numpy(), perm)
+    assert np.array_equal(gd.cpu().numpy(), g[perm])
+    assert np.array_equal(y.cpu().numpy(), y0[perm])
+    B.api.unpack_order(p, num, y.data_ptr(), gd.data_ptr(), 0, order.data_ptr(), s)
+    torch.cuda.synchronize()
+    assert np.array_equal(gd.cpu().numpy(), g) and np.array_equal(y.cpu().numpy(), y0)
