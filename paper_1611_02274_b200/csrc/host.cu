@@ -339,7 +339,7 @@ int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double*
     return BODE_OK;
 }
 
-constexpr int kMaxChunks = 16;  // host-pointer pipeline depth per shard
+constexpr int kMaxChunks = 32;  // host-pointer pipeline depth per shard
 
 // Per-device buffers reused across calls (no cudaMalloc on the hot path once warm).
 struct DeviceBuffers {
