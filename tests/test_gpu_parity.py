@@ -461,3 +461,29 @@ def test_pleiades_exact_outside_fast_range_bitwise(gpu, oracle, scale):
     assert np.array_equal(y.view(np.uint64), yo.view(np.uint64))
     for k in COUNTS:
         assert np.array_equal(st[k], so[k]), k
+
+
+def test_int_driver_pinned_32_chunk_pipeline(gpu):
+    """bode_int_driver on pinned host buffers at 2^21 systems runs the full
+    32-chunk H2D / kernel / D2H pipeline (strided column chunks); states and
+    stats equal the device-pointer entry's bit for bit."""
+    import ctypes
+    import torch
+    L = B.lib()
+    num = 1 << 21
+    prob = A.make_problem(A.PLEIADES)
+    y0 = perturb(PLEIADES_IC, 0.01, 5, num)
+    tol = A.default_tol()
+    yh = torch.from_numpy(y0.copy()).pin_memory()
+    sth = torch.zeros(num * 8, dtype=torch.int64).pin_memory()
+    B.api.check(L.bode_int_driver(ctypes.byref(prob), A.SOLVER_RKCK, A.ARITH_FAST, 0.3, 0.4, num,
+                                  None, ctypes.cast(yh.data_ptr(), ctypes.POINTER(ctypes.c_double)),
+                                  ctypes.byref(tol), ctypes.c_void_p(sth.data_ptr()), 1))
+    yd = torch.from_numpy(y0.copy()).cuda()
+    std = torch.zeros(num * 8, dtype=torch.int64, device="cuda")
+    B.int_driver_device(B.OdeProblem(prob.kind, prob.dim, prob.param_dim), "rkck", "fast", 0.3,
+                        0.4, num, 0, yd.data_ptr(), tol, std.data_ptr(), False,
+                        torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(yh.numpy().view(np.uint64), yd.cpu().numpy().view(np.uint64))
+    assert np.array_equal(sth.numpy(), std.cpu().numpy())
