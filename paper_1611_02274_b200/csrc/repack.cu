@@ -18,6 +18,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -109,28 +110,48 @@ __global__ void identity_order(long long* __restrict__ ord, long long num) {
 }
 
 // sum over systems of cost, and of the cost of each system's warp group's
-// slowest member (groups of `group` consecutive systems, group | 32): one
-// thread per system, shuffle reductions, one atomic pair per warp
+// slowest member (groups of `group` consecutive systems, group | 32)
 __global__ void lockstep_sums(const DevStats* __restrict__ st, long long num, int group,
                               unsigned long long* __restrict__ sums) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool valid = i < num;
-    const long long c0 = valid ? st[i].rhs_evals : 0;
-    const unsigned long long c = c0 > 0 ? (unsigned long long)c0 : 0ull;
-    unsigned long long m = c;
-    for (int o = group / 2; o > 0; o /= 2) {
-        const unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
-        m = t > m ? t : m;
+    // grid-stride over warp-aligned positions (the stride is a multiple of 32,
+    // so a lane group never straddles two iterations), shuffle reductions per
+    // warp, then one atomic pair per block: a few thousand atomics instead of
+    // one pair per warp
+    __shared__ unsigned long long part[2][32];
+    unsigned long long s = 0ull, w = 0ull;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i - threadIdx.x % 32 < num;
+         i += stride) {
+        const bool valid = i < num;
+        const long long c0 = valid ? st[i].rhs_evals : 0;
+        const unsigned long long c = c0 > 0 ? (unsigned long long)c0 : 0ull;
+        unsigned long long m = c;
+        for (int o = group / 2; o > 0; o /= 2) {
+            const unsigned long long t = __shfl_xor_sync(0xffffffffu, m, o);
+            m = t > m ? t : m;
+        }
+        s += c;
+        w += valid ? m : 0ull;
     }
-    unsigned long long s = c, w = valid ? m : 0ull;
 #pragma unroll
     for (int o = 16; o > 0; o /= 2) {
         s += __shfl_xor_sync(0xffffffffu, s, o);
         w += __shfl_xor_sync(0xffffffffu, w, o);
     }
+    const int warp = threadIdx.x / 32, nwarps = blockDim.x / 32;
     if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&sums[0], s);
-        atomicAdd(&sums[1], w);
+        part[0][warp] = s;
+        part[1][warp] = w;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long bs = 0ull, bw = 0ull;
+        for (int k = 0; k < nwarps; ++k) {
+            bs += part[0][k];
+            bw += part[1][k];
+        }
+        atomicAdd(&sums[0], bs);
+        atomicAdd(&sums[1], bw);
     }
 }
 
@@ -280,7 +301,10 @@ int lockstep_efficiency(const DevStats* st, long long num, int group, double* ef
         RP_CUDA(cudaMallocHost(&hsum[dev], 2 * sizeof(unsigned long long)));
     }
     RP_CUDA(cudaMemsetAsync(dsum[dev], 0, 2 * sizeof(unsigned long long), s));
-    lockstep_sums<<<blocks(num, 256), 256, 0, s>>>(st, num, group, dsum[dev]);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = (unsigned)std::min<long long>(blocks(num, 256), 8ll * sms);
+    lockstep_sums<<<grid, 256, 0, s>>>(st, num, group, dsum[dev]);
     RP_CUDA(cudaMemcpyAsync(hsum[dev], dsum[dev], 2 * sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, s));
     RP_CUDA(cudaStreamSynchronize(s));
