@@ -120,3 +120,23 @@ def test_supported_matrix():
         for arith in (0, 1):
             p = A.make_problem(kind, dim)
             assert L.bode_problem_supported(ctypes.byref(p), solver, arith) == 1
+
+
+def test_scheduling_knob_validation():
+    """Host-side setters reject out-of-range values before any device use, and
+    the re-pack entry points validate their arguments (include/bode.h)."""
+    L = B.lib()
+    assert L.bode_set_repack_threshold(1.5) == A.E_INVALID_SHAPE
+    assert L.bode_set_repack_threshold(-0.1) == A.E_INVALID_SHAPE
+    assert L.bode_set_presort_param(-3) == A.E_INVALID_SHAPE
+    assert L.bode_set_block_size(48) == A.E_INVALID_SHAPE
+    for ok in (-2, -1, 0):
+        assert L.bode_set_presort_param(ok) == 0
+    assert L.bode_set_presort_param(-2) == 0  # the default
+    assert L.bode_set_repack_threshold(0.7) == 0
+    prob = A.make_problem(A.EXPDECAY)
+    # param_row must name a parameter row; g and order must be given
+    assert L.bode_repack_by_param(ctypes.byref(prob), 8, None, None, None, None, 0,
+                                  None) == A.E_INVALID_SHAPE
+    assert L.bode_repack_by_param(ctypes.byref(prob), 8, ctypes.c_void_p(8), ctypes.c_void_p(8),
+                                  None, ctypes.c_void_p(8), 1, None) == A.E_INVALID_SHAPE
