@@ -91,6 +91,34 @@ __device__ __forceinline__ R seq_sum(const Group<L>& G, const R (&terms)[C], R i
     }
 }
 
+// Two independent sequential sums advanced together (each in its own
+// component order, so each is bitwise seq_sum's): the chains interleave, and
+// the pair costs one chain's latency.
+template <class R, int L, int C>
+__device__ __forceinline__ void seq_sum2(const Group<L>& G, const R (&a)[C], const R (&b)[C],
+                                         R& sa, R& sb) {
+    if constexpr (L == 1) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            sa = sa + a[c];
+            sb = sb + b[c];
+        }
+    } else {
+#pragma unroll 1
+        for (int k = 0; k < L; ++k) {
+            if (G.lane == k) {
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    sa = sa + a[c];
+                    sb = sb + b[c];
+                }
+            }
+            sa = R(G.from(val(sa), k));
+            sb = R(G.from(val(sb), k));
+        }
+    }
+}
+
 // -------------------------------------------------------------------------
 // Pleiades (problems.cpp:9-37): N = 28, masses m_i = i + 1, pairs i<j with
 // i outer, j inner; action/reaction share one distance evaluation.

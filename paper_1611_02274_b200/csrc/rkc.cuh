@@ -285,12 +285,17 @@ __device__ __forceinline__ int power_method(const Group<L>& G, bool on, R t, con
     const R sqrtU = sqrt_(kUround);
     const R small = R(1.0) / hMax;
     R v[C], tmp[C];
+    R nrmY(0.0), nrmV(0.0);
+    {  // ||y|| and ||v|| (spectral_radius.cpp:11-13, :33-34): two chains at once
 #pragma unroll
-    for (int c = 0; c < C; ++c) tmp[c] = y[c] * y[c];
-    const R nrmY = sqrt_(rkc_seq_sum<R, L, C>(G, tmp, R(0.0)));
-#pragma unroll
-    for (int c = 0; c < C; ++c) tmp[c] = R(eig[c]) * R(eig[c]);
-    const R nrmV = sqrt_(rkc_seq_sum<R, L, C>(G, tmp, R(0.0)));
+        for (int c = 0; c < C; ++c) {
+            tmp[c] = y[c] * y[c];
+            v[c] = R(eig[c]) * R(eig[c]);
+        }
+        seq_sum2<R, L, C>(G, tmp, v, nrmY, nrmV);
+        nrmY = sqrt_(nrmY);
+        nrmV = sqrt_(nrmV);
+    }
     R dynrm;
     if (nrmY != R(0.0) && nrmV != R(0.0)) {
         dynrm = nrmY * sqrtU;
