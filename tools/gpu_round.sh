@@ -72,9 +72,6 @@ for p in $PARTS; do
         -s 1 -c 1 -o $OUT/prof_static_w1 python bench.py --steps 10 --warmup 0 --systems 1048576 \
         --no-secondary --no-e2e --no-cpu > $OUT/ncu_static.txt 2>&1
       echo "ncu_persist rc=$?" >> $OUT/status.txt ;;
-    ab_fastreg)
-      for R in 255 200 168; do BODE_MAXREG=$R timeout 600 python bench.py --no-e2e --no-cpu --no-secondary > $OUT/bench_fastreg$R.txt 2>&1; done
-      echo "ab_fastreg rc=$?" >> $OUT/status.txt ;;
     strag) timeout 600 python tools/straggler_sim.py > $OUT/straggler.txt 2>&1; echo "strag rc=$?" >> $OUT/status.txt ;;
     sweep) timeout 1500 python tools/sweep.py > $OUT/sweep.txt 2>&1; echo "sweep rc=$?" >> $OUT/status.txt ;;
     multirank)
@@ -92,13 +89,6 @@ for p in $PARTS; do
       for L in 1 2; do BODE_LANES=$L timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/bench_exact_lanes$L.txt 2>&1; done
       echo "ab_exact_lanes rc=$?" >> $OUT/status.txt ;;
     qrkc) timeout 900 python bench.py --no-e2e --no-cpu --steps 10 --systems 65536 > $OUT/quick_rkc.txt 2>&1; echo "qrkc rc=$?" >> $OUT/status.txt ;;
-    ab_bru)
-      for V in "4 255" "4 128" "8 255" "8 128" "16 128"; do set -- $V
-        BODE_LANES=$1 BODE_MAXREG=$2 timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 65536 --rkc-systems 1048576 > $OUT/bench_bru_L$1_R$2.txt 2>&1; done
-      echo "ab_bru rc=$?" >> $OUT/status.txt ;;
-    ab_exactreg)
-      for R in 168 128 200; do BODE_MAXREG=$R timeout 600 python bench.py --arith exact --no-e2e --no-cpu --no-secondary > $OUT/bench_exactreg$R.txt 2>&1; done
-      echo "ab_exactreg rc=$?" >> $OUT/status.txt ;;
     ab_heatblk)
       for V in "128 128" "112 64" "112 128" "128 64"; do set -- $V
         BODE_LANES=8 BODE_MAXREG=$1 timeout 600 python bench.py --no-e2e --no-cpu --steps 5 --systems 65536 --rkc-systems 1048576 --block $2 > $OUT/bench_heat_R$1_B$2.txt 2>&1; done
