@@ -60,6 +60,7 @@ const int bode_registered_brusselator32 = [] {
     static const bode::KernelEntry e[] = {
         // RKC EXACT measured (2^20 systems, 5 windows, system-windows/s): 4 lanes
         // uncapped 6.33e7, 8 @128 6.07e7, 4 @168 5.83e7, 8 @168 5.58e7 (r01cq);
+        // 4 @224 in 32-thread blocks 5.78e7, 4 @200 in 64-thread blocks 5.89e7 (r01df);
         // the heavier reaction RHS and 3 instead of 7 sum hand-offs favour 4 lanes
         bode::make_entry<Bru, bode::xd, 4, 1, false, 0>(BODE_PROBLEM_BRUSSELATOR, BODE_ARITH_EXACT),
         bode::make_entry<Bru, double, 4, 1, false, 0>(BODE_PROBLEM_BRUSSELATOR, BODE_ARITH_FAST),
