@@ -107,8 +107,8 @@ def test_outer_loop_repack_is_bitwise_invisible(gpu):
         assert t0 == t1 and np.array_equal(a.view(np.uint64), b.view(np.uint64))
 
 
-@pytest.mark.parametrize("with_sink", [False, True])
-def test_outer_loop_presort_by_param_is_bitwise_invisible(gpu, with_sink):
+@pytest.mark.parametrize("with_sink,t_end", [(False, 1.0), (True, 1.0), (False, 0.1)])
+def test_outer_loop_presort_by_param_is_bitwise_invisible(gpu, with_sink, t_end):
     """bode_set_presort_param(0): config 4 sorted by |g0| before the first
     window (bode_repack_by_param), snapshots and the result in the caller's
     order, bitwise the unsorted run's."""
@@ -121,8 +121,8 @@ def test_outer_loop_presort_by_param_is_bitwise_invisible(gpu, with_sink):
         snaps = []
         batch = B.BatchStates(num, prob.dim, prob.param_dim, y0.copy(), g.copy())
         sink = (lambda t, b: snaps.append((t, b.values.copy()))) if with_sink else None
-        r = B.outer_loop(B.OdeProblem(prob.kind, prob.dim, prob.param_dim), batch, 0.0, 1.0, 0.1,
-                         solver="rkc", arith="exact", sink=sink)
+        r = B.outer_loop(B.OdeProblem(prob.kind, prob.dim, prob.param_dim), batch, 0.0, t_end,
+                         0.1, solver="rkc", arith="exact", sink=sink)
         runs[row] = (r, snaps)
     B.api.check(L.bode_set_presort_param(-2))  # back to the default
     (r0, s0), (r1, s1) = runs[-1], runs[0]
