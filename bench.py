@@ -4,24 +4,32 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl bode|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
 
-Workload (BASELINE.json configs[1]): RKCK on the Pleiades problem (N = 28),
-2^22 systems per GPU with the reference's perturbed initial conditions
+Workload (BASELINE.json configs[4] = config 5 at N GPUs; its RKCK leg is
+configs[1]'s workload at 2^24): RKCK on the Pleiades problem (N = 28),
+2^24 systems in total, with the reference's perturbed initial conditions
 (perturbInitialConditions(pleiades_ic, 0.01, seed 42), problems.cpp:171-191).
 A "step" is one outer window of 0.1 time units over all systems (a restart,
-batch_driver.hpp:36-39); K = 10 steps is the paper's [0, 1] protocol
-(PAPER.md:652). value = systems x windows / device time (max over ranks),
-inputs resident in HBM; e2e = the same metric through the host-pointer C ABI
-(bode_int_driver) with pinned host buffers, H2D + D2H inside every step.
-The y array (940 MB) exceeds L2 (126 MB), so no L2 flush is needed.
+batch_driver.hpp:36-39). Step k integrates window (k mod 10) of the paper's
+[0, 1] protocol and every 10th step restarts from y0 -- the
+same schedule as the reference arm and the CPU baseline. The restore is a
+device copy outside the timed intervals (per-window CUDA events).
 
-Multi-GPU: systems are independent, so each rank integrates its own 2^22
-systems with no collective on the data path (weak scaling); torch.distributed
-only provides the barrier and the max-over-ranks of the device time.
+value = systems x windows / device time (max over ranks), inputs resident in
+HBM; e2e = the same metric through the host-pointer C ABI (bode_int_driver)
+with pinned host buffers, H2D + D2H inside every step, and (N > 1) the final
+result gather to rank 0 inside the timed region. The y array (3.76 GB)
+exceeds L2 (126 MB), so no L2 flush is needed.
+
+Multi-GPU (config 5): the 2^24 systems are split into contiguous shards, one
+per rank (strong scaling; batch_driver.cpp:68-73 across GPUs). No collective
+runs on the data path; the only exchange is the final gather of the shards to
+rank 0 (paper_1611_02274_b200/dist.py, NCCL over NVLink).
 
 Roofline: the path is FP64-compute bound (AI ~74 flop/B for RKCK-Pleiades);
 achieved = algorithmic flops (SURVEY.md 8d formulas on the per-system
 counters the kernel emits) / kernel time; peak = this device's DFMA
-throughput measured in the same run (MEASURED_PEAKS.json has no FP64 entry).
+throughput measured in the same run (MEASURED_PEAKS.json has no FP64 entry),
+with the nominal 64 DFMA/clk/SM figure beside it.
 """
 from __future__ import annotations
 
@@ -44,6 +52,14 @@ sys.path.insert(0, os.path.join(REPO, "tests"))
 METRIC = "ODE systems integrated/sec (RKCK, RKC) at 1/2/4/8 B200 vs CPU ref, %FP64 roof"
 UNIT = "system-windows/s"
 F_RHS = {"pleiades": 420, "heat": None, "expdecay": 1, "harmonic": 0}
+CYCLE = 10  # windows per [0, 1] protocol; the schedule restarts from y0 after each
+T_START = time.monotonic()
+
+
+def window_bounds(k: int):
+    """Step k of the bench schedule: window (k mod 10) of [0, 1]."""
+    j = k % CYCLE
+    return 0.0 + j * 0.1, 0.0 + (j + 1) * 0.1
 
 
 def algorithmic_flops(problem: str, solver: str, dim: int, stats: np.ndarray, windows: int) -> float:
@@ -121,60 +137,126 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_rate(problem, solver, base, mag, seed, num, windows, g=None, threads=None):
-    """The reference CPU path (oracle/_ref = unmodified reference sources;
-    fallback: the oracle restatement) on all host threads (or `threads`)."""
-    from golden_cases import perturb
+# ------------------------------------------------------------ inputs ----
+def gen_states(L, base, mag, seed, first, count):
+    """Systems [first, first+count) of perturbInitialConditions(base, mag, seed)
+    as a local SoA array (bode_perturb_initial_conditions_range, threaded C)."""
+    base = np.ascontiguousarray(base, dtype=np.float64)
+    out = np.empty(count * base.size)
+    dp = ctypes.POINTER(ctypes.c_double)
+    rc = L.bode_perturb_initial_conditions_range(base.ctypes.data_as(dp), base.size, mag, seed,
+                                                 first, count, out.ctypes.data_as(dp))
+    assert rc == 0, L.bode_last_error()
+    return out
+
+
+def stiffness_range(first, count, seed=9):
+    """Config 4's g0_i = 10^(2 + 2*unitSymmetricAt(9, i)) for i in [first, first+count)."""
+    k = np.arange(first, first + count, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(seed) + (k + np.uint64(1)) * np.uint64(0x9e3779b97f4a7c15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xbf58476d1ce4e5b9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94d049bb133111eb)
+        z = z ^ (z >> np.uint64(31))
+    u = 2.0 * ((z >> np.uint64(11)).astype(np.float64) * 2.0 ** -53) - 1.0
+    return 10.0 ** (2.0 + 2.0 * u)
+
+
+# ------------------------------------------------------- CPU reference ----
+def cpu_reference(problem, solver, base, mag, seed, num, g=None, threads=None, repeats=3):
+    """The reference CPU path timed like timedOuterLoop (bench.cpp:196-214):
+    batchode::outerLoop over [0, 1] in 10 windows of 0.1 (oracle/_ref = the
+    unmodified reference sources; fallback: the oracle restatement), all host
+    threads (or `threads`), one warm-up window, best of `repeats`.
+    Returns (rate, cores, kind, best_seconds, y_final, stats)."""
     from oracle_lib import Oracle, RefLib, ref_available
     from paper_1611_02274_b200 import _abi as A
     prob = A.make_problem(problem, base.size)
     solv = A.SOLVER_NAMES[solver]
-    y0 = perturb(base, mag, seed, num)
+    y0 = gen_states(_lib(), base, mag, seed, 0, num)
     cores = threads or os.cpu_count()
     if ref_available():
         lib, kind = RefLib(), "reference"
+        run = lambda y, t0, t1, h: lib.outer_loop(prob, solv, t0, t1, h, y, g, workers=cores)
+    else:
+        lib, kind = Oracle(), "port"
+        run = lambda y, t0, t1, h: lib.outer_loop(prob, solv, t0, t1, h, y, g, threads=cores)
+    run(y0, 0.0, 0.1, 0.1)  # warm-up window
+    best, out = None, None
+    for _ in range(repeats):
+        t = time.perf_counter()
+        rc, y, st, nwin = run(y0, 0.0, 1.0, 0.1)
+        dt = time.perf_counter() - t
+        assert rc == 0 and nwin == CYCLE
+        if best is None or dt < best:
+            best, out = dt, (y, st)
+    return num * CYCLE / best, cores, kind, best, out[0], out[1]
+
+
+_L = None
+
+
+def _lib():
+    global _L
+    if _L is None:
+        import paper_1611_02274_b200 as P
+        _L = P.lib()
+    return _L
+
+
+def run_reference_arm(args):
+    """--impl reference: the reference's own CPU path (oracle/_ref) on the host
+    cores, on this arm's workload (RKCK Pleiades, perturb 0.01 seed 42) and
+    step schedule; each step is one window over a bounded sample of systems."""
+    from oracle_lib import Oracle, RefLib, ref_available
+    from paper_1611_02274_b200 import _abi as A
+    from golden_cases import PLEIADES_IC
+    num = args.cpu_sample
+    prob = A.make_problem(A.PLEIADES)
+    y0 = gen_states(_lib(), PLEIADES_IC, 0.01, 42, 0, num)
+    cores = os.cpu_count()
+    if ref_available():
+        lib, kind = RefLib(), "reference"
         run = lambda y, t0, t1: lib.lib.ref_integrate_batch(
-            ctypes.byref(prob), solv, t0, t1, num, A.dptr(y), A.dptr(g),
+            ctypes.byref(prob), A.SOLVER_RKCK, t0, t1, num, A.dptr(y), None,
             ctypes.byref(A.default_tol()), None, cores)
     else:
         lib, kind = Oracle(), "port"
         run = lambda y, t0, t1: lib.lib.orc_integrate_batch(
-            ctypes.byref(prob), solv, t0, t1, num, A.dptr(y), A.dptr(g),
+            ctypes.byref(prob), A.SOLVER_RKCK, t0, t1, num, A.dptr(y), None,
             ctypes.byref(A.default_tol()), None, cores)
     y = y0.copy()
-    run(y, 0.0, 0.1)  # warm-up window
-    # the GPU arm's schedule: windows (k mod 10) of [0, 1], restarting from y0
-    t = time.perf_counter()
-    for k in range(windows):
-        if k % 10 == 0:
+    for k in range(args.warmup):
+        if k % CYCLE == 0:
             y = y0.copy()
-        t0 = 0.0 + (k % 10) * 0.1
-        rc = run(y, t0, 0.0 + (k % 10 + 1) * 0.1)
+        assert run(y, *window_bounds(k)) == 0
+    dt = 0.0
+    for k in range(args.steps):
+        if k % CYCLE == 0:
+            y = y0.copy()  # outside the timed interval, as in the GPU arm
+        t = time.perf_counter()
+        rc = run(y, *window_bounds(k))
+        dt += time.perf_counter() - t
         assert rc == 0
-    dt = time.perf_counter() - t
-    return num * windows / dt, cores, kind, dt
-
-
-def run_reference_arm(args):
-    from golden_cases import PLEIADES_IC
-    rate, cores, kind, dt = cpu_reference_rate("pleiades", "rkck", PLEIADES_IC, 0.01, 42,
-                                               args.cpu_sample, args.steps)
+    rate = num * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "RKCK Pleiades, perturb 0.01 seed 42, eps 1e-10, windows "
-                               "(k mod 10) of [0, 1] as in the GPU arm",
-                   "systems_sampled": args.cpu_sample, "window": 0.1},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "RKCK Pleiades (N=28), perturb 0.01 seed 42, eps 1e-10; step k "
+                               "= window (k mod 10) of [0, 1], restart from y0 every 10 steps "
+                               "(the GPU arm's schedule)",
+                   "systems_sampled": num, "window": 0.1},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": f"{args.cpu_sample} systems x {args.steps} windows "
-                                   f"(+1 warm-up window)"},
+                         "sample": f"{num} systems x {args.steps} windows "
+                                   f"(+{args.warmup} warm-up windows), integrateBatch per window"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------- device ----
 def measured_traffic(capture: str, num: int):
     """DRAM bytes per launch for `num` systems, from the newest committed ncu
     capture summary (profiles/*_ncu.json: dram read+write per system-window),
@@ -236,15 +318,20 @@ def _parse_cpulist(text):
 
 
 def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warmup, stream,
-                   repack=False, presort_row=None):
-    """K windows on HBM-resident state; per-launch CUDA events on `stream`.
+                   repack=False, presort_row=None, return_state=False):
+    """K windows on HBM-resident state; per-window CUDA events on `stream`.
+    Step k integrates window (k mod 10) of [0, 1]; the state restarts from y0
+    before every 10th step with a device copy outside the timed intervals.
     repack: after the first timed window, re-pack the batch by the cost each
     system showed (bode_repack_by_cost), and restore the caller's order after
     the last (bode_unpack); both inside the timed region. presort_row: sort by
-    |g[presort_row]| before the first window instead (bode_repack_by_param)."""
+    |g[presort_row]| before the first window instead (bode_repack_by_param).
+    Re-packing moves systems, so it is only used within one [0, 1] cycle."""
     reorder = repack or presort_row is not None
+    assert not reorder or steps <= CYCLE
     num = y0.size // dim
-    yd = torch.from_numpy(y0).to("cuda")
+    y0d = torch.from_numpy(y0).to("cuda")
+    yd = y0d.clone()
     gd = torch.from_numpy(g0).to("cuda") if g0 is not None else None
     st = torch.zeros(num * 8, dtype=torch.int64, device="cuda")
     tol = A.default_tol()
@@ -252,9 +339,11 @@ def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warm
     gp = gd.data_ptr() if gd is not None else 0
 
     def window(k, merge):
-        t0 = 0.0 + (k % 10) * 0.1
-        P.int_driver_device(prob, solver, arith, t0, 0.0 + (k % 10 + 1) * 0.1, num, gp,
-                            yd.data_ptr(), tol, st.data_ptr(), merge, stream.cuda_stream)
+        if k > 0 and k % CYCLE == 0:
+            yd.copy_(y0d)
+        t0, t1 = window_bounds(k)
+        P.int_driver_device(prob, solver, arith, t0, t1, num, gp, yd.data_ptr(), tol,
+                            st.data_ptr(), merge, stream.cuda_stream)
 
     L = P.lib()
     order = torch.empty(num, dtype=torch.int64, device="cuda") if reorder else None
@@ -270,13 +359,15 @@ def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warm
                                    ctypes.c_void_p(gp), ctypes.c_void_p(st.data_ptr()),
                                    ctypes.c_void_p(order.data_ptr()),
                                    ctypes.c_void_p(stream.cuda_stream)))
-        yd.copy_(torch.from_numpy(y0))
+        yd.copy_(y0d)
         if gd is not None:
             gd.copy_(torch.from_numpy(g0))
         torch.cuda.synchronize()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         n0 = P.lib().bode_launch_count()
-        ev[0].record(stream)
+        pre = torch.cuda.Event(enable_timing=True)
+        pre.record(stream)
         if reorder:
             P.api.check(L.bode_order_init(ctypes.c_void_p(order.data_ptr()), num,
                                           ctypes.c_void_p(stream.cuda_stream)))
@@ -286,7 +377,12 @@ def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warm
                 ctypes.c_void_p(st.data_ptr()), ctypes.c_void_p(order.data_ptr()), presort_row,
                 ctypes.c_void_p(stream.cuda_stream)))
         for k in range(steps):
-            window(k, k > 0)
+            if k > 0 and k % CYCLE == 0:
+                yd.copy_(y0d)  # restart from y0, outside [ev0[k], ev1[k]]
+            ev0[k].record(stream)
+            t0, t1 = window_bounds(k)
+            P.int_driver_device(prob, solver, arith, t0, t1, num, gp, yd.data_ptr(), tol,
+                                st.data_ptr(), k > 0, stream.cuda_stream)
             if repack and k == 0 and steps > 1:
                 P.api.check(L.bode_repack_by_cost(
                     ctypes.byref(cprob), num, ctypes.c_void_p(yd.data_ptr()),
@@ -297,12 +393,24 @@ def measure_device(P, A, torch, problem, solver, arith, dim, y0, g0, steps, warm
                     ctypes.byref(cprob), num, ctypes.c_void_p(yd.data_ptr()),
                     ctypes.c_void_p(gp), ctypes.c_void_p(st.data_ptr()),
                     ctypes.c_void_p(order.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
-            ev[k + 1].record(stream)
+            ev1[k].record(stream)
         torch.cuda.synchronize()
     launches = P.lib().bode_launch_count() - n0
-    per = [ev[k].elapsed_time(ev[k + 1]) for k in range(steps)]
+    per = [ev0[k].elapsed_time(ev1[k]) for k in range(steps)]
+    if presort_row is not None and steps:
+        per[0] += pre.elapsed_time(ev0[0])  # the presort belongs to the timed region
     stats = st.cpu().numpy().view(A.STATS_DTYPE).copy()
-    return sum(per) / 1e3, per, stats, launches, yd
+    y_out = yd.cpu().numpy() if return_state else None
+    del yd, y0d, gd, st, order
+    torch.cuda.empty_cache()
+    return sum(per) / 1e3, per, stats, launches, y_out
+
+
+def sysrel(y, yo, num, dim):
+    """Per-system max-norm relative error (acceptance.cpp:142-147)."""
+    a, o = y.reshape(dim, num), yo.reshape(dim, num)
+    den = np.max(np.abs(o), axis=0)
+    return np.max(np.abs(a - o), axis=0) / np.where(den > 0, den, 1.0)
 
 
 def main():
@@ -312,18 +420,24 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="bode", choices=["bode", "reference"])
     # (not --num: torchrun's own parser would take it for --numa-binding)
-    ap.add_argument("--systems", dest="num", type=int, default=1 << 22, help="systems per GPU")
+    ap.add_argument("--systems", dest="num", type=int, default=1 << 24,
+                    help="systems in total, split over the ranks (config 5: 2^24)")
     ap.add_argument("--arith", default="fast", choices=["fast", "exact"])
-    ap.add_argument("--rkc-systems", dest="rkc_num", type=int, default=1 << 22)
+    ap.add_argument("--rkc-systems", dest="rkc_num", type=int, default=1 << 24,
+                    help="RKC heat64 systems in total (config 5: 2^24)")
+    ap.add_argument("--aux-systems", dest="aux_num", type=int, default=1 << 22,
+                    help="systems for the config 2-stress / 4 / Brusselator secondaries")
     ap.add_argument("--persistent", action="store_true",
                     help="persistent kernels with dynamic refill (default: static)")
     ap.add_argument("--no-secondary", dest="secondary", action="store_false",
                     help="skip the EXACT / RKC measurements")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 15)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 16)
     ap.add_argument("--block", type=int, default=0,
                     help="threads per block override (0: each kernel's default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--budget-s", type=float, default=1200.0,
+                    help="wall-clock budget: secondaries that would start after it are skipped")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -338,8 +452,8 @@ def main():
     import torch
     import paper_1611_02274_b200 as P
     from paper_1611_02274_b200 import _abi as A
-    from golden_cases import PLEIADES_IC, brusselator_ic, brusselator_params, heat_ic, perturb
-    from paper_1611_02274_b200.api import stiffness_params
+    from paper_1611_02274_b200 import dist as D
+    from golden_cases import PLEIADES_IC, brusselator_ic, brusselator_params, heat_ic
 
     # BODE_BENCH_SHARE_GPU=1 (functional test of the multi-rank path on one
     # GPU): ranks share cuda:0 and the barrier/max-over-ranks run on gloo
@@ -359,114 +473,6 @@ def main():
     P.api.check(L.bode_set_block_size(args.block))
     stream = torch.cuda.Stream()
 
-    peak = ctypes.c_double()
-    psec = ctypes.c_double()
-    P.api.check(L.bode_selftest_fp64_peak(ctypes.byref(peak), ctypes.byref(psec)))
-
-    # ---- headline: RKCK Pleiades, per-rank shard of args.num systems ----
-    num = args.num
-    y0 = perturb(PLEIADES_IC, 0.01, 42 + rank, num)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        secs, per, stats, launches, _ = measure_device(P, A, torch, "pleiades", "rkck",
-                                                       args.arith, 28, y0, None, args.steps,
-                                                       args.warmup, stream)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-        tt = torch.tensor([secs], device=red_dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        secs = float(tt.item())
-    value = world * num * args.steps / secs
-    flops = algorithmic_flops("pleiades", "rkck", 28, stats, args.steps)
-    achieved = flops / sum(p / 1e3 for p in per)
-
-    # ---- e2e through the host-pointer C ABI (pinned buffers, H2D+D2H every window) ----
-    e2e = None
-    if not args.no_e2e:
-        with gpu_local_memory(torch, local):
-            yh = torch.from_numpy(y0.copy()).pin_memory()
-            sth = torch.zeros(num * 8, dtype=torch.int64).pin_memory()
-        yp = ctypes.cast(yh.data_ptr(), ctypes.POINTER(ctypes.c_double))
-        prob = A.make_problem(A.PLEIADES)
-        tol = A.default_tol()
-        ar = A.ARITH_NAMES[args.arith]
-        P.api.check(L.bode_int_driver(ctypes.byref(prob), 0, ar, 0.0, 0.1, num, None, yp,
-                                      ctypes.byref(tol), ctypes.c_void_p(sth.data_ptr()), 1))
-        yh.copy_(torch.from_numpy(y0))
-        if dist:
-            dist.barrier()
-        t = time.perf_counter()
-        for k in range(args.steps):
-            P.api.check(L.bode_int_driver(ctypes.byref(prob), 0, ar, 0.0 + (k % 10) * 0.1,
-                                          0.0 + (k % 10 + 1) * 0.1, num, None, yp,
-                                          ctypes.byref(tol), ctypes.c_void_p(sth.data_ptr()), 1))
-        e2e_s = time.perf_counter() - t
-        if dist:
-            tt = torch.tensor([e2e_s], device=red_dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = float(tt.item())
-        e2e = {"value": world * num * args.steps / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": num * 28 * 8, "d2h_bytes_per_step": num * (28 * 8 + 64),
-               "ms_per_step": e2e_s / args.steps * 1e3, "pinned_host": True}
-        # the paper's intDriver(t, tEnd, numODE, gGlobal, yGlobal) exactly: y in and
-        # out, no per-system stats requested (stats = NULL), same windows
-        yh.copy_(torch.from_numpy(y0))
-        if dist:
-            dist.barrier()
-        t = time.perf_counter()
-        for k in range(args.steps):
-            P.api.check(L.bode_int_driver(ctypes.byref(prob), 0, ar, 0.0 + (k % 10) * 0.1,
-                                          0.0 + (k % 10 + 1) * 0.1, num, None, yp,
-                                          ctypes.byref(tol), None, 1))
-        pp_s = time.perf_counter() - t
-        if dist:
-            tt = torch.tensor([pp_s], device=red_dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            pp_s = float(tt.item())
-        e2e["paper_protocol_no_stats"] = {
-            "value": world * num * args.steps / pp_s, "unit": UNIT,
-            "h2d_bytes_per_step": num * 28 * 8, "d2h_bytes_per_step": num * 28 * 8,
-            "ms_per_step": pp_s / args.steps * 1e3}
-        # the same 10-window protocol through bode_outer_loop (batchode::outerLoop's
-        # drop-in): host buffers in and out, the state resident in HBM between
-        # windows, so one H2D and one D2H per call instead of per window
-        steps_out = ctypes.c_int32(0)
-        P.api.check(L.bode_outer_loop(ctypes.byref(prob), 0, ar, 0.0, 0.2, 0.1, num, None, yp,
-                                      ctypes.byref(tol), ctypes.c_void_p(sth.data_ptr()), 1,
-                                      P.api.SINK(), None, ctypes.byref(steps_out)))  # warm-up
-        yh.copy_(torch.from_numpy(y0))
-        if dist:
-            dist.barrier()
-        t = time.perf_counter()
-        P.api.check(L.bode_outer_loop(ctypes.byref(prob), 0, ar, 0.0, 1.0, 0.1, num, None, yp,
-                                      ctypes.byref(tol), ctypes.c_void_p(sth.data_ptr()), 1,
-                                      P.api.SINK(), None, ctypes.byref(steps_out)))
-        ol_s = time.perf_counter() - t
-        if dist:
-            tt = torch.tensor([ol_s], device=red_dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ol_s = float(tt.item())
-        e2e["outer_loop"] = {"value": world * num * steps_out.value / ol_s, "unit": UNIT,
-                             "windows": steps_out.value, "ms_total": ol_s * 1e3,
-                             "h2d_bytes_per_call": num * 28 * 8,
-                             "d2h_bytes_per_call": num * (28 * 8 + 64)}
-
-    def secondary(problem, solver, arith, dim, y0s, g0s, label, steps, repack=False,
-                  presort_row=None):
-        sec, perw, sts, _, _ = measure_device(P, A, torch, problem, solver, arith, dim, y0s, g0s,
-                                               steps, 1, stream, repack=repack,
-                                               presort_row=presort_row)
-        f = algorithmic_flops(problem, solver, dim, sts, steps)
-        n = y0s.size // dim
-        return {"workload": label, "value": world * n * steps / secs_max(sec),
-                "unit": UNIT, "ms_per_step": sec / steps * 1e3,
-                "achieved_tflops": f / sec / 1e12, "frac_of_fp64_peak": f / sec / peak.value,
-                "flop_per_system_window": f / (n * steps),
-                "kernel_ms_per_window": [round(x, 4) for x in perw]}
-
     def secs_max(sec):
         if not dist:
             return sec
@@ -474,54 +480,174 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         return float(tt.item())
 
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    peak = ctypes.c_double()
+    psec = ctypes.c_double()
+    P.api.check(L.bode_selftest_fp64_peak(ctypes.byref(peak), ctypes.byref(psec)))
+
+    # ---- headline: RKCK Pleiades, this rank's contiguous shard of args.num ----
+    total = args.num
+    b, e = D.shard_range(total, world, rank)
+    num = e - b
+    y0 = gen_states(L, PLEIADES_IC, 0.01, 42, b, num)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        secs, per, stats, launches, _ = measure_device(P, A, torch, "pleiades", "rkck",
+                                                       args.arith, 28, y0, None, args.steps,
+                                                       args.warmup, stream)
+    torch.cuda.synchronize()
+    barrier()
+    secs = secs_max(secs)
+    value = total * args.steps / secs
+    flops = algorithmic_flops("pleiades", "rkck", 28, stats, args.steps)
+    achieved = flops / sum(p / 1e3 for p in per)
+
+    # ---- e2e through the host-pointer C ABI (pinned buffers, H2D+D2H every window) ----
+    e2e = None
+    if not args.no_e2e:
+        with gpu_local_memory(torch, local):
+            yh = torch.from_numpy(y0).pin_memory()
+            sth = torch.zeros(num * 8, dtype=torch.int64).pin_memory()
+            yg = (torch.empty(total * 28, dtype=torch.float64).pin_memory()
+                  if world > 1 and rank == 0 else None)
+        y0t = torch.from_numpy(y0)
+        yp = ctypes.cast(yh.data_ptr(), ctypes.POINTER(ctypes.c_double))
+        prob = A.make_problem(A.PLEIADES)
+        tol = A.default_tol()
+        ar = A.ARITH_NAMES[args.arith]
+
+        def e2e_run(with_stats):
+            """K windows through bode_int_driver with the bench schedule; the
+            host restore of y0 every 10 steps is outside the timed calls. For
+            N > 1 the final gather of every shard to rank 0 is timed too."""
+            stp = ctypes.c_void_p(sth.data_ptr()) if with_stats else None
+            for k in range(min(args.warmup, 1)):  # warm the pinned pipeline
+                P.api.check(L.bode_int_driver(ctypes.byref(prob), 0, ar, *window_bounds(k), num,
+                                              None, yp, ctypes.byref(tol), stp, 1))
+            dt = 0.0
+            for k in range(args.steps):
+                if k % CYCLE == 0:
+                    yh.copy_(y0t)
+                barrier()
+                t = time.perf_counter()
+                P.api.check(L.bode_int_driver(ctypes.byref(prob), 0, ar, *window_bounds(k), num,
+                                              None, yp, ctypes.byref(tol), stp, 1))
+                dt += time.perf_counter() - t
+            gather_s = 0.0
+            if world > 1:
+                barrier()
+                t = time.perf_counter()
+                D.gather_soa_to_rank0(torch, dist, yh, 28, total, yg)
+                gather_s = time.perf_counter() - t
+            return secs_max(dt + gather_s), gather_s
+
+        e2e_s, gather_s = e2e_run(True)
+        gbytes = total * 28 * 8 if world > 1 else 0
+        e2e = {"value": total * args.steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": num * 28 * 8,
+               "d2h_bytes_per_step": num * (28 * 8 + 64) + gbytes // max(args.steps, 1),
+               "ms_per_step": e2e_s / args.steps * 1e3, "pinned_host": True,
+               "api": "bode_int_driver (host pointers, per-window H2D/kernel/D2H pipeline)"}
+        if world > 1:
+            e2e["gather"] = {"ms": gather_s * 1e3, "bytes": gbytes,
+                             "how": "shards to rank 0 over NCCL, one D2H of the global SoA"}
+        # the paper's intDriver(t, tEnd, numODE, gGlobal, yGlobal) exactly: y in and
+        # out, no per-system stats requested (stats = NULL), same windows
+        pp_s, _ = e2e_run(False)
+        e2e["paper_protocol_no_stats"] = {
+            "value": total * args.steps / pp_s, "unit": UNIT,
+            "h2d_bytes_per_step": num * 28 * 8, "d2h_bytes_per_step": num * 28 * 8,
+            "ms_per_step": pp_s / args.steps * 1e3}
+        # one [0, 1] protocol through bode_outer_loop (batchode::outerLoop's
+        # drop-in): host buffers in and out, the state resident in HBM between
+        # windows, so one H2D and one D2H per call instead of per window
+        steps_out = ctypes.c_int32(0)
+        P.api.check(L.bode_outer_loop(ctypes.byref(prob), 0, ar, 0.0, 0.2, 0.1, num, None, yp,
+                                      ctypes.byref(tol), ctypes.c_void_p(sth.data_ptr()), 1,
+                                      P.api.SINK(), None, ctypes.byref(steps_out)))  # warm-up
+        yh.copy_(y0t)
+        barrier()
+        t = time.perf_counter()
+        P.api.check(L.bode_outer_loop(ctypes.byref(prob), 0, ar, 0.0, 1.0, 0.1, num, None, yp,
+                                      ctypes.byref(tol), ctypes.c_void_p(sth.data_ptr()), 1,
+                                      P.api.SINK(), None, ctypes.byref(steps_out)))
+        ol_s = secs_max(time.perf_counter() - t)
+        e2e["outer_loop"] = {"value": total * steps_out.value / ol_s, "unit": UNIT,
+                             "windows": steps_out.value, "ms_total": ol_s * 1e3,
+                             "h2d_bytes_per_call": num * 28 * 8,
+                             "d2h_bytes_per_call": num * (28 * 8 + 64)}
+        del yh, sth, yg
+
+    # ---- secondaries: the other configs, each over this rank's shard ----
+    skipped = []
+
+    def secondary(key, problem, solver, arith, dim, make, n_total, label, steps, repack=False,
+                  presort_row=None):
+        if time.monotonic() - T_START > args.budget_s:
+            skipped.append(key)
+            return
+        sb, se = D.shard_range(n_total, world, rank)
+        y0s, g0s = make(sb, se - sb)
+        sec, perw, sts, _, _ = measure_device(P, A, torch, problem, solver, arith, dim, y0s, g0s,
+                                              steps, 1, stream, repack=repack,
+                                              presort_row=presort_row)
+        f = algorithmic_flops(problem, solver, dim, sts, steps)
+        n = se - sb
+        extra[key] = {"workload": label, "value": n_total * steps / secs_max(sec),
+                      "unit": UNIT, "systems": n_total, "windows": steps,
+                      "ms_per_step": sec / steps * 1e3,
+                      "achieved_tflops": f / sec / 1e12, "frac_of_fp64_peak": f / sec / peak.value,
+                      "flop_per_system_window": f / (n * steps),
+                      "kernel_ms_per_window": [round(x, 4) for x in perw]}
+
     extra = {}
+    w10 = min(args.steps, CYCLE)
     if args.secondary:
-        extra["rkck_exact"] = secondary(
-            "pleiades", "rkck", "exact", 28, y0, None,
-            f"RKCK Pleiades, {num} systems, EXACT policy (bitwise reference arithmetic)",
-            args.steps)
+        pl = lambda mag, seed: (lambda b0, n: (gen_states(L, PLEIADES_IC, mag, seed, b0, n), None))
+        secondary("rkck_exact", "pleiades", "rkck", "exact", 28, pl(0.01, 42), total,
+                  f"RKCK Pleiades, {total} systems, EXACT policy (bitwise reference arithmetic)",
+                  args.steps)
+        heat = lambda b0, n: (gen_states(L, heat_ic(64), 0.01, 42, b0, n), None)
         if args.rkc_num > 0:
-            yh0 = perturb(heat_ic(64), 0.01, 42 + rank, args.rkc_num)
-            extra["rkc_heat64"] = secondary(
-                "heat", "rkc", "exact", 64, yh0, None,
-                f"RKC heat n=64 (config 3), {args.rkc_num} systems, EXACT", min(args.steps, 10))
-            ye0 = perturb(np.array([1.0]), 0.01, 42 + rank, args.rkc_num)
-            g0 = stiffness_params(args.rkc_num)
-            extra["rkc_stiff_expdecay"] = secondary(
-                "expdecay", "rkc", "exact", 1, ye0, g0,
-                f"RKC expDecay, g0 log-uniform in [1,1e4] (config 4), {args.rkc_num} systems, EXACT",
-                min(args.steps, 10))
+            secondary("rkc_heat64", "heat", "rkc", "exact", 64, heat, args.rkc_num,
+                      f"RKC heat n=64 (config 3/5), {args.rkc_num} systems, EXACT", w10)
+            secondary("rkc_heat64_fast", "heat", "rkc", "fast", 64, heat, args.rkc_num,
+                      f"RKC heat n=64 (config 3/5), {args.rkc_num} systems, FAST", w10)
+        if args.aux_num > 0:
+            na = args.aux_num
+            for ar_ in ("fast", "exact"):
+                secondary(f"rkck_stress_{ar_}", "pleiades", "rkck", ar_, 28, pl(0.1, 42), na,
+                          f"RKCK Pleiades perturb 0.1 (config 2 divergence stress), {na} "
+                          f"systems, {ar_.upper()}", w10)
+            expd = lambda b0, n: (gen_states(L, np.array([1.0]), 0.01, 42, b0, n),
+                                  stiffness_range(b0, n))
+            secondary("rkc_stiff_expdecay", "expdecay", "rkc", "exact", 1, expd, na,
+                      f"RKC expDecay, g0 log-uniform in [1,1e4] (config 4), {na} systems, "
+                      f"EXACT, natural order", w10)
             # the same natural-order batch, re-packed by its window-1 cost
             # (bode_repack_by_cost) and restored at the end, inside the timing
-            extra["rkc_stiff_expdecay_repacked"] = secondary(
-                "expdecay", "rkc", "exact", 1, ye0, g0,
-                f"RKC expDecay, config 4 batch (natural order) re-packed by cost after window "
-                f"1, {args.rkc_num} systems, EXACT", min(args.steps, 10), repack=True)
-            # the same natural-order batch sorted by |g0| (its spectral radius, the
-            # reference's specRadHint) before window 1 (bode_repack_by_param) and
-            # restored at the end, inside the timing
-            extra["rkc_stiff_expdecay_presorted"] = secondary(
-                "expdecay", "rkc", "exact", 1, ye0, g0,
-                f"RKC expDecay, config 4 batch (natural order) sorted by |g0| before window 1, "
-                f"{args.rkc_num} systems, EXACT", min(args.steps, 10), presort_row=0)
-            # the same batch with the systems sorted by stiffness (SURVEY 8d config 4:
-            # shuffled and sorted): warps then hold similar stage counts
-            order = np.argsort(g0, kind="stable")
-            extra["rkc_stiff_expdecay_sorted"] = secondary(
-                "expdecay", "rkc", "exact", 1, ye0[order], g0[order],
-                f"RKC expDecay, config 4 batch sorted by g0, {args.rkc_num} systems, EXACT",
-                min(args.steps, 10))
-            yb0 = perturb(brusselator_ic(32), 0.01, 7 + rank, args.rkc_num)
-            gb0 = brusselator_params(args.rkc_num, 0.02, 0.5)
-            gbn = brusselator_params(args.rkc_num, 0.002, 0.02)
-            extra["rkck_brusselator_fast"] = secondary(
-                "brusselator", "rkck", "fast", 64, yb0, gbn,
-                f"RKCK FAST Brusselator n=32 (registered problem, generic RKCK kernel), alpha "
-                f"log-spaced in [0.002, 0.02], {args.rkc_num} systems", min(args.steps, 10))
-            extra["rkc_brusselator"] = secondary(
-                "brusselator", "rkc", "exact", 64, yb0, gb0,
-                f"RKC Brusselator reaction-diffusion n=32 (dim 64, registered problem), alpha "
-                f"log-spaced in [0.02, 0.5], {args.rkc_num} systems, EXACT", min(args.steps, 10))
+            secondary("rkc_stiff_expdecay_repacked", "expdecay", "rkc", "exact", 1, expd, na,
+                      f"RKC expDecay config 4 batch re-packed by cost after window 1, {na} "
+                      f"systems, EXACT", w10, repack=True)
+            # sorted by |g0| (its spectral radius, the reference's specRadHint)
+            # before window 1 (bode_repack_by_param), restored at the end, timed
+            secondary("rkc_stiff_expdecay_presorted", "expdecay", "rkc", "exact", 1, expd, na,
+                      f"RKC expDecay config 4 batch sorted by |g0| before window 1, {na} "
+                      f"systems, EXACT", w10, presort_row=0)
+            bru = lambda lo, hi: (lambda b0, n: (
+                gen_states(L, brusselator_ic(32), 0.01, 7, b0, n),
+                brusselator_params(na, lo, hi).reshape(3, na)[:, b0:b0 + n].copy().reshape(-1)))
+            secondary("rkck_brusselator_fast", "brusselator", "rkck", "fast", 64,
+                      bru(0.002, 0.02), na,
+                      f"RKCK FAST Brusselator n=32 (registered problem, generic RKCK kernel), "
+                      f"alpha log-spaced in [0.002, 0.02], {na} systems", w10)
+            secondary("rkc_brusselator", "brusselator", "rkc", "exact", 64, bru(0.02, 0.5), na,
+                      f"RKC Brusselator reaction-diffusion n=32 (dim 64, registered problem), "
+                      f"alpha log-spaced in [0.02, 0.5], {na} systems, EXACT", w10)
 
     if rank != 0:
         if dist:
@@ -531,17 +657,8 @@ def main():
     traffic, traffic_src, ncu_evidence = measured_traffic(
         "rkck_fast" if args.arith == "fast" else "rkck_exact", num)
     cpu = None
-    if not args.no_cpu:
-        rate, cores, kind, dt = cpu_reference_rate("pleiades", "rkck", PLEIADES_IC, 0.01, 42,
-                                                   args.cpu_sample, 10)
-        rate1, _, _, dt1 = cpu_reference_rate("pleiades", "rkck", PLEIADES_IC, 0.01, 42,
-                                              max(1024, args.cpu_sample // 16), 10, threads=1)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
-               "sample": f"{args.cpu_sample} Pleiades systems x 10 windows ([0,1]), all host "
-                         f"threads, {dt:.2f} s",
-               "one_thread": {"value": rate1, "unit": UNIT, "cores": 1,
-                              "sample": f"{max(1024, args.cpu_sample // 16)} systems x 10 "
-                                        f"windows, {dt1:.2f} s"}}
+    if not args.no_cpu and time.monotonic() - T_START < args.budget_s:
+        cpu = cpu_leg(args, P, A, torch, stream, extra)
 
     clocks = clk.summary()
     # nominal FP64 FMA peak at the SM clock observed during the timed region:
@@ -551,13 +668,17 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"RKCK Pleiades (N=28), {num} systems per GPU, perturb 0.01 "
-                               f"seed 42+rank, eps 1e-10, window 0.1 (restart)",
-                   "arith": args.arith, "systems_per_gpu": num, "window": 0.1,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"RKCK Pleiades (N=28), {total} systems in total (config 5; "
+                               f"configs[1]'s workload at 2^24), perturb 0.01 seed 42, eps "
+                               f"1e-10; step k = window (k mod 10) of [0, 1] (restart), y0 "
+                               f"restored every 10 steps",
+                   "arith": args.arith, "systems": total, "systems_per_gpu": num,
+                   "window": 0.1,
                    "scheduling": "persistent refill" if args.persistent else "static",
                    "l2": "state (num*28*8 B) exceeds the 126 MB L2; no flush needed",
-                   "parallelism": f"dp{world} (independent shards, no collective)"},
+                   "parallelism": f"dp{world} (contiguous shards, no collective; final gather "
+                                  f"to rank 0 in e2e)"},
         "roofline": {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak.value / 1e12,
                      "unit": "TFLOP/s", "frac": achieved / peak.value, "traffic": traffic,
                      "traffic_source": traffic_src, "ncu": ncu_evidence,
@@ -574,10 +695,67 @@ def main():
         "work_per_system_window": {
             "attempts": float((stats["steps_accepted"] + stats["steps_rejected"]).sum()) / (num * args.steps),
             "rhs_evals": float(stats["rhs_evals"].sum()) / (num * args.steps)},
+        "skipped_over_budget": skipped,
+        "wall_s": time.monotonic() - T_START,
     }
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def cpu_leg(args, P, A, torch, stream, extra):
+    """The reference CPU path on this host for every config the line reports
+    (2^16 systems, [0, 1] in 10 windows, one warm-up window,
+    best of 3), and -- as the checker, not as the thing measured -- the GPU's
+    agreement with it on the config-2 stress sample under both policies."""
+    from golden_cases import PLEIADES_IC, heat_ic
+    n = args.cpu_sample
+    rate, cores, kind, dt, _, _ = cpu_reference("pleiades", "rkck", PLEIADES_IC, 0.01, 42, n)
+    n1 = max(1024, n // 16)
+    rate1, _, _, dt1, _, _ = cpu_reference("pleiades", "rkck", PLEIADES_IC, 0.01, 42, n1,
+                                           threads=1, repeats=1)
+    cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
+           "sample": f"{n} Pleiades systems x 10 windows ([0,1]) via outerLoop, all host "
+                     f"threads, one warm-up window, best of 3: {dt:.2f} s",
+           "one_thread": {"value": rate1, "unit": UNIT, "cores": 1,
+                          "sample": f"{n1} systems x 10 windows, {dt1:.2f} s"},
+           "configs": {}}
+    heat_n = n
+    for key, prob, solver, base, mag, ns, g, gpu_key in (
+            ("rkc_heat64", "heat", "rkc", heat_ic(64), 0.01, heat_n, None, "rkc_heat64"),
+            ("rkc_stiff_expdecay", "expdecay", "rkc", np.array([1.0]), 0.01, n,
+             stiffness_range(0, n), "rkc_stiff_expdecay_presorted"),
+            ("rkck_stress", "pleiades", "rkck", PLEIADES_IC, 0.1, n, None, "rkck_stress_fast")):
+        if time.monotonic() - T_START > args.budget_s:
+            break
+        r, c, k, d, yref, sref = cpu_reference(prob, solver, base, mag, 42, ns, g=g)
+        ent = {"value": r, "unit": UNIT, "cores": c, "kind": k,
+               "sample": f"{ns} systems x 10 windows, one warm-up window, best of 3: {d:.2f} s"}
+        if gpu_key in extra:
+            ent["gpu_over_cpu"] = extra[gpu_key]["value"] / r
+        if key == "rkck_stress":
+            ent["parity"] = stress_parity(P, A, torch, stream, base, mag, ns, yref, sref)
+        cpu["configs"][key] = ent
+    return cpu
+
+
+def stress_parity(P, A, torch, stream, base, mag, num, yref, sref):
+    """Config-2 stress (perturb 0.1): per-system max-norm relative error of
+    the GPU's [0, 1] result against the reference's, and count agreement,
+    under both policies (north_star bar: 1e-3 * eps = 1e-13)."""
+    out = {}
+    y0 = gen_states(P.lib(), base, mag, 42, 0, num)
+    for arith in ("fast", "exact"):
+        _, _, st, _, y = measure_device(P, A, torch, "pleiades", "rkck", arith, 28, y0, None,
+                                        CYCLE, 0, stream, return_state=True)
+        err = sysrel(y, yref, num, 28)
+        same = np.ones(num, bool)
+        for k in ("steps_accepted", "steps_rejected", "rhs_evals", "underflow"):
+            same &= st[k] == sref[k]
+        out[arith] = {"systems": num, "within_1e-13": float(((err <= 1e-13) & same).mean()),
+                      "max_rel_err": float(err.max()), "count_mismatches": int((~same).sum()),
+                      "bitwise": bool(np.array_equal(y.view(np.uint64), yref.view(np.uint64)))}
+    return out
 
 
 if __name__ == "__main__":

@@ -109,6 +109,8 @@ def lib():
         "bode_splitmix64_at": (c_u64, [c_u64, c_u64]),
         "bode_unit_symmetric_at": (c_d, [c_u64, c_u64]),
         "bode_perturb_initial_conditions": (ctypes.c_int, [PD, c_i32, c_d, c_u64, c_i64, PD]),
+        "bode_perturb_initial_conditions_range": (ctypes.c_int, [PD, c_i32, c_d, c_u64, c_i64,
+                                                                 c_i64, PD]),
         "bode_pleiades_ic": (None, [PD]),
         "bode_heat_initial_condition": (None, [c_i32, PD]),
         "bode_selftest_cbrt": (ctypes.c_int, [PD, PD, c_i64]),

@@ -993,16 +993,26 @@ double bode_unit_symmetric_at(uint64_t seed, uint64_t k) {
 
 int bode_perturb_initial_conditions(const double* base, int32_t dim, double magnitude,
                                     uint64_t seed, int64_t count, double* out) {
+    return bode_perturb_initial_conditions_range(base, dim, magnitude, seed, 0, count, out);
+}
+
+// Systems [first, first + count) of the reference's perturbation stream
+// (counter k = i*dim + j, problems.cpp:175-187) as a local SoA array of
+// `count` columns: a rank builds exactly its own shard of a global batch.
+int bode_perturb_initial_conditions_range(const double* base, int32_t dim, double magnitude,
+                                          uint64_t seed, int64_t first, int64_t count,
+                                          double* out) {
     if (count < 1) return fail(BODE_E_INVALID_SHAPE, "perturbInitialConditions: count must be positive");
+    if (first < 0) return fail(BODE_E_INVALID_SHAPE, "perturbInitialConditions: negative first system");
     if (dim < 1 || base == nullptr) return fail(BODE_E_INVALID_SHAPE, "perturbInitialConditions: empty base state");
     if (!(magnitude >= 0.0 && magnitude <= 0.1))
         return fail(BODE_E_INVALID_SHAPE, "perturbInitialConditions: magnitude outside [0, 0.1]");
     const unsigned hw = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
     const int64_t workers = std::min<int64_t>(hw, std::max<int64_t>(1, count / 65536));
     auto body = [&](int64_t lo, int64_t hi) {
-        for (int64_t i = lo; i < hi; ++i)
-            for (int j = 0; j < dim; ++j) {
-                const uint64_t k = static_cast<uint64_t>(i) * static_cast<uint64_t>(dim) + j;
+        for (int j = 0; j < dim; ++j)
+            for (int64_t i = lo; i < hi; ++i) {
+                const uint64_t k = static_cast<uint64_t>(first + i) * static_cast<uint64_t>(dim) + j;
                 const double u = bode_unit_symmetric_at(seed, k);
                 out[i + count * j] = base[j] * (1.0 + u * magnitude);
             }

@@ -94,3 +94,86 @@ def test_gloo_world2_matches_single_process(oracle):
     assert np.array_equal(y.view(np.uint64), y_ref.view(np.uint64))
     for k in ("steps_accepted", "steps_rejected", "rhs_evals", "h_min_seen", "h_max_seen"):
         assert np.array_equal(st[k], st_ref[k]), k
+
+
+def _gather_worker(rank, world, port, num, dim, q):
+    import torch
+    import torch.distributed as dist
+    from paper_1611_02274_b200.dist import gather_soa_to_rank0, shard_range
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    b, e = shard_range(num, world, rank)
+    y = np.arange(num * dim, dtype=np.float64).reshape(dim, num)
+    loc = torch.from_numpy(np.ascontiguousarray(y[:, b:e]).reshape(-1))
+    out = gather_soa_to_rank0(torch, dist, loc, dim, num)
+    if rank == 0:
+        q.put(out.numpy().copy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _empty_shard_worker(rank, world, port, q):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path.insert(0, here)
+    import torch.distributed as dist
+    from golden_cases import PLEIADES_IC, perturb
+    from oracle_lib import Oracle
+    from paper_1611_02274_b200 import _abi as A
+    from paper_1611_02274_b200.dist import integrate_sharded
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    O = Oracle()
+    prob = A.make_problem(A.PLEIADES)
+    y0 = perturb(PLEIADES_IC, 0.01, 3, 2)
+    calls = []
+
+    def local(y_loc, g_loc):
+        calls.append(y_loc.size)
+        rc, y, st, _ = O.outer_loop(prob, A.SOLVER_RKCK, 0.0, 0.1, 0.1, y_loc, threads=1)
+        assert rc == 0
+        return y, st
+
+    y, st = integrate_sharded(local, y0, None, 2, 28, 0)
+    assert (rank < 2) == bool(calls)  # the empty shard never integrates
+    if rank == 0:
+        q.put((y, st))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _spawn(target, world, *args):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, *args, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    return out
+
+
+@pytest.mark.parametrize("world,num", [(2, 301), (3, 2)])
+def test_gather_soa_to_rank0_gloo(world, num):
+    """The final result gather used by bench.py's multi-rank e2e: ragged and
+    empty shards land in the global SoA layout byte for byte."""
+    dim = 5
+    out = _spawn(_gather_worker, world, num, dim)
+    assert np.array_equal(out, np.arange(num * dim, dtype=np.float64))
+
+
+def test_integrate_sharded_empty_shard_gloo(oracle):
+    """world > num: the rank with no systems skips the integration."""
+    from golden_cases import PLEIADES_IC, perturb
+    from paper_1611_02274_b200 import _abi as A
+    y, st = _spawn(_empty_shard_worker, 3)
+    y0 = perturb(PLEIADES_IC, 0.01, 3, 2)
+    rc, y_ref, st_ref, _ = oracle.outer_loop(A.make_problem(A.PLEIADES), A.SOLVER_RKCK, 0.0, 0.1,
+                                             0.1, y0)
+    assert np.array_equal(y.view(np.uint64), y_ref.view(np.uint64))
+    assert np.array_equal(st["rhs_evals"], st_ref["rhs_evals"])

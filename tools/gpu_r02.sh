@@ -1,0 +1,22 @@
+#!/bin/bash
+# Round-2 GPU session helper. Usage (under gpurun): bash tools/gpu_r02.sh <tag> [parts...]
+set -u
+TAG=${1:-r02}; shift || true
+PARTS=${*:-"tests bench"}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi > $OUT/nvidia-smi.txt 2>&1
+nproc > $OUT/nproc.txt
+for p in $PARTS; do
+  case $p in
+    tests) timeout 900 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $OUT/status.txt ;;
+    smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1; echo "smoke rc=$?" >> $OUT/status.txt ;;
+    bench) /usr/bin/time -v timeout 1700 python3 bench.py --gpus 1 --steps 20 --warmup 5 > $OUT/bench.txt 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/status.txt ;;
+    ref) timeout 600 python3 bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $OUT/bench_ref.txt 2>&1; echo "ref rc=$?" >> $OUT/status.txt ;;
+    multirank)
+      BODE_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+        --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 12 --warmup 3 \
+        --systems 1048576 --rkc-systems 65536 --aux-systems 65536 --no-cpu > $OUT/bench_2rank.txt 2>&1
+      echo "multirank rc=$?" >> $OUT/status.txt ;;
+  esac
+done
