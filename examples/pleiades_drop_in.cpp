@@ -1,7 +1,7 @@
 // pleiades_drop_in.cpp -- the reference's Pleiades protocol (bench.cpp:89-119,
 // PAPER.md:652) written against the bode:: drop-in API instead of batchode::.
 //
-//   build: g++ -std=c++17 -O2 -Iinclude examples/pleiades_drop_in.cpp \
+//   build: g++ -std=c++20 -O2 -Iinclude examples/pleiades_drop_in.cpp \
 //              -Lpaper_1611_02274_b200/lib -lbode -Wl,-rpath,... -o pleiades_drop_in
 //   run:   ./pleiades_drop_in [numSystems]   (prints a checksum line per window)
 #include <cstdio>
@@ -26,8 +26,8 @@ int main(int argc, char** argv) {
             });
         long accepted = 0, rejected = 0;
         for (const auto& st : res.stats) {
-            accepted += st.steps_accepted;
-            rejected += st.steps_rejected;
+            accepted += st.stepsAccepted;
+            rejected += st.stepsRejected;
         }
         std::printf("systems=%d windows=%d accepted=%ld rejected=%ld x1[0]=%.17g\n", num,
                     res.outerSteps, accepted, rejected, res.states.at(0, 0));

@@ -96,11 +96,40 @@ def build_examples(verbose: bool = True):
             f.write(r.stderr)
         if verbose:
             print(f"[bode build] built {so}", flush=True)
+    # test programs (tests/cpp): device problem libraries, then C++ tests linked
+    # against libbode and those libraries
+    test_libs = []
+    for src in glob.glob(os.path.join(repo, "tests", "cpp", "*.cu")):
+        name = os.path.splitext(os.path.basename(src))[0]
+        so = os.path.join(LIB_DIR, "libtest_" + name + ".so")
+        test_libs.append("test_" + name)
+        if not _stale(so, [src, SO] + _headers() + [os.path.join(INCLUDE, "bode_problem.cuh")]):
+            continue
+        cmd = [NVCC, *ARCH, *FLAGS, "-shared", src, "-L", LIB_DIR, "-lbode",
+               "-Xlinker", f"-rpath,{LIB_DIR}", "-Xlinker", "-rpath,$ORIGIN", "-o", so]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"test problem library build failed for {src}:\n{r.stderr}")
+        if verbose:
+            print(f"[bode build] built {so}", flush=True)
+    for src in glob.glob(os.path.join(repo, "tests", "cpp", "*.cpp")):
+        exe = os.path.join(LIB_DIR, os.path.splitext(os.path.basename(src))[0])
+        libs = [os.path.join(LIB_DIR, "lib" + l + ".so") for l in test_libs]
+        if not _stale(exe, [src, SO, os.path.join(INCLUDE, "bode.hpp")] + libs):
+            continue
+        cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", INCLUDE, src, "-L", LIB_DIR,
+               "-Wl,--no-as-needed", *[f"-l{l}" for l in test_libs], "-Wl,--as-needed",
+               "-lbode", f"-Wl,-rpath,{LIB_DIR}", "-Wl,-rpath,$ORIGIN", "-o", exe]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"test program build failed for {src}:\n{r.stderr}")
+        if verbose:
+            print(f"[bode build] built {exe}", flush=True)
     for src in glob.glob(os.path.join(repo, "examples", "*.cpp")):
         exe = os.path.join(LIB_DIR, os.path.splitext(os.path.basename(src))[0])
         if not _stale(exe, [src, SO, os.path.join(INCLUDE, "bode.hpp")]):
             continue
-        cmd = ["g++", "-std=c++17", "-O2", "-I", INCLUDE, src, "-L", LIB_DIR, "-lbode",
+        cmd = ["g++", "-std=c++20", "-O2", "-I", INCLUDE, src, "-L", LIB_DIR, "-lbode",
                f"-Wl,-rpath,{LIB_DIR}", "-Wl,-rpath,$ORIGIN", "-o", exe]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -14,11 +14,13 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -341,21 +343,118 @@ int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double*
 
 constexpr int kMaxChunks = 32;  // host-pointer pipeline depth per shard
 
-// Per-device buffers reused across calls (no cudaMalloc on the hot path once warm).
-struct DeviceBuffers {
-    std::mutex m;
+// Device buffers, streams and events of one shard, leased exclusively for one
+// call: concurrent or nested calls (from another host thread, or from a sink)
+// never share state, and several shards may live on one device. Leases are
+// pooled per device, so a warm call does no cudaMalloc.
+struct Lease {
+    int device = 0;
     double* y = nullptr;
     double* g = nullptr;
     DevStats* st = nullptr;
-    size_t y_cap = 0, g_cap = 0, st_cap = 0;
     long long* ord = nullptr;  // outer loop: position -> original index after re-packing
-    double* ysnap = nullptr;   // outer loop: snapshot in original order
-    size_t ord_cap = 0, ysnap_cap = 0;
+    double* ysnap[2] = {nullptr, nullptr};  // outer loop: staged snapshots (caller's order)
+    size_t y_cap = 0, g_cap = 0, st_cap = 0, ord_cap = 0, ysnap_cap[2] = {0, 0};
     cudaStream_t streams[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
     cudaEvent_t events[2 * kMaxChunks] = {};                 // per chunk: H2D done, kernel done
+    cudaEvent_t snap_ready[2] = {};   // snapshot slot staged in ysnap (compute stream)
+    cudaEvent_t snap_copied[2] = {};  // snapshot slot's D2H finished (D2H stream)
 };
 
-DeviceBuffers g_dev[64];
+class LeasePool {
+  public:
+    // On the caller's current device (== device).
+    int acquire(int device, Lease** out) {
+        {
+            std::lock_guard<std::mutex> lock(m_);
+            if (!free_[device].empty()) {
+                *out = free_[device].back();
+                free_[device].pop_back();
+                return BODE_OK;
+            }
+        }
+        Lease* L = new Lease;
+        L->device = device;
+        for (auto& s : L->streams)
+            BODE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        for (auto& ev : L->events) BODE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        for (int i = 0; i < 2; ++i) {
+            BODE_CUDA(cudaEventCreateWithFlags(&L->snap_ready[i], cudaEventDisableTiming));
+            BODE_CUDA(cudaEventCreateWithFlags(&L->snap_copied[i], cudaEventDisableTiming));
+        }
+        *out = L;
+        return BODE_OK;
+    }
+    void release(Lease* L) {
+        // nothing may still be in flight on a lease handed to the next caller
+        // (error paths return early)
+        cudaSetDevice(L->device);
+        for (auto& s : L->streams) cudaStreamSynchronize(s);
+        std::lock_guard<std::mutex> lock(m_);
+        free_[L->device].push_back(L);
+    }
+
+  private:
+    std::mutex m_;
+    std::vector<Lease*> free_[64];
+};
+
+LeasePool& lease_pool() {
+    static LeasePool* p = new LeasePool();  // outlives static destructors
+    return *p;
+}
+
+struct LeaseGuard {
+    Lease* L = nullptr;
+    LeaseGuard() = default;
+    LeaseGuard(const LeaseGuard&) = delete;
+    LeaseGuard& operator=(const LeaseGuard&) = delete;
+    ~LeaseGuard() {
+        if (L) lease_pool().release(L);
+    }
+};
+
+// Pinned host staging for the outer loop's asynchronous snapshots, kept
+// across calls (pinning gigabytes costs far more than a window).
+class PinnedCache {
+  public:
+    int acquire(size_t bytes, void** out) {
+        {
+            std::lock_guard<std::mutex> lock(m_);
+            for (size_t i = 0; i < free_.size(); ++i)
+                if (free_[i].second >= bytes) {
+                    *out = free_[i].first;
+                    sizes_.push_back(free_[i]);
+                    free_.erase(free_.begin() + i);
+                    return BODE_OK;
+                }
+        }
+        void* p = nullptr;
+        BODE_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocPortable));
+        std::lock_guard<std::mutex> lock(m_);
+        sizes_.push_back({p, bytes});
+        *out = p;
+        return BODE_OK;
+    }
+    void release(void* p) {
+        std::lock_guard<std::mutex> lock(m_);
+        for (size_t i = 0; i < sizes_.size(); ++i)
+            if (sizes_[i].first == p) {
+                free_.push_back(sizes_[i]);
+                sizes_.erase(sizes_.begin() + i);
+                return;
+            }
+    }
+
+  private:
+    std::mutex m_;
+    std::vector<std::pair<void*, size_t>> free_, sizes_;  // idle / handed out
+};
+
+PinnedCache& pinned_cache() {
+    static PinnedCache* p = new PinnedCache();
+    return *p;
+}
 
 template <class T>
 int ensure(T** p, size_t* cap, size_t count) {
@@ -382,9 +481,12 @@ struct Shard {
     int64_t begin, count;
 };
 
-// Contiguous shards (batch_driver.cpp:68-73) over `gpus` devices starting at
-// the calling thread's current device, so a one-process-per-GPU caller (torchrun
-// rank r with cuda:r current) and num_gpus = 1 stays on its own GPU.
+// Contiguous shards (batch_driver.cpp:68-73), the reference's `workers`: shard
+// d runs on device (current + d) mod device_count, so a one-process-per-GPU
+// caller (torchrun rank r with cuda:r current) and num_gpus = 1 stays on its
+// own GPU, and num_gpus above the device count puts several shards on one
+// device (as workers above the core count share cores). Results are bitwise
+// independent of the shard count (batch_driver.hpp:16-21).
 std::vector<Shard> make_shards(int64_t num, int gpus) {
     std::vector<Shard> v;
     int cur = 0, n = 1;
@@ -412,14 +514,16 @@ struct DeviceRestore {
     }
 };
 
+constexpr int kMaxShards = 4096;
+
 int check_devices(int gpus) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
         cudaGetLastError();
         return fail(BODE_E_NO_DEVICE, "no CUDA device available (there is no CPU fallback)");
     }
-    if (gpus < 1) return fail(BODE_E_INVALID_SHAPE, "num_gpus must be positive");
-    if (gpus > n) return fail(BODE_E_NO_DEVICE, "num_gpus exceeds the visible device count");
+    if (gpus < 1) return fail(BODE_E_INVALID_SHAPE, "workers (num_gpus) must be positive");
+    if (gpus > kMaxShards) return fail(BODE_E_INVALID_SHAPE, "workers (num_gpus) above 4096");
     if (n > 64) return fail(BODE_E_UNSUPPORTED, "more than 64 visible devices");
     return BODE_OK;
 }
@@ -434,17 +538,14 @@ int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard&
                      int64_t num, const double* g, double* y, bode_stats_t* stats, double t,
                      double tEnd, const DevTol& tol) {
     BODE_CUDA(cudaSetDevice(sh.device));
-    DeviceBuffers& B = g_dev[sh.device];
-    std::lock_guard<std::mutex> lock(B.m);
-    const int N = p->dim, P = p->param_dim;
-    int rc = ensure(&B.y, &B.y_cap, (size_t)sh.count * N);
+    LeaseGuard guard;
+    int rc = lease_pool().acquire(sh.device, &guard.L);
     if (rc) return rc;
+    Lease& B = *guard.L;
+    const int N = p->dim, P = p->param_dim;
+    if ((rc = ensure(&B.y, &B.y_cap, (size_t)sh.count * N))) return rc;
     if (P > 0 && (rc = ensure(&B.g, &B.g_cap, (size_t)sh.count * P))) return rc;
     if (stats && (rc = ensure(&B.st, &B.st_cap, (size_t)sh.count))) return rc;
-    for (auto& s : B.streams)
-        if (!s) BODE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    for (auto& ev : B.events)
-        if (!ev) BODE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
 
     const bool pinned = host_pinned(y);
     const int64_t min_chunk = 1 << 16;
@@ -482,22 +583,108 @@ int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard&
     return BODE_OK;
 }
 
+// Runs f(shard index) for every shard: one host thread per device in use,
+// each taking its device's shards in order.
 template <class F>
 int for_each_shard(const std::vector<Shard>& shards, F&& f) {
-    if (shards.size() == 1) return f(shards[0]);
+    if (shards.size() == 1) return f(size_t(0));
+    std::vector<int> devs;
+    for (const Shard& s : shards)
+        if (std::find(devs.begin(), devs.end(), s.device) == devs.end()) devs.push_back(s.device);
     std::vector<int> rcs(shards.size(), BODE_OK);
     std::vector<std::string> msgs(shards.size());
-    std::vector<std::thread> pool;
-    for (size_t i = 0; i < shards.size(); ++i)
-        pool.emplace_back([&, i] {
-            rcs[i] = f(shards[i]);
-            if (rcs[i]) msgs[i] = g_last_error;
-        });
-    for (auto& th : pool) th.join();
+    auto run_device = [&](int dev) {
+        for (size_t i = 0; i < shards.size(); ++i) {
+            if (shards[i].device != dev) continue;
+            rcs[i] = f(i);
+            if (rcs[i]) {
+                msgs[i] = g_last_error;
+                return;
+            }
+        }
+    };
+    if (devs.size() == 1) {
+        run_device(devs[0]);
+    } else {
+        std::vector<std::thread> pool;
+        for (int d : devs) pool.emplace_back(run_device, d);
+        for (auto& th : pool) th.join();
+    }
     for (size_t i = 0; i < shards.size(); ++i)
         if (rcs[i]) return fail(rcs[i], msgs[i]);
     return BODE_OK;
 }
+
+// Delivers outer-loop snapshots to the caller's sink from one library thread,
+// in window order, while the next windows compute: job k waits for its
+// snapshot's D2H events, then calls sink(t_k, staging). done() tells the
+// producer when a staging slot may be overwritten.
+class SinkWorker {
+  public:
+    struct Job {
+        int64_t k;
+        double t;
+        const double* y;
+        std::vector<std::pair<int, cudaEvent_t>> events;  // (device, D2H done)
+    };
+    SinkWorker(bode_sink_fn fn, void* user, int64_t num, int dim)
+        : fn_(fn), user_(user), num_(num), dim_(dim), th_([this] { loop(); }) {}
+    ~SinkWorker() { finish(); }
+    void push(Job j) {
+        std::lock_guard<std::mutex> lock(m_);
+        q_.push_back(std::move(j));
+        cv_.notify_all();
+    }
+    // blocks until the sink for window k has returned
+    void wait_done(int64_t k) {
+        std::unique_lock<std::mutex> lock(m_);
+        cv_.wait(lock, [&] { return done_ >= k || failed_; });
+    }
+    void finish() {
+        {
+            std::lock_guard<std::mutex> lock(m_);
+            stop_ = true;
+            cv_.notify_all();
+        }
+        if (th_.joinable()) th_.join();
+    }
+    bool failed() const { return failed_; }
+
+  private:
+    void loop() {
+        for (;;) {
+            Job j;
+            {
+                std::unique_lock<std::mutex> lock(m_);
+                cv_.wait(lock, [&] { return stop_ || !q_.empty(); });
+                if (q_.empty()) return;
+                j = std::move(q_.front());
+                q_.pop_front();
+            }
+            bool ok = true;
+            for (auto& de : j.events) {
+                ok = ok && cudaSetDevice(de.first) == cudaSuccess &&
+                     cudaEventSynchronize(de.second) == cudaSuccess;
+            }
+            if (ok) fn_(j.t, j.y, num_, dim_, user_);
+            std::lock_guard<std::mutex> lock(m_);
+            if (!ok) failed_ = true;
+            done_ = j.k;
+            cv_.notify_all();
+        }
+    }
+    bode_sink_fn fn_;
+    void* user_;
+    int64_t num_;
+    int dim_;
+    std::mutex m_;
+    std::condition_variable cv_;
+    std::deque<Job> q_;
+    int64_t done_ = 0;
+    bool stop_ = false;
+    bool failed_ = false;
+    std::thread th_;
+};
 
 }  // namespace
 
@@ -763,8 +950,8 @@ int bode_int_driver(const bode_problem_t* p, int32_t solver, int32_t arith, doub
     const DevTol dt = to_dev(tol);
     DeviceRestore restore;
     const auto shards = make_shards(num, num_gpus);
-    return for_each_shard(shards, [&](const Shard& sh) {
-        return run_shard_window(e, p, sh, num, g, y, stats, t, t_end, dt);
+    return for_each_shard(shards, [&](size_t i) {
+        return run_shard_window(e, p, shards[i], num, g, y, stats, t, t_end, dt);
     });
 }
 
@@ -784,46 +971,76 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
     const int N = p->dim, P = p->param_dim;
     const int64_t nwin = bode_num_windows(t0, t_end, h_outer);
 
-    // Buffers per shard; y stays resident across windows.
-    // With pinned host memory the first window's upload and the last window's
-    // download are pipelined with its kernels in column chunks of the shard's
-    // SoA arrays (launches with a row stride): H2D on streams[0], kernels on
-    // streams[1], D2H on streams[2], chained by per-chunk events.
-    const bool pinned = host_pinned(y);
-    rc = for_each_shard(shards, [&](const Shard& sh) {
+    // One lease per shard for the whole call; y stays resident across windows
+    // (SURVEY 8f row 1). With pinned host memory the first window's upload and
+    // the last window's download are pipelined with its kernels in column
+    // chunks of the shard's SoA arrays (launches with a row stride): H2D on
+    // streams[0], kernels on streams[1], D2H on streams[2], per-chunk events.
+    std::vector<LeaseGuard> leases(shards.size());
+    rc = for_each_shard(shards, [&](size_t i) {
+        const Shard& sh = shards[i];
         BODE_CUDA(cudaSetDevice(sh.device));
-        DeviceBuffers& B = g_dev[sh.device];
-        std::lock_guard<std::mutex> lock(B.m);
-        int r = ensure(&B.y, &B.y_cap, (size_t)sh.count * N);
+        int r = lease_pool().acquire(sh.device, &leases[i].L);
         if (r) return r;
+        Lease& B = *leases[i].L;
+        if ((r = ensure(&B.y, &B.y_cap, (size_t)sh.count * N))) return r;
         if (P > 0 && (r = ensure(&B.g, &B.g_cap, (size_t)sh.count * P))) return r;
         if ((r = ensure(&B.st, &B.st_cap, (size_t)sh.count))) return r;
         if ((r = ensure(&B.ord, &B.ord_cap, (size_t)sh.count))) return r;
-        for (auto& st : B.streams)
-            if (!st) BODE_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-        for (auto& ev : B.events)
-            if (!ev) BODE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        if (sink != nullptr && nwin > 1)
+            for (int slot = 0; slot < 2; ++slot)
+                if ((r = ensure(&B.ysnap[slot], &B.ysnap_cap[slot], (size_t)sh.count * N)))
+                    return r;
         if ((r = bode::init_order(B.ord, sh.count, B.streams[1]))) return fail(r, "order init failed");
         return BODE_OK;
     });
     if (rc) return rc;
 
+    // Snapshots of windows 1..n-1 (batch_driver.cpp:104-114) are asynchronous:
+    // after window k's kernel the state is staged on the device (ysnap[k%2],
+    // in the caller's order), its D2H into pinned staging[k%2] runs on the D2H
+    // stream while window k+1 computes, and a library thread hands it to the
+    // sink once the copy lands. A slot is reused at window k+2, after the sink
+    // for window k returned. The final window's state goes to y as before.
+    void* staging[2] = {nullptr, nullptr};
+    struct StagingGuard {
+        void** s;
+        ~StagingGuard() {
+            for (int i = 0; i < 2; ++i)
+                if (s[i]) pinned_cache().release(s[i]);
+        }
+    } staging_guard{staging};
+    std::unique_ptr<SinkWorker> worker;
+    if (sink != nullptr && nwin > 1) {
+        for (int i = 0; i < 2; ++i)
+            if ((rc = pinned_cache().acquire((size_t)num * N * sizeof(double), &staging[i])))
+                return rc;
+        worker.reset(new SinkWorker(sink, user, num, N));
+    }
+
     double t = t0;
+    const bool pinned = host_pinned(y);
     std::vector<char> repacked(shards.size(), 0);
     const double threshold = g_repack_threshold.load();
     const int presort_sel = g_presort_param.load();
     const int presort_row = presort_sel == -2 ? stiffness_param_row(p) : presort_sel;
     for (int64_t k = 1; k <= nwin; ++k) {
         const double tk = (k == nwin) ? t_end : t0 + static_cast<double>(k) * h_outer;
-        const bool snap = sink != nullptr || k == nwin;
-        rc = for_each_shard(shards, [&](const Shard& sh) {
+        const bool last = k == nwin;
+        const bool async_snap = worker != nullptr && !last;
+        const int slot = (int)(k % 2);
+        if (async_snap && k > 2) {
+            worker->wait_done(k - 2);  // staging[slot] is free again
+            if (worker->failed()) return fail(BODE_E_CUDA, "snapshot copy failed");
+        }
+        double* host_snap = async_snap ? static_cast<double*>(staging[slot]) : nullptr;
+        rc = for_each_shard(shards, [&](size_t si) {
+            const Shard& sh = shards[si];
             BODE_CUDA(cudaSetDevice(sh.device));
-            DeviceBuffers& B = g_dev[sh.device];
-            std::lock_guard<std::mutex> lock(B.m);
+            Lease& B = *leases[si].L;
             cudaStream_t sh2d = B.streams[0], s = B.streams[1], sd2h = B.streams[2];
-            const size_t si = &sh - shards.data();
             const long long cnt = sh.count;
-            const bool first = k == 1, last = k == nwin;
+            const bool first = k == 1;
             const int nch = pinned ? (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, cnt / (1 << 16)))
                                    : 1;
             // sort by a stiffness parameter before the first window: needs the
@@ -894,18 +1111,29 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
                     return fail(r, "unpack failed");
                 repacked[si] = 0;
             }
-            if (snap && !chunked_out) {
-                const double* ysrc = B.y;
-                if (repacked[si]) {  // snapshot in the caller's order
-                    if ((r = ensure(&B.ysnap, &B.ysnap_cap, (size_t)cnt * N))) return r;
-                    if ((r = bode::unpack(N, P, cnt, B.y, nullptr, nullptr, B.ord, B.ysnap, s)))
+            if (async_snap) {
+                // stage the snapshot (caller's order) once slot's previous D2H is done
+                double* ys = B.ysnap[slot];
+                BODE_CUDA(cudaStreamWaitEvent(s, B.snap_copied[slot], 0));
+                if (repacked[si]) {
+                    if ((r = bode::unpack(N, P, cnt, B.y, nullptr, nullptr, B.ord, ys, s)))
                         return fail(r, "snapshot unpack failed");
-                    ysrc = B.ysnap;
+                } else {
+                    BODE_CUDA(cudaMemcpyAsync(ys, B.y, (size_t)cnt * N * sizeof(double),
+                                              cudaMemcpyDeviceToDevice, s));
                 }
-                BODE_CUDA(cudaMemcpy2DAsync(y + sh.begin, num * sizeof(double), ysrc,
+                BODE_CUDA(cudaEventRecord(B.snap_ready[slot], s));
+                BODE_CUDA(cudaStreamWaitEvent(sd2h, B.snap_ready[slot], 0));
+                BODE_CUDA(cudaMemcpy2DAsync(host_snap + sh.begin, num * sizeof(double), ys,
+                                            cnt * sizeof(double), cnt * sizeof(double), N,
+                                            cudaMemcpyDeviceToHost, sd2h));
+                BODE_CUDA(cudaEventRecord(B.snap_copied[slot], sd2h));
+            }
+            if (last && !chunked_out) {
+                BODE_CUDA(cudaMemcpy2DAsync(y + sh.begin, num * sizeof(double), B.y,
                                             cnt * sizeof(double), cnt * sizeof(double), N,
                                             cudaMemcpyDeviceToHost, s));
-                if (last && stats)
+                if (stats)
                     BODE_CUDA(cudaMemcpyAsync(stats + sh.begin, B.st, cnt * sizeof(DevStats),
                                               cudaMemcpyDeviceToHost, s));
             }
@@ -921,13 +1149,26 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
                     repacked[si] = 1;
                 }
             }
-            for (auto& st : B.streams) BODE_CUDA(cudaStreamSynchronize(st));
+            if (last)
+                for (auto& st : B.streams) BODE_CUDA(cudaStreamSynchronize(st));
             return BODE_OK;
         });
         if (rc) return rc;
-        if (sink) sink(tk, y, num, N, user);
+        if (async_snap) {
+            SinkWorker::Job j{k, tk, host_snap, {}};
+            for (size_t si = 0; si < shards.size(); ++si)
+                j.events.push_back({shards[si].device, leases[si].L->snap_copied[slot]});
+            worker->push(std::move(j));
+        }
         t = tk;
     }
+    if (worker) {
+        worker->wait_done(nwin - 1);
+        const bool bad = worker->failed();
+        worker->finish();
+        if (bad) return fail(BODE_E_CUDA, "snapshot copy failed");
+    }
+    if (sink) sink(t_end, y, num, N, user);  // the final state, in y (batch_driver.cpp:112)
     if (outer_steps) *outer_steps = (int32_t)nwin;
     return BODE_OK;
 }

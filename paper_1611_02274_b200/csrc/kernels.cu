@@ -22,6 +22,7 @@ const KernelEntry* kernel_table(int* count) {
         BODE_BOTH_ARITH(ExpDecay, 1, 0, false, 2),
         BODE_BOTH_ARITH(Harmonic, 1, 0, false, 3),
         BODE_BOTH_ARITH(Zero<2>, 1, 0, false, 4),
+        BODE_BOTH_ARITH(Zero<1>, 1, 0, false, 4),
         BODE_BOTH_ARITH(Riccati, 1, 0, false, 5),
         BODE_BOTH_ARITH(Diag<3>, 1, 0, false, 6),
         BODE_BOTH_ARITH(Const<1>, 1, 0, false, 7),
@@ -50,6 +51,7 @@ const KernelEntry* kernel_table(int* count) {
         BODE_BOTH_ARITH_R(ExpDecay, 1, 1, false, 2, 64),
         BODE_BOTH_ARITH(Harmonic, 1, 1, false, 3),
         BODE_BOTH_ARITH(Zero<2>, 1, 1, false, 4),
+        BODE_BOTH_ARITH(Zero<1>, 1, 1, false, 4),
         BODE_BOTH_ARITH(Diag<3>, 1, 1, false, 6),
         BODE_BOTH_ARITH(Const<1>, 1, 1, false, 7),
     };

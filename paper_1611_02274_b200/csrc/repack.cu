@@ -29,24 +29,34 @@ namespace {
 
 using bode::DevStats;
 
+// Scratch comes from the stream-ordered allocator on the call's own stream
+// (cudaMallocAsync / cudaFreeAsync), so concurrent calls on different streams
+// -- or a user call next to bode_outer_loop's internal stream -- never share
+// it. The device's default pool keeps freed blocks (release threshold raised
+// once per device), so a warm call does not reach the driver allocator.
 struct Scratch {
-    std::mutex m;
     void* p = nullptr;
-    size_t cap = 0;
-};
-Scratch g_scratch[64];
-
-int scratch(int dev, size_t bytes, void** out) {
-    if (dev < 0 || dev >= 64) return BODE_E_UNSUPPORTED;
-    Scratch& s = g_scratch[dev];
-    if (s.cap < bytes) {
-        if (s.p) cudaFree(s.p);
-        s.p = nullptr;
-        s.cap = 0;
-        if (cudaMalloc(&s.p, bytes) != cudaSuccess) return BODE_E_CUDA;
-        s.cap = bytes;
+    cudaStream_t s = nullptr;
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
     }
-    *out = s.p;
+};
+
+int scratch(int dev, size_t bytes, cudaStream_t s, Scratch* out) {
+    static std::once_flag once[64];
+    if (dev < 0 || dev >= 64) return BODE_E_UNSUPPORTED;
+    std::call_once(once[dev], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+    if (cudaMallocAsync(&out->p, bytes, s) != cudaSuccess) {
+        out->p = nullptr;
+        return BODE_E_CUDA;
+    }
+    out->s = s;
     return BODE_OK;
 }
 
@@ -185,7 +195,6 @@ int repack_by(int N, int P, long long num, double* y, double* g, DevStats* st, l
     int dev = 0;
     RP_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64) return BODE_E_UNSUPPORTED;
-    std::lock_guard<std::mutex> lock(g_scratch[dev].m);
     size_t sort_bytes = 0;
     RP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (unsigned*)nullptr,
                                             (unsigned*)nullptr, (unsigned*)nullptr,
@@ -196,9 +205,9 @@ int repack_by(int N, int P, long long num, double* y, double* g, DevStats* st, l
     const size_t bytes = 4 * al(n * sizeof(unsigned)) + al(sort_bytes) +
                          al(n * rows * sizeof(double)) + al(n * sizeof(DevStats)) +
                          al(n * sizeof(long long));
-    void* base = nullptr;
-    if (scratch(dev, bytes, &base) != BODE_OK) return BODE_E_CUDA;
-    char* c = static_cast<char*>(base);
+    Scratch sc;
+    if (scratch(dev, bytes, s, &sc) != BODE_OK) return BODE_E_CUDA;
+    char* c = static_cast<char*>(sc.p);
     unsigned* key = reinterpret_cast<unsigned*>(c);
     c += al(n * sizeof(unsigned));
     unsigned* key2 = reinterpret_cast<unsigned*>(c);
@@ -254,12 +263,12 @@ int unpack(int N, int P, long long num, double* y, double* g, DevStats* st, long
     int dev = 0;
     RP_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64) return BODE_E_UNSUPPORTED;
-    std::lock_guard<std::mutex> lock(g_scratch[dev].m);
     const size_t n = (size_t)num;
     const int rows = N > P ? N : P;
     const size_t bytes = ((n * rows * sizeof(double) + 255) & ~size_t(255)) + n * sizeof(DevStats);
-    void* base = nullptr;
-    if (scratch(dev, bytes, &base) != BODE_OK) return BODE_E_CUDA;
+    Scratch sc;
+    if (scratch(dev, bytes, s, &sc) != BODE_OK) return BODE_E_CUDA;
+    void* base = sc.p;
     double* buf = static_cast<double*>(base);
     DevStats* st2 = reinterpret_cast<DevStats*>(static_cast<char*>(base) +
                                                 ((n * rows * sizeof(double) + 255) & ~size_t(255)));

@@ -29,3 +29,25 @@ def test_cpp_drop_in_matches_oracle(gpu, oracle):
     assert int(fields["accepted"]) == int(st["steps_accepted"].sum())
     assert int(fields["rejected"]) == int(st["steps_rejected"].sum())
     assert float(fields["x1[0]"]) == y[0]
+
+
+BATCH_EXE = os.path.join(A.PKG_DIR, "lib", "test_batch_dropin")
+
+
+def test_reference_batch_tests_host_cases():
+    """test_batch.cpp's host-only cases (pack/unpack/validation) compiled
+    against include/bode.hpp; without a device the program runs only those."""
+    assert os.path.exists(BATCH_EXE), "run paper_1611_02274_b200.build (builds tests/cpp/)"
+    out = subprocess.run([BATCH_EXE], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.startswith("PASS")
+
+
+@pytest.mark.gpu
+def test_reference_batch_tests_on_gpu(gpu):
+    """All of test_batch.cpp:16-258, transcribed against the bode:: drop-in,
+    including worker invariance (1, 2, 4, 8 shards on the available devices)
+    and the NaN-freeze case on a registered device problem."""
+    out = subprocess.run([BATCH_EXE], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.startswith("PASS") and "host-only" not in out.stdout, out.stdout

@@ -11,7 +11,7 @@ for p in $PARTS; do
   case $p in
     tests) timeout 900 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $OUT/status.txt ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1; echo "smoke rc=$?" >> $OUT/status.txt ;;
-    bench) /usr/bin/time -v timeout 1700 python3 bench.py --gpus 1 --steps 20 --warmup 5 > $OUT/bench.txt 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/status.txt ;;
+    bench) S=$(date +%s); timeout 1700 python3 bench.py --gpus 1 --steps 20 --warmup 5 > $OUT/bench.txt 2> $OUT/bench.err; echo "bench rc=$? wall=$(( $(date +%s) - S ))s" >> $OUT/status.txt ;;
     ref) timeout 600 python3 bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $OUT/bench_ref.txt 2>&1; echo "ref rc=$?" >> $OUT/status.txt ;;
     multirank)
       BODE_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
