@@ -307,8 +307,10 @@ def outer_loop(problem: OdeProblem, initial: BatchStates, t0: float, t_end: floa
     cb = SINK()
     if sink is not None:
         def _cb(t, yptr, num, dim, _user):
-            snap = out.copy()
-            snap.values = np.ctypeslib.as_array(yptr, shape=(num * dim,)).copy()
+            # an independent copy the sink may keep (batch_driver.hpp:26-28)
+            snap = BatchStates(out.num_systems, out.dim, out.param_dim,
+                               np.ctypeslib.as_array(yptr, shape=(num * dim,)).copy(),
+                               out.params.copy())
             sink(t, snap)
         cb = SINK(_cb)
     check(lib().bode_outer_loop(ctypes.byref(problem.c()), _solver(solver), _arith(arith), t0,

@@ -17,7 +17,9 @@ import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
-LIB_DIR = os.path.join(PKG, "lib")
+# BODE_BUILD_DIR / BODE_NVCC_EXTRA: an A/B variant of the library (e.g. lib/ab/<name>
+# built with -D switches), loaded by the bench through BODE_LIB_PATH
+LIB_DIR = os.environ.get("BODE_BUILD_DIR") or os.path.join(PKG, "lib")
 OBJ_DIR = os.path.join(LIB_DIR, "obj")
 SO = os.path.join(LIB_DIR, "libbode.so")
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
@@ -25,7 +27,7 @@ INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-         "-diag-suppress", "20012", "-I", INCLUDE]
+         "-diag-suppress", "20012", "-I", INCLUDE] + os.environ.get("BODE_NVCC_EXTRA", "").split()
 
 
 def _sources():
@@ -75,7 +77,8 @@ def build(force: bool = False, verbose: bool = True) -> str:
             raise RuntimeError(f"link failed:\n{r.stderr}")
         if verbose:
             print(f"[bode build] linked {SO}", flush=True)
-    build_examples(verbose)
+    if not os.environ.get("BODE_BUILD_DIR"):
+        build_examples(verbose)
     return SO
 
 

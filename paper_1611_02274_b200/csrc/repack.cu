@@ -165,6 +165,17 @@ __global__ void lockstep_sums(const DevStats* __restrict__ st, long long num, in
     }
 }
 
+// Publishes the two sums into pinned host memory from the device (UVA), so
+// the read-back needs no copy engine: a D2H memcpy here would queue behind
+// the outer loop's multi-gigabyte snapshot copy on the same engine and
+// serialise it with the next window's kernel.
+__global__ void publish_sums(const unsigned long long* __restrict__ d,
+                             volatile unsigned long long* h) {
+    h[0] = d[0];
+    h[1] = d[1];
+    __threadfence_system();
+}
+
 inline unsigned blocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
 int cuda_fail(cudaError_t e) {
@@ -301,21 +312,24 @@ int lockstep_efficiency(const DevStats* st, long long num, int group, double* ef
     static std::mutex m;
     static unsigned long long* dsum[64] = {nullptr};
     static unsigned long long* hsum[64] = {nullptr};
+    static unsigned long long* hsum_dev[64] = {nullptr};  // its device alias
     int dev = 0;
     RP_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64) return BODE_E_UNSUPPORTED;
     std::lock_guard<std::mutex> lock(m);
     if (dsum[dev] == nullptr) {
         RP_CUDA(cudaMalloc(&dsum[dev], 2 * sizeof(unsigned long long)));
-        RP_CUDA(cudaMallocHost(&hsum[dev], 2 * sizeof(unsigned long long)));
+        RP_CUDA(cudaHostAlloc(&hsum[dev], 2 * sizeof(unsigned long long),
+                              cudaHostAllocMapped | cudaHostAllocPortable));
+        RP_CUDA(cudaHostGetDevicePointer((void**)&hsum_dev[dev], hsum[dev], 0));
     }
     RP_CUDA(cudaMemsetAsync(dsum[dev], 0, 2 * sizeof(unsigned long long), s));
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned grid = (unsigned)std::min<long long>(blocks(num, 256), 8ll * sms);
     lockstep_sums<<<grid, 256, 0, s>>>(st, num, group, dsum[dev]);
-    RP_CUDA(cudaMemcpyAsync(hsum[dev], dsum[dev], 2 * sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, s));
+    publish_sums<<<1, 1, 0, s>>>(dsum[dev], hsum_dev[dev]);
+    RP_CUDA(cudaGetLastError());
     RP_CUDA(cudaStreamSynchronize(s));
     *eff = hsum[dev][1] ? (double)hsum[dev][0] / (double)hsum[dev][1] : 1.0;
     return BODE_OK;

@@ -22,6 +22,8 @@ from golden_cases import PLEIADES_IC, heat_ic
 
 pytestmark = pytest.mark.gpu
 
+# (stages_total is not kept by the reference's stats, ode_problem.hpp:57-81;
+# the restatement's is compared in test_gpu_parity.py)
 COUNTS = ("steps_accepted", "steps_rejected", "rhs_evals", "spec_rad_evals", "underflow")
 
 
@@ -72,7 +74,7 @@ def test_rkck_pleiades_2_24_stride(gpu, checker):
                                    ("exact", "fast"))
     ye, se = out["exact"]
     assert np.array_equal(ye.view(np.uint64), yo.view(np.uint64))
-    for k in COUNTS + ("stages_total", "h_min_seen", "h_max_seen"):
+    for k in COUNTS + ("h_min_seen", "h_max_seen"):
         assert np.array_equal(se[k], so[k]), k
     yf, sf = out["fast"]
     err = sysrel(yf, yo, idx.size, 28)
@@ -90,7 +92,7 @@ def test_rkc_heat64_2_24_stride(gpu, checker):
                                    ("exact",))
     ye, se = out["exact"]
     assert np.array_equal(ye.view(np.uint64), yo.view(np.uint64))
-    for k in COUNTS + ("stages_total", "h_min_seen", "h_max_seen"):
+    for k in COUNTS + ("h_min_seen", "h_max_seen"):
         assert np.array_equal(se[k], so[k]), k
 
 
@@ -106,7 +108,7 @@ def test_config4_stiffness_varied_2_22_stride(gpu, checker):
                                    ("exact",), g=g)
     ye, se = out["exact"]
     assert np.array_equal(ye.view(np.uint64), yo.view(np.uint64))
-    for k in COUNTS + ("stages_total", "h_min_seen", "h_max_seen"):
+    for k in COUNTS + ("h_min_seen", "h_max_seen"):
         assert np.array_equal(se[k], so[k]), k
 
 
@@ -121,7 +123,7 @@ def test_rkck_stress_policies(gpu, checker):
                                    ("exact", "fast"))
     ye, se = out["exact"]
     assert np.array_equal(ye.view(np.uint64), yo.view(np.uint64))
-    for k in COUNTS + ("stages_total",):
+    for k in COUNTS:
         assert np.array_equal(se[k], so[k]), k
     yf, sf = out["fast"]
     err = sysrel(yf, yo, num, 28)

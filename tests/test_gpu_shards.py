@@ -115,24 +115,39 @@ def test_async_snapshots_equal_windowed_integrate_batch(gpu, solver, problem):
 
 def test_async_sink_overlaps_the_next_window(gpu):
     """With a sink, each window's snapshot D2H runs under the next window's
-    kernel: the loop costs about the same as without a sink, well below the
-    no-sink time plus one synchronous D2H per window."""
+    kernel: the loop costs about the same as without a sink, below the
+    no-sink time plus one synchronous D2H per window. (C-level call with a
+    no-op sink, so only the library's own snapshot path is timed.)"""
+    import ctypes
     import torch
-    prob = B.problems.heat_equation(64)
     num = 1 << 19
+    prob = A.make_problem(A.HEAT, 64)
     y0 = B.problems.perturb_initial_conditions(heat_ic(64), 0.01, 4, num).values
     yh = torch.from_numpy(y0.copy()).pin_memory()
-    b = B.BatchStates(num, 64, 0, yh.numpy(), np.zeros(0))
-    B.outer_loop(prob, b, 0.0, 0.2, 0.1, solver="rkc")  # warm
-    t = time.perf_counter()
-    B.outer_loop(prob, b, 0.0, 1.0, 0.1, solver="rkc")
-    t_plain = time.perf_counter() - t
-    n_snap = [0]
-    t = time.perf_counter()
-    B.outer_loop(prob, b, 0.0, 1.0, 0.1, solver="rkc",
-                 sink=lambda tt, s: n_snap.__setitem__(0, n_snap[0] + 1))
-    t_sink = time.perf_counter() - t
-    # one synchronous D2H of the state per window (pinned, measured here)
+    yp = ctypes.cast(yh.data_ptr(), ctypes.POINTER(ctypes.c_double))
+    st = A.empty_stats(num)
+    L = B.lib()
+    calls = [0]
+
+    def noop(t, y, n, d, u):
+        calls[0] += 1
+
+    cb = B.api.SINK(noop)
+    steps = ctypes.c_int32(0)
+
+    def run(sink, t_end=1.0):
+        yh.copy_(torch.from_numpy(y0))
+        t = time.perf_counter()
+        B.api.check(L.bode_outer_loop(ctypes.byref(prob), 1, 0, 0.0, t_end, 0.1, num, None, yp,
+                                      ctypes.byref(A.default_tol()), A.vptr(st), 1, sink, None,
+                                      ctypes.byref(steps)))
+        return time.perf_counter() - t
+
+    run(B.api.SINK(), 0.2)
+    run(cb, 0.2)  # warm: pinned staging is cached after the first sink call
+    calls[0] = 0
+    t_plain = min(run(B.api.SINK()) for _ in range(2))
+    t_sink = min(run(cb) for _ in range(2))
     d = torch.empty(num * 64, dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
     t = time.perf_counter()
@@ -142,10 +157,8 @@ def test_async_sink_overlaps_the_next_window(gpu):
     t_d2h = time.perf_counter() - t
     print(f"outer loop 2^19 heat64: plain {t_plain*1e3:.1f} ms, with sink {t_sink*1e3:.1f} ms, "
           f"9 synchronous snapshot D2H {t_d2h*1e3:.1f} ms")
-    assert n_snap[0] == 10
-    # the sink path builds Python snapshots (copies) too; allow that, but not
-    # a serial D2H per window
-    assert t_sink < t_plain + 0.6 * t_d2h + 0.25 * t_plain
+    assert calls[0] == 20
+    assert t_sink < t_plain + 0.5 * t_d2h + 0.01
 
 
 def test_concurrent_calls_and_nested_sink(gpu):
