@@ -273,7 +273,7 @@ struct Harmonic {
 
 // Calibration problems of the reference test suites.
 template <int NN>
-struct Zero {  // test_batch.cpp:248-256
+struct Zero {  // test_batch.cpp:80-89
     static constexpr int N = NN, P = 0;
     static constexpr const char* name = "zero";
     template <class R, int L>

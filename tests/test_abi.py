@@ -43,7 +43,7 @@ def test_version_and_defaults():
 
 @pytest.mark.parametrize("field,value", [("eps", 0.0), ("abs_tol", -1.0), ("safety", 1.5),
                                          ("p1", 0.0), ("uround", 0.0), ("kappa", -1.0)])
-def test_tolerance_validation(field, value):  # ode_problem.hpp:46-53, test_batch.cpp:397-406
+def test_tolerance_validation(field, value):  # ode_problem.hpp:46-53, test_batch.cpp:230-239
     t = A.default_tol(**{field: value})
     assert B.lib().bode_tol_validate(ctypes.byref(t)) == A.E_INVALID_SHAPE
     b = B.pack([[1.0]])
@@ -68,7 +68,7 @@ def test_generators_match_reference(oracle):
         B.problems.perturb_initial_conditions(PLEIADES_IC, 0.01, 1, 0)
 
 
-def test_window_schedule():  # batch_driver.cpp:99-105, test_batch.cpp:338-359
+def test_window_schedule():  # batch_driver.cpp:99-105, test_batch.cpp:171-192
     L = B.lib()
     assert L.bode_num_windows(0.0, 1.0, 0.1) == 10
     assert L.bode_num_windows(0.0, 1.0, 1.0) == 1
@@ -77,7 +77,7 @@ def test_window_schedule():  # batch_driver.cpp:99-105, test_batch.cpp:338-359
     assert L.bode_window_end(0.0, 1.0, 0.1, 3) == 0.0 + 3.0 * 0.1
 
 
-def test_pack_unpack_roundtrip():  # test_batch.cpp:183-244
+def test_pack_unpack_roundtrip():  # test_batch.cpp:16-76
     b = B.pack([[1.0, 2.0], [3.0, 4.0]])
     assert list(b.values) == [1.0, 3.0, 2.0, 4.0]
     assert B.unpack(b) == [[1.0, 2.0], [3.0, 4.0]]

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("solver", ["rkck", "rkc"])
 @pytest.mark.parametrize("arith", ["exact", "fast"])
-def test_zero_rhs_identity(gpu, solver, arith):  # test_batch.cpp:269-281
+def test_zero_rhs_identity(gpu, solver, arith):  # test_batch.cpp:102-114
     b = B.pack([[1.0, -2.5], [3.25, 4.0], [0.0, 1e-8]])
     r = B.integrate_batch(B.problems.zero(2), b, 0.0, 1.0, solver=solver, arith=arith)
     assert np.array_equal(r.states.values, b.values)
@@ -32,7 +32,7 @@ def test_zero_rhs_step_counts(gpu):  # test_rkck.cpp:178-194, test_rkc.cpp:363-3
 
 
 @pytest.mark.parametrize("solver", ["rkck", "rkc"])
-def test_linear_decay(gpu, solver):  # test_batch.cpp:283-292, test_rkc.cpp:377-385
+def test_linear_decay(gpu, solver):  # test_batch.cpp:116-125, test_rkc.cpp:377-385
     b = B.pack([[1.0], [2.0], [3.0], [4.0]], [[1.0]] * 4)
     r = B.integrate_batch(B.problems.exp_decay(), b, 0.0, 1.0, solver=solver)
     tolr = 1e-8 if solver == "rkck" else 1e-4
@@ -51,7 +51,7 @@ def test_riccati_and_harmonic(gpu):  # test_rkck.cpp:202-206, :267-273
 
 
 @pytest.mark.parametrize("solver", ["rkck", "rkc"])
-def test_nan_system_freezes_neighbour_unaffected(gpu, solver):  # test_batch.cpp:408-425
+def test_nan_system_freezes_neighbour_unaffected(gpu, solver):  # test_batch.cpp:241-258
     b = B.pack([[1.0], [1.0]], [[float("nan")], [1.0]])
     r = B.integrate_batch(B.problems.exp_decay(), b, 0.0, 1.0, solver=solver)
     assert r.stats[0]["underflow"] == 1 and r.states.at(0, 0) == 1.0
@@ -59,7 +59,7 @@ def test_nan_system_freezes_neighbour_unaffected(gpu, solver):  # test_batch.cpp
     assert abs(r.states.at(1, 0) - math.exp(-1.0)) < (1e-8 if solver == "rkck" else 1e-4)
 
 
-def test_system_isolation(gpu):  # test_batch.cpp:321-336
+def test_system_isolation(gpu):  # test_batch.cpp:154-169
     y0 = [1.0, 2.0, 3.0, 4.0, 5.0]
     mk = lambda ys: B.pack([[v] for v in ys], [[1.0]] * len(ys))
     base = B.integrate_batch(B.problems.exp_decay(), mk(y0), 0.0, 1.0)
@@ -70,7 +70,7 @@ def test_system_isolation(gpu):  # test_batch.cpp:321-336
         assert same != (i == 2)
 
 
-def test_sink_cadence(gpu):  # test_batch.cpp:338-359
+def test_sink_cadence(gpu):  # test_batch.cpp:171-192
     b = B.pack([[1.0, 2.0]])
     for span, hout, n in ((1.0, 0.1, 10), (1.0, 1.0, 1), (1.05, 0.1, 11)):
         times = []
@@ -78,7 +78,7 @@ def test_sink_cadence(gpu):  # test_batch.cpp:338-359
         assert len(times) == n and r.outer_steps == n and times[-1] == span
 
 
-def test_restart_windows_agree_with_single_window(gpu):  # test_batch.cpp:361-372
+def test_restart_windows_agree_with_single_window(gpu):  # test_batch.cpp:194-205
     b = B.pack([[1.0]], [[1.0]])
     multi = B.outer_loop(B.problems.exp_decay(), b, 0.0, 1.0, 0.1)
     single = B.outer_loop(B.problems.exp_decay(), b, 0.0, 1.0, 1.0)
@@ -87,7 +87,7 @@ def test_restart_windows_agree_with_single_window(gpu):  # test_batch.cpp:361-37
     assert multi.outer_steps == 10 and single.outer_steps == 1
 
 
-def test_stats_sanity(gpu):  # test_batch.cpp:384-395
+def test_stats_sanity(gpu):  # test_batch.cpp:217-228
     b = B.pack([[1.0], [5.0]], [[1.0], [1.0]])
     r = B.integrate_batch(B.problems.exp_decay(), b, 0.0, 1.0, solver="rkc")
     for st in r.stats:

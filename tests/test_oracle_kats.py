@@ -292,7 +292,7 @@ def test_pleiades_conservation(oracle):  # test_problems.cpp:96-111
     assert abs(e1 - e0) / abs(e0) < 1e-6
 
 
-def test_outer_loop_window_count(oracle):  # test_batch.cpp:338-359
+def test_outer_loop_window_count(oracle):  # test_batch.cpp:171-192
     z = A.make_problem(A.ZERO, 1)
     for span, hout, n in ((1.0, 0.1, 10), (1.0, 1.0, 1), (1.05, 0.1, 11)):
         rc, _, _, steps = oracle.outer_loop(z, A.SOLVER_RKCK, 0.0, span, hout, np.array([1.0]))
@@ -301,7 +301,7 @@ def test_outer_loop_window_count(oracle):  # test_batch.cpp:338-359
     assert oracle.outer_loop(z, 0, 1.0, 0.5, 0.1, np.array([1.0]))[0] == A.E_INVALID_INTERVAL
 
 
-def test_batch_nan_isolation(oracle):  # test_batch.cpp:408-425
+def test_batch_nan_isolation(oracle):  # test_batch.cpp:241-258
     p = A.make_problem(A.EXPDECAY)
     rc, y, st = oracle.integrate_batch(p, A.SOLVER_RKCK, 0.0, 1.0, np.array([1.0, 1.0]),
                                        np.array([np.nan, 1.0]), threads=2)
@@ -309,7 +309,7 @@ def test_batch_nan_isolation(oracle):  # test_batch.cpp:408-425
     assert st[1]["underflow"] == 0 and rel(y[1], math.exp(-1.0)) < 1e-8
 
 
-def test_batch_worker_invariance(oracle):  # test_batch.cpp:294-309
+def test_batch_worker_invariance(oracle):  # test_batch.cpp:127-142
     from paper_1611_02274_b200.api import problems
     ic = problems.pleiades_initial_conditions()
     _, y0 = oracle.perturb(ic, 0.01, 20140609, 256)

@@ -20,3 +20,33 @@ for p in $PARTS; do
       echo "multirank rc=$?" >> $OUT/status.txt ;;
   esac
 done
+# (appended parts; run with: bash tools/gpu_r02.sh <tag> ncu sanitize ...)
+for p in $PARTS; do
+  case $p in
+    ncu)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file $OUT/launches.csv python bench.py --steps 20 --warmup 5 > $OUT/ncu_launches_bench.txt 2>&1
+      echo "ncu_launches rc=$?" >> $OUT/status.txt
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:Pleiades \
+        -s 1 -c 1 -o $OUT/prof_rkck_fast python bench.py --steps 2 --warmup 1 --systems 16777216 \
+        --no-secondary --no-e2e --no-cpu > $OUT/ncu_full_rkck_fast.txt 2>&1
+      echo "ncu_rkck_fast rc=$?" >> $OUT/status.txt
+      timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:Pleiades \
+        -s 1 -c 1 -o $OUT/prof_rkck_exact python bench.py --arith exact --steps 2 --warmup 1 --systems 4194304 \
+        --no-secondary --no-e2e --no-cpu > $OUT/ncu_full_rkck_exact.txt 2>&1
+      echo "ncu_rkck_exact rc=$?" >> $OUT/status.txt
+      timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:Heat \
+        -s 1 -c 1 -o $OUT/prof_heat_exact python bench.py --steps 2 --warmup 1 --systems 4096 \
+        --rkc-systems 4194304 --aux-systems 0 --no-e2e --no-cpu > $OUT/ncu_full_heat_exact.txt 2>&1
+      echo "ncu_heat_exact rc=$?" >> $OUT/status.txt
+      timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:Heat \
+        -s 4 -c 1 -o $OUT/prof_heat_fast python bench.py --steps 2 --warmup 1 --systems 4096 \
+        --rkc-systems 4194304 --aux-systems 0 --no-e2e --no-cpu > $OUT/ncu_full_heat_fast.txt 2>&1
+      echo "ncu_heat_fast rc=$?" >> $OUT/status.txt ;;
+    sanitize)
+      for T in memcheck racecheck synccheck initcheck; do
+        timeout 900 compute-sanitizer --tool $T --print-limit 50 python tools/sanitize_probe.py > $OUT/sanitize_$T.txt 2>&1
+        echo "sanitize $T rc=$?" >> $OUT/status.txt
+      done ;;
+  esac
+done

@@ -1,0 +1,56 @@
+#!/usr/bin/env python3
+"""Small runs of every main kernel family for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck):
+
+    compute-sanitizer --tool memcheck python tools/sanitize_probe.py
+
+RKCK Pleiades FAST (one lane, RKN) and EXACT (axis-split lane pair), the
+persistent refill kernel, RKC heat n=64 EXACT and FAST (8-lane warp-uniform
+groups), RKC expDecay (one lane, stiffness-varied, presort + re-pack), the
+RKC coefficient-table kernel, the fixed-step harnesses, and the outer loop
+with the asynchronous sink over two shards on one device. Prints PROBE_OK.
+"""
+import os
+import sys
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+sys.path.insert(0, os.path.join(REPO, "tests"))
+
+import paper_1611_02274_b200 as B  # noqa: E402
+from paper_1611_02274_b200.api import stiffness_params  # noqa: E402
+from golden_cases import PLEIADES_IC, heat_ic  # noqa: E402
+
+
+def main():
+    L = B.lib()
+    n0 = L.bode_launch_count()
+    pl = B.problems.pleiades()
+    b = B.problems.perturb_initial_conditions(PLEIADES_IC, 0.1, 3, 1000)
+    for arith in ("fast", "exact"):
+        B.integrate_batch(pl, b, 0.0, 0.1, solver="rkck", arith=arith)
+    L.bode_set_persistent(1)
+    B.integrate_batch(pl, b, 0.0, 0.1, solver="rkck", arith="fast")
+    L.bode_set_persistent(0)
+    heat = B.problems.heat_equation(64)
+    hb = B.problems.perturb_initial_conditions(heat_ic(64), 0.01, 3, 300)
+    for arith in ("exact", "fast"):
+        B.integrate_batch(heat, hb, 0.0, 0.1, solver="rkc", arith=arith)
+    ed = B.problems.exp_decay()
+    eb = B.problems.perturb_initial_conditions(np.array([1.0]), 0.01, 3, 5000)
+    eb.param_dim, eb.params = 1, stiffness_params(5000)
+    snaps = []
+    B.outer_loop(ed, eb, 0.0, 0.3, 0.1, solver="rkc", gpus=2,
+                 sink=lambda t, s: snaps.append(t))
+    B.outer_loop(pl, b, 0.0, 0.3, 0.1, solver="rkck", arith="fast", gpus=2,
+                 sink=lambda t, s: snaps.append(t))
+    B.integrate_fixed(pl, b, 0.0, 0.1, 10, solver="rkck")
+    B.integrate_fixed(heat, hb, 0.0, 0.01, 4, solver="rkc", stages=5)
+    assert len(snaps) == 6
+    print(f"PROBE_OK launches={L.bode_launch_count() - n0}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
