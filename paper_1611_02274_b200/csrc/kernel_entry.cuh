@@ -106,7 +106,7 @@ static KernelEntry make_entry(int kind, int arith) {
     if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1)
         e.smem_per_thread = nystrom_smem_doubles<P, R>() * (int)sizeof(double);
     else
-        e.smem_per_thread = SOLVER == 1 ? kRkcSmemStride<C_of<P, L>()>() * (int)sizeof(double)
+        e.smem_per_thread = SOLVER == 1 ? kRkcSmemStride<C_of<P, L>(), L>() * (int)sizeof(double)
                             : KSMEM     ? kSmemStride<C_of<P, L>()>() * (int)sizeof(double)
                                         : 0;
     e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG>;

@@ -118,8 +118,12 @@ struct RkcCoefGen {
 // kRkcYInSmem) the state y (3C + 8 doubles, odd stride). The stats are touched a few times per attempt;
 // keeping their 15 registers out of the stage loop removes most spills at
 // the 128-register cap.
+// Lane groups (L > 1) add C doubles of scratch for the sequential sums
+// (rkc_seq_sum): each lane posts its terms there for its group.
+template <int C, int L = 1>
+__host__ __device__ constexpr int kRkcSmemStride() { return ((L > 1 ? 4 : 3) * C + 8) | 1; }
 template <int C>
-__host__ __device__ constexpr int kRkcSmemStride() { return (3 * C + 8) | 1; }
+__host__ __device__ constexpr int kRkcTermsOffset() { return 3 * C + 8; }
 
 // Per-device coefficient table for s = 2..kRkcTableMaxS: row(s) holds
 // muTilde_1 followed by (mu_j, nu_j, muTilde_j, gammaTilde_j, c_{j-1}) for
@@ -240,9 +244,49 @@ __device__ __forceinline__ void elementwise_quotients(Num num, Den den, R (&out)
 // for a lane group: seq_sum's shuffle hand-off. (Measured alternatives, all
 // slower: lane 0 running the chain from shared memory, -4%; a shared-memory
 // hand-off with __syncwarp, -5%; gathering every term by shuffles, -18%.)
+// The RKC sums of squares (error norm rkc.cpp:122-127, initial step
+// :160-164, power-method norm spectral_radius.cpp:11-13).
+//  EXACT, lane groups: the reference's sequential order. Each lane posts its C
+//   terms to its shared-memory scratch, and every lane of the group runs the
+//   whole N-term chain over the group's scratch (broadcast loads, issued
+//   ahead of the adds), so the chain carries no shuffle hand-offs.
+//  FAST: pairwise within the lane, then a butterfly across the group. IEEE
+//   addition commutes, so every lane ends with the same value.
+#ifndef BODE_RKC_SUM
+#define BODE_RKC_SUM 1
+#endif
 template <class R, int L, int C>
 __device__ __forceinline__ R rkc_seq_sum(const Group<L>& G, const R (&terms)[C], R init) {
-    return seq_sum<R, L, C>(G, terms, init);
+    if constexpr (L == 1 || BODE_RKC_SUM == 0) {
+        return seq_sum<R, L, C>(G, terms, init);
+    } else if constexpr (is_exact<R>::value) {
+        extern __shared__ double bode_smem[];
+        constexpr int S = kRkcSmemStride<C, L>();
+        double* mine = bode_smem + threadIdx.x * S + kRkcTermsOffset<C>();
+#pragma unroll
+        for (int c = 0; c < C; ++c) mine[c] = val(terms[c]);
+        __syncwarp();
+        const double* grp = bode_smem + (threadIdx.x & ~(L - 1)) * S + kRkcTermsOffset<C>();
+        R s = init;
+#pragma unroll
+        for (int k = 0; k < L; ++k)
+#pragma unroll
+            for (int c = 0; c < C; ++c) s = s + R(grp[k * S + c]);
+        __syncwarp();  // the scratch is rewritten by the next sum
+        return s;
+    } else {
+        R part[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) part[c] = terms[c];
+#pragma unroll
+        for (int w = 1; w < C; w *= 2)
+#pragma unroll
+            for (int c = 0; c + w < C; c += 2 * w) part[c] = part[c] + part[c + w];
+        R s = part[0];
+#pragma unroll
+        for (int o = 1; o < L; o *= 2) s = s + R(__shfl_xor_sync(0xffffffffu, val(s), o, L));
+        return init + s;
+    }
 }
 
 // For lane groups (L > 1) every lane of the warp reaches every shuffle of the
@@ -292,7 +336,12 @@ __device__ __forceinline__ int power_method(const Group<L>& G, bool on, R t, con
             tmp[c] = y[c] * y[c];
             v[c] = R(eig[c]) * R(eig[c]);
         }
-        seq_sum2<R, L, C>(G, tmp, v, nrmY, nrmV);
+        if constexpr (is_exact<R>::value || L == 1 || BODE_RKC_SUM == 0) {
+            seq_sum2<R, L, C>(G, tmp, v, nrmY, nrmV);
+        } else {
+            nrmY = rkc_seq_sum<R, L, C>(G, tmp, nrmY);
+            nrmV = rkc_seq_sum<R, L, C>(G, v, nrmV);
+        }
         nrmY = sqrt_(nrmY);
         nrmV = sqrt_(nrmV);
     }
@@ -655,7 +704,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
     static_assert(L > 1, "one lane per system: rkc_system_lane");
     constexpr int C = P::N / L;
     extern __shared__ double bode_smem[];
-    DevStats& st = *reinterpret_cast<DevStats*>(bode_smem + threadIdx.x * kRkcSmemStride<C>() + 2 * C);
+    DevStats& st = *reinterpret_cast<DevStats*>(bode_smem + threadIdx.x * kRkcSmemStride<C, L>() + 2 * C);
     stats_init(st);
     const R tEnd(tEnd_in);
     R t(t_in);
@@ -670,10 +719,10 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
     const R cbrtU = cbrt_(uround);  // cbrt(errOld) when errOld is floored at uround
     long long numStep = 0;
     // f0 and the power-method eigenvector live in this lane's shared-memory
-    // row (stride kRkcSmemStride<C>, odd => conflict-free): f0 is read once
+    // row (stride kRkcSmemStride<C, L>, odd => conflict-free): f0 is read once
     // per element per stage, eig only by the power method; registers go to
     // y and the two stage vectors.
-    double* const eig = bode_smem + threadIdx.x * kRkcSmemStride<C>();
+    double* const eig = bode_smem + threadIdx.x * kRkcSmemStride<C, L>();
     F0Store<R, C, kRkcF0InSmem> f0(eig + C);
     F0Store<R, C, kRkcYInSmem && (C >= 4)> ys(eig + 2 * C + 8);
     {

@@ -50,3 +50,14 @@ for p in $PARTS; do
       done ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    ab_sum)  # heat64 RKC with the new sums vs lib/ab/sum0 (BODE_RKC_SUM=0), alternating
+      I=0; for V in sum0 new sum0 new; do I=$((I+1))
+        if [ $V = new ]; then LP=; else LP=$PWD/paper_1611_02274_b200/lib/ab/$V/libbode.so; fi
+        BODE_LIB_PATH=$LP timeout 600 python bench.py --steps 5 --warmup 1 --systems 4096 --rkc-systems 4194304 \
+          --aux-systems 0 --no-e2e --no-cpu > $OUT/ab_sum_${I}_$V.txt 2>&1; done
+      echo "ab_sum rc=$?" >> $OUT/status.txt ;;
+    trkc) timeout 900 python -m pytest tests -x -q -m gpu -k "heat or rkc or stiff or expdecay or brusselator or user" -s > $OUT/pytest_rkc.txt 2>&1; echo "trkc rc=$?" >> $OUT/status.txt ;;
+  esac
+done
