@@ -61,3 +61,8 @@ for p in $PARTS; do
     trkc) timeout 900 python -m pytest tests -x -q -m gpu -k "heat or rkc or stiff or expdecay or brusselator or user" -s > $OUT/pytest_rkc.txt 2>&1; echo "trkc rc=$?" >> $OUT/status.txt ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    lat) [ -x tools/fp64_latency ] && timeout 120 tools/fp64_latency > $OUT/fp64_latency.json 2>&1; echo "lat rc=$?" >> $OUT/status.txt ;;
+  esac
+done
