@@ -119,7 +119,7 @@ void toStats(const IntegrationStats& s, bode_stats_t* o, long stages) {
     o->h_min_seen = s.hMinSeen;
     o->h_max_seen = s.hMaxSeen;
     o->underflow = s.underflow ? 1 : 0;
-    o->reserved = 0;
+    o->budget_exhausted = 0;
 }
 
 BatchStates toBatch(const bode_problem_t* p, int64_t num, const double* y, const double* g) {

@@ -62,7 +62,7 @@ class Stats(ctypes.Structure):
                 ("rhs_evals", ctypes.c_int64), ("spec_rad_evals", ctypes.c_int64),
                 ("stages_total", ctypes.c_int64), ("h_min_seen", ctypes.c_double),
                 ("h_max_seen", ctypes.c_double), ("underflow", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("budget_exhausted", ctypes.c_int32)]
 
 
 assert ctypes.sizeof(Stats) == 64
@@ -70,7 +70,7 @@ assert ctypes.sizeof(Stats) == 64
 STATS_DTYPE = np.dtype([
     ("steps_accepted", "<i8"), ("steps_rejected", "<i8"), ("rhs_evals", "<i8"),
     ("spec_rad_evals", "<i8"), ("stages_total", "<i8"), ("h_min_seen", "<f8"),
-    ("h_max_seen", "<f8"), ("underflow", "<i4"), ("reserved", "<i4")])
+    ("h_max_seen", "<f8"), ("underflow", "<i4"), ("budget_exhausted", "<i4")])
 assert STATS_DTYPE.itemsize == 64
 
 

@@ -94,6 +94,8 @@ def lib():
         "bode_set_block_size": (ctypes.c_int, [c_i32]),
         "bode_launch_count": (c_i64, []),
         "bode_set_persistent": (ctypes.c_int, [c_i32]),
+        "bode_set_wide": (ctypes.c_int, [c_i32]),
+        "bode_set_attempt_budget": (ctypes.c_int, [c_i64]),
         "bode_register_kernels": (ctypes.c_int, [vp, c_i32, c_i32]),
         "bode_order_init": (ctypes.c_int, [vp, c_i64, vp]),
         "bode_repack_by_cost": (ctypes.c_int, [P(A.Problem), c_i64, vp, vp, vp, vp, vp]),

@@ -15,17 +15,32 @@ struct DevTol {  // bode_tol_t, by value in the kernel parameters
     int refill_min;          // persistent kernels: idle lanes that trigger a refill round
     long long stride;        // SoA row stride of y and g in doubles (0: the launch's num),
                              // so a launch can cover a column range of a larger batch
+    int dim;                 // the problem's dimension (run-time-dimension kernels, wide.cuh)
+    double* scratch;         // wide.cuh: per-block vector scratch in global memory, or null
+    long long max_attempts;  // per-window attempt budget per system (0: none)
 };
 
 struct DevStats {  // bode_stats_t, per system (AoS, 64 bytes)
     long long steps_accepted, steps_rejected, rhs_evals, spec_rad_evals, stages_total;
     double h_min_seen, h_max_seen;
-    int underflow, reserved;
+    int underflow, budget_exhausted;
 };
 static_assert(sizeof(DevStats) == 64, "DevStats must match bode_stats_t");
 
 template <class P, int L>
 constexpr int C_of() { return P::N / L; }
+
+// One-system-per-block kernels (wide.cuh): state-length vectors per system,
+// threads per block (upper bound), and the largest vector set kept in
+// shared memory (beyond it the vectors live in a per-block global scratch).
+constexpr int kWideVecs = 8;
+constexpr int kWideMaxBlock = 512;
+constexpr int kWideSmemMax = 200 * 1024;
+// threads per block for dimension n: one component per thread up to
+// kWideMaxBlock, in whole warps
+__host__ __device__ constexpr int wide_block(int n) {
+    return n >= kWideMaxBlock ? kWideMaxBlock : ((n + 31) / 32) * 32;
+}
 
 // Launchers return the launching runtime's cudaGetLastError() as an int.
 using LaunchFn = int (*)(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
@@ -59,6 +74,9 @@ struct KernelEntry {
     int (*launch_fixed)(const void* fn, dim3 grid, dim3 block, cudaStream_t s, const double* g,
                          double* y, long long num, double t0, double tEnd, long long numSteps,
                          long long stages, double kappa) = nullptr;
+    // 1: one system per thread block for any dimension (wide.cuh), dim == 0;
+    // chosen when no lane-group kernel is compiled for the problem's dim
+    int wide = 0;
 };
 
 const KernelEntry* kernel_table(int* count);

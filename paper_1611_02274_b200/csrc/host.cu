@@ -38,6 +38,8 @@ using bode::KernelEntry;
 thread_local std::string g_last_error;
 std::atomic<long long> g_launches{0};
 std::atomic<int> g_block_override{0};
+std::atomic<int> g_force_wide{0};  // one-system-per-block kernels even where lane kernels exist
+std::atomic<long long> g_attempt_budget{0};  // per-window attempts per system (0: none)
 std::atomic<int> g_persistent{0};  // dynamic-refill kernels where compiled (opt-in)
 std::atomic<double> g_repack_threshold{0.7};  // outer loop: re-pack below this efficiency
 std::atomic<int> g_presort_param{-2};  // outer loop: sort by |g[row]| first (-1 off, -2 auto)
@@ -67,7 +69,7 @@ const double kPleiadesIC[28] = {
     3.0,  3.0, -1.0, -3.0, 2.0, -2.0, 2.0,  3.0,  -3.0, 2.0, 0.0,  0.0,   -4.0, 4.0,
     0.0,  0.0, 0.0,  0.0,  0.0, 1.75, -1.5, 0.0,  0.0,  0.0, -1.25, 1.0, 0.0,  0.0};
 
-DevTol to_dev(const bode_tol_t* t) {
+DevTol to_dev(const bode_tol_t* t, int dim) {
     DevTol d;
     d.eps = t->eps;
     d.abs_tol = t->abs_tol;
@@ -90,6 +92,9 @@ DevTol to_dev(const bode_tol_t* t) {
     }();
     d.refill_min = refill_min;
     d.stride = 0;
+    d.dim = dim;
+    d.scratch = nullptr;
+    d.max_attempts = g_attempt_budget.load();
     return d;
 }
 
@@ -199,15 +204,28 @@ const KernelEntry* find_entry(const bode_problem_t* p, int solver, int arith) {
         const KernelEntry* begin() const { return b; }
         const KernelEntry* end() const { return e; }
     };
+    // one system per block (wide.cuh) for a problem kind with a run-time
+    // dimension: when no lane-group kernel is compiled for p->dim, or forced
+    auto wide = [&]() -> const KernelEntry* {
+        for (int i = 0; i < n; ++i)
+            if (tab[i].wide && tab[i].kind == p->kind && tab[i].param_dim == p->param_dim &&
+                tab[i].solver == solver && tab[i].arith == arith)
+                return &tab[i];
+        return nullptr;
+    };
+    if (g_force_wide.load())
+        if (const KernelEntry* e = wide()) return e;
     const KernelEntry* first = nullptr;
     if (const KernelEntry* e =
             find_in(Span{tab, tab + n}, p, solver, arith, want_lanes, want_maxreg, &first))
         return e;
-    std::lock_guard<std::mutex> lock(registry_mutex());
-    if (const KernelEntry* e =
-            find_in(registry(), p, solver, arith, want_lanes, want_maxreg, &first))
-        return e;
-    return first;
+    {
+        std::lock_guard<std::mutex> lock(registry_mutex());
+        if (const KernelEntry* e =
+                find_in(registry(), p, solver, arith, want_lanes, want_maxreg, &first))
+            return e;
+    }
+    return first ? first : wide();
 }
 
 int check_problem_shape(const bode_problem_t* p) {
@@ -295,6 +313,41 @@ int block_for(const KernelEntry* e) {
     return b;
 }
 
+// One window of a one-system-per-block kernel (wide.cuh): the system's
+// kWideVecs state-length vectors in dynamic shared memory when they fit,
+// otherwise in a stream-ordered per-block scratch; a grid-stride loop over
+// the systems with the grid sized to the resident capacity.
+int launch_wide(const KernelEntry* e, cudaStream_t s, const double* g, double* y, DevStats* st,
+                long long num, double t, double tEnd, DevTol tol, int merge) {
+    const int n = tol.dim;
+    if (n < 2) return fail(BODE_E_INVALID_SHAPE, "run-time-dimension kernel needs dim >= 2");
+    int dev = 0, sms = 0;
+    BODE_CUDA(cudaGetDevice(&dev));
+    BODE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int block = bode::wide_block(n);
+    const size_t vec_bytes = (size_t)bode::kWideVecs * (size_t)n * sizeof(double);
+    const bool in_smem = vec_bytes <= (size_t)bode::kWideSmemMax;
+    const size_t smem = in_smem ? vec_bytes : 0;
+    BODE_CUDA((cudaError_t)e->prepare(e->fn, dev, (int)smem));
+    long long grid = 1;
+    if (in_smem) {
+        int per_sm = 0;
+        BODE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->fn, block, smem));
+        grid = std::min<long long>(num, (long long)std::max(per_sm, 1) * sms);
+    } else {
+        // global scratch: at most two blocks per SM, within a 4 GiB budget
+        const long long budget = std::max<long long>(1, (4LL << 30) / (long long)vec_bytes);
+        grid = std::min<long long>(num, std::min<long long>(2LL * sms, budget));
+        BODE_CUDA(cudaMallocAsync((void**)&tol.scratch, (size_t)grid * vec_bytes, s));
+    }
+    cudaError_t le = (cudaError_t)e->launch(e->fn, dim3((unsigned)grid), dim3(block), smem, s, g,
+                                            y, st, num, t, tEnd, tol, merge);
+    if (tol.scratch != nullptr) BODE_CUDA(cudaFreeAsync(tol.scratch, s));
+    BODE_CUDA(le);
+    g_launches.fetch_add(1);
+    return BODE_OK;
+}
+
 // Launch one window over `num` systems resident on the current device.
 int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double* y,
                   DevStats* st, long long num, double t, double tEnd, const DevTol& tol_in,
@@ -307,6 +360,7 @@ int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double*
         int rc = rkc_table_for(e, tol.kappa, s, &tol.rkc_coef);
         if (rc) return rc;
     }
+    if (e->wide) return launch_wide(e, s, g, y, st, num, t, tEnd, tol, merge);
     const int block = block_for(e);
     const long long threads = num * e->lanes;
     const long long grid = (threads + block - 1) / block;
@@ -842,6 +896,17 @@ int bode_set_block_size(int32_t threads) {
 
 int64_t bode_launch_count(void) { return g_launches.load(); }
 
+int bode_set_attempt_budget(int64_t max_attempts) {
+    if (max_attempts < 0) return fail(BODE_E_INVALID_SHAPE, "attempt budget must be >= 0");
+    g_attempt_budget.store(max_attempts);
+    return BODE_OK;
+}
+
+int bode_set_wide(int32_t mode) {
+    g_force_wide.store(mode ? 1 : 0);
+    return BODE_OK;
+}
+
 int bode_set_persistent(int32_t enable) {
     g_persistent.store(enable ? 1 : 0);
     return BODE_OK;
@@ -937,7 +1002,7 @@ int bode_int_driver_device(const bode_problem_t* p, int32_t solver, int32_t arit
     if (rc) return rc;
     if ((rc = check_devices(1))) return rc;
     return launch_window(e, (cudaStream_t)stream, g_dev, y_dev, (DevStats*)stats_dev, num, t,
-                         t_end, to_dev(tol), merge_stats ? 1 : 0);
+                         t_end, to_dev(tol, p->dim), merge_stats ? 1 : 0);
 }
 
 int bode_int_driver(const bode_problem_t* p, int32_t solver, int32_t arith, double t,
@@ -947,7 +1012,7 @@ int bode_int_driver(const bode_problem_t* p, int32_t solver, int32_t arith, doub
     int rc = validate_call(p, solver, arith, t, t_end, num, g, y, tol, &e);
     if (rc) return rc;
     if ((rc = check_devices(num_gpus))) return rc;
-    const DevTol dt = to_dev(tol);
+    const DevTol dt = to_dev(tol, p->dim);
     DeviceRestore restore;
     const auto shards = make_shards(num, num_gpus);
     return for_each_shard(shards, [&](size_t i) {
@@ -965,7 +1030,7 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
     int rc = validate_call(p, solver, arith, t0, t_end, num, g, y, tol, &e);
     if (rc) return rc;
     if ((rc = check_devices(num_gpus))) return rc;
-    const DevTol dt = to_dev(tol);
+    const DevTol dt = to_dev(tol, p->dim);
     DeviceRestore restore;
     const auto shards = make_shards(num, num_gpus);
     const int N = p->dim, P = p->param_dim;

@@ -16,6 +16,7 @@
 #include "rkck_nystrom.cuh"
 #include "rkck_pleiades2.cuh"
 #include "fixed.cuh"
+#include "wide.cuh"
 
 namespace bode {
 
@@ -151,6 +152,45 @@ static KernelEntry make_entry(int kind, int arith) {
             return (int)cudaGetLastError();
         };
     }
+    if constexpr (SOLVER == 1)
+        e.build_rkc_table = [](double* tab, double kappa, cudaStream_t s) -> int {
+            rkc_coef_table_kernel<R><<<(unsigned)((kRkcTableMaxS + 63) / 64), 64, 0, s>>>(tab, kappa);
+            return (int)cudaGetLastError();
+        };
+    return e;
+}
+
+// One system per thread block for a problem with a run-time dimension
+// (wide.cuh); matched by kind when no lane-group kernel fits the dim.
+template <class Prob, class R, int SOLVER>
+static KernelEntry make_wide_entry(int kind, int arith) {
+    KernelEntry e;
+    e.kind = kind;
+    e.dim = 0;
+    e.param_dim = Prob::P;
+    e.solver = SOLVER;
+    e.arith = arith;
+    e.lanes = 32;  // one group per warp for the lockstep-efficiency check
+    e.maxreg = 0;
+    e.smem_per_thread = 0;
+    e.default_block = 0;
+    e.wide = 1;
+    e.fn = (const void*)&wide_kernel<Prob, R, SOLVER>;
+    e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                  const double* g, double* y, DevStats* st, long long num, double t,
+                  double tEnd, DevTol tol, int merge) -> int {
+        auto k = (void (*)(const double*, double*, DevStats*, long long, double, double, DevTol,
+                           int))fn;
+        k<<<grid, block, smem, s>>>(g, y, st, num, t, tEnd, tol, merge);
+        return (int)cudaGetLastError();
+    };
+    e.prepare = [](const void* fn, int device, int smem_bytes) -> int {
+        cudaError_t err = cudaSetDevice(device);
+        if (err == cudaSuccess && smem_bytes > 48 * 1024)
+            err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+        return (int)err;
+    };
+    e.build_rkc_table = nullptr;
     if constexpr (SOLVER == 1)
         e.build_rkc_table = [](double* tab, double kappa, cudaStream_t s) -> int {
             rkc_coef_table_kernel<R><<<(unsigned)((kRkcTableMaxS + 63) / 64), 64, 0, s>>>(tab, kappa);

@@ -54,6 +54,11 @@ const KernelEntry* kernel_table(int* count) {
         BODE_BOTH_ARITH(Zero<1>, 1, 1, false, 4),
         BODE_BOTH_ARITH(Diag<3>, 1, 1, false, 6),
         BODE_BOTH_ARITH(Const<1>, 1, 1, false, 7),
+        // heatEquation(n) for any other n >= 2: one system per thread block
+        make_wide_entry<HeatWide, xd, 0>(1, 0),
+        make_wide_entry<HeatWide, double, 0>(1, 1),
+        make_wide_entry<HeatWide, xd, 1>(1, 0),
+        make_wide_entry<HeatWide, double, 1>(1, 1),
     };
     *count = (int)(sizeof(table) / sizeof(table[0]));
     return table;

@@ -578,6 +578,7 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
         BODE_PHASE_CTRL_END
         if (state == kTop) {
             if (!(tEnd - t > uround * fabs_(tEnd))) break;
+            if (budget_spent(st, tol)) break;
             hMin = R(10.0) * uround * fmax_(fabs_(t), hMax);
             if (R(1.1) * wsH >= fabs_(tEnd - t)) wsH = fabs_(tEnd - t);
             state = (numStep % 25 == 0) ? kSrThenAttempt : kAttempt;
@@ -753,6 +754,8 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
         }
         if (live && state == kTop) {
             if (!(tEnd - t > uround * fabs_(tEnd))) {
+                live = false;
+            } else if (budget_spent(st, tol)) {
                 live = false;
             } else {
                 hMin = R(10.0) * uround * fmax_(fabs_(t), hMax);

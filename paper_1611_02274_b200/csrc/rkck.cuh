@@ -23,7 +23,7 @@ __device__ __forceinline__ void stats_init(DevStats& s) {
     s.h_min_seen = __longlong_as_double(0x7ff0000000000000ll);  // +inf
     s.h_max_seen = 0.0;
     s.underflow = 0;
-    s.reserved = 0;
+    s.budget_exhausted = 0;
 }
 
 // IntegrationStats::recordAcceptedStep (ode_problem.hpp:66-70)
@@ -43,6 +43,18 @@ __device__ __forceinline__ void stats_merge(DevStats& a, const DevStats& b) {
     a.h_min_seen = fmin(a.h_min_seen, b.h_min_seen);
     a.h_max_seen = fmax(a.h_max_seen, b.h_max_seen);
     a.underflow = a.underflow || b.underflow;
+    a.budget_exhausted = a.budget_exhausted || b.budget_exhausted;
+}
+
+// The opt-in per-window attempt budget (bode_set_attempt_budget; not in the
+// reference, off by default): true once this window's attempts reach it. The
+// caller then freezes the system at its last accepted state, as on underflow.
+__device__ __forceinline__ bool budget_spent(DevStats& st, const DevTol& tol) {
+    if (tol.max_attempts > 0 && st.steps_accepted + st.steps_rejected >= tol.max_attempts) {
+        st.budget_exhausted = 1;
+        return true;
+    }
+    return false;
 }
 
 // Cash-Karp tableau (rkck.cpp:8-27), evaluated as the same double quotients.
@@ -133,6 +145,7 @@ __device__ __forceinline__ void rkck_system(const Group<L>& G, double t_in, doub
 
 #pragma unroll 1
     while (tEnd - t > uround * fabs_(tEnd)) {
+        if (budget_spent(st, tol)) break;
         h = fmin_(tEnd - t, h);
         R arg[C], out[C];
         if (!haveF) {  // rejected retries reuse f(t, y) (rkck.cpp:133-137)

@@ -341,6 +341,7 @@ struct NystromRkck {
             }
             h = R(hNew);
         }
+        if (live && budget_spent(st, tol)) live = false;
     }
 
     // error norm, controller and the accept/reject update of one attempt
@@ -473,6 +474,7 @@ struct NystromRkck {
             }
             h = hNew;
         }
+        if (live && budget_spent(st, tol)) live = false;
     }
 };
 

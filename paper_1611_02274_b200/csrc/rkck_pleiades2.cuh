@@ -323,6 +323,7 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
             h = hNew;
         }
         if (live) live = tEnd - t > uround * fabs_(tEnd);
+        if (live && budget_spent(st, tol)) live = false;
     }
 }
 

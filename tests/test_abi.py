@@ -120,12 +120,22 @@ def test_supported_matrix():
         for arith in (0, 1):
             p = A.make_problem(kind, dim)
             assert L.bode_problem_supported(ctypes.byref(p), solver, arith) == 1
+    # heatEquation(n) for any n >= 2 (problems.cpp:94-115): lane-group kernels
+    # for n in {8, 16, 32, 64}, one system per block (csrc/wide.cuh) otherwise
+    for n in (2, 3, 63, 100, 4000, 1_000_000):
+        for solver in (0, 1):
+            for arith in (0, 1):
+                p = A.make_problem(A.HEAT, n)
+                assert L.bode_problem_supported(ctypes.byref(p), solver, arith) == 1
+    assert L.bode_set_wide(1) == 0 and L.bode_set_wide(0) == 0
 
 
 def test_scheduling_knob_validation():
     """Host-side setters reject out-of-range values before any device use, and
     the re-pack entry points validate their arguments (include/bode.h)."""
     L = B.lib()
+    assert L.bode_set_attempt_budget(-1) == A.E_INVALID_SHAPE
+    assert L.bode_set_attempt_budget(0) == 0
     assert L.bode_set_repack_threshold(1.5) == A.E_INVALID_SHAPE
     assert L.bode_set_repack_threshold(-0.1) == A.E_INVALID_SHAPE
     assert L.bode_set_presort_param(-3) == A.E_INVALID_SHAPE

@@ -1,0 +1,110 @@
+"""heatEquation(n) for any n >= 2 (problems.cpp:94-115): the one-system-per-
+block kernels (csrc/wide.cuh) for the dimensions no lane-group kernel is
+compiled for, against the oracle.
+
+Bars as in test_gpu_parity.py: EXACT bitwise (states and every counter),
+RKCK FAST <= 1e-13 per system with identical counts, RKC FAST reported
+against the reference within relTol (its step selection is chaotic at the
+ulp level). The reference's own large-dimension smoke case is
+test_rkc.cpp:491-512 (dim 1e6).
+"""
+import numpy as np
+import pytest
+
+import paper_1611_02274_b200 as B
+from paper_1611_02274_b200 import _abi as A
+from golden_cases import perturb, heat_ic
+from test_gpu_parity import run_gpu, sysrel, COUNTS
+
+pytestmark = pytest.mark.gpu
+
+
+def _bitwise(y, st, yo, so):
+    assert np.array_equal(y.view(np.uint64), yo.view(np.uint64))
+    for k in COUNTS + ("stages_total",):
+        assert np.array_equal(st[k], so[k]), k
+    assert np.array_equal(st["h_min_seen"], so["h_min_seen"])
+    assert np.array_equal(st["h_max_seen"], so["h_max_seen"])
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 17, 63, 100, 129, 513])
+def test_heat_any_n_rkc_exact_bitwise(gpu, oracle, n):
+    num = 96
+    prob = A.make_problem(A.HEAT, n)
+    assert B.lib().bode_problem_supported(prob, A.SOLVER_RKC, A.ARITH_EXACT) == 1
+    y0 = perturb(heat_ic(n), 0.01, 7 + n, num)
+    t1 = 0.2 if n <= 129 else 0.02
+    y, st = run_gpu(prob, A.SOLVER_RKC, y0, None, "exact", t1=t1, hout=t1 / 2)
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKC, 0.0, t1, t1 / 2, y0)
+    assert rc == 0
+    _bitwise(y, st, yo, so)
+
+
+@pytest.mark.parametrize("n,t1", [(2, 0.1), (5, 0.05), (17, 0.01), (100, 1e-3)])
+def test_heat_any_n_rkck_exact_bitwise_and_fast(gpu, oracle, n, t1):
+    num = 64
+    prob = A.make_problem(A.HEAT, n)
+    y0 = perturb(heat_ic(n), 0.01, 3 + n, num)
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKCK, 0.0, t1, t1, y0)
+    assert rc == 0
+    y, st = run_gpu(prob, A.SOLVER_RKCK, y0, None, "exact", t1=t1, hout=t1)
+    _bitwise(y, st, yo, so)
+    y, st = run_gpu(prob, A.SOLVER_RKCK, y0, None, "fast", t1=t1, hout=t1)
+    assert sysrel(y, yo, num, n).max() <= 1e-13
+    for k in ("steps_accepted", "steps_rejected", "rhs_evals"):
+        assert np.array_equal(st[k], so[k]), k
+
+
+@pytest.mark.parametrize("n", [37, 200])
+def test_heat_any_n_rkc_fast_within_reltol(gpu, oracle, n):
+    num = 64
+    prob = A.make_problem(A.HEAT, n)
+    y0 = perturb(heat_ic(n), 0.01, 11, num)
+    y, st = run_gpu(prob, A.SOLVER_RKC, y0, None, "fast", t1=0.1, hout=0.1)
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKC, 0.0, 0.1, 0.1, y0)
+    assert sysrel(y, yo, num, n).max() <= 1e-6
+
+
+@pytest.mark.parametrize("solver", [A.SOLVER_RKC, A.SOLVER_RKCK])
+def test_forced_wide_equals_lane_kernels_at_n64(gpu, solver):
+    """The block kernel and the 8-lane heat64 kernel are two schedules of the
+    same arithmetic: bitwise equal under EXACT."""
+    L = B.lib()
+    num = 300
+    prob = A.make_problem(A.HEAT, 64)
+    y0 = perturb(heat_ic(64), 0.01, 5, num)
+    t1 = 0.1 if solver == A.SOLVER_RKC else 1e-3
+    y_lane, st_lane = run_gpu(prob, solver, y0, None, "exact", t1=t1, hout=t1)
+    L.bode_set_wide(1)
+    try:
+        n0 = L.bode_launch_count()
+        y_wide, st_wide = run_gpu(prob, solver, y0, None, "exact", t1=t1, hout=t1)
+        assert L.bode_launch_count() > n0
+    finally:
+        L.bode_set_wide(0)
+    _bitwise(y_wide, st_wide, y_lane, st_lane)
+
+
+def test_heat_global_scratch_path_bitwise(gpu, oracle):
+    """n = 4000: 8 n doubles exceed the shared-memory budget, so the vectors
+    live in a per-block global scratch (stream-ordered allocation)."""
+    n, num = 4000, 6
+    prob = A.make_problem(A.HEAT, n)
+    y0 = perturb(heat_ic(n), 0.01, 1, num)
+    t1 = 1e-3
+    y, st = run_gpu(prob, A.SOLVER_RKC, y0, None, "exact", t1=t1, hout=t1)
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKC, 0.0, t1, t1, y0)
+    _bitwise(y, st, yo, so)
+
+
+def test_heat_dim_1e6_smoke(gpu, oracle):
+    """One heat system of 10^6 interior points (test_rkc.cpp:491-512's size),
+    one short RKC window: bitwise the oracle."""
+    n = 1_000_000
+    prob = A.make_problem(A.HEAT, n)
+    y0 = heat_ic(n).astype(np.float64)
+    t1 = 1e-8
+    y, st = run_gpu(prob, A.SOLVER_RKC, y0, None, "exact", t1=t1, hout=t1)
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKC, 0.0, t1, t1, y0)
+    assert st["steps_accepted"][0] >= 5 and st["stages_total"][0] > 400
+    _bitwise(y, st, yo, so)
