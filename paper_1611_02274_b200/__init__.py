@@ -8,4 +8,5 @@ from . import _abi  # noqa: F401
 from .api import (BatchResult, BatchStates, BodeError, CudaError, InvalidInterval,  # noqa: F401
                   InvalidShape, InvalidStageCount, NoDevice, OdeProblem, OuterLoopResult,
                   Unsupported, fill_params, int_driver_device, integrate_batch, integrate_fixed, lib,
-                  outer_loop, pack, problems, stiffness_params, tolerance_settings, unpack)
+                  outer_loop, pack, problems, stats_summary, stiffness_params, tolerance_settings,
+                  unpack)

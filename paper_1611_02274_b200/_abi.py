@@ -67,6 +67,15 @@ class Stats(ctypes.Structure):
 
 assert ctypes.sizeof(Stats) == 64
 
+
+class StatsSummary(ctypes.Structure):  # bode_stats_summary_t
+    _fields_ = [("num", ctypes.c_int64), ("attempts_total", ctypes.c_int64),
+                ("attempts_max", ctypes.c_int64), ("attempts_argmax", ctypes.c_int64),
+                ("attempts_mean", ctypes.c_double), ("rhs_evals_total", ctypes.c_int64),
+                ("rhs_evals_max", ctypes.c_int64), ("underflow_count", ctypes.c_int64),
+                ("budget_exhausted_count", ctypes.c_int64),
+                ("lockstep_efficiency", ctypes.c_double)]
+
 STATS_DTYPE = np.dtype([
     ("steps_accepted", "<i8"), ("steps_rejected", "<i8"), ("rhs_evals", "<i8"),
     ("spec_rad_evals", "<i8"), ("stages_total", "<i8"), ("h_min_seen", "<f8"),

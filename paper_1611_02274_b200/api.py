@@ -96,6 +96,7 @@ def lib():
         "bode_set_persistent": (ctypes.c_int, [c_i32]),
         "bode_set_wide": (ctypes.c_int, [c_i32]),
         "bode_set_attempt_budget": (ctypes.c_int, [c_i64]),
+        "bode_stats_summary": (ctypes.c_int, [vp, c_i64, P(A.StatsSummary)]),
         "bode_register_kernels": (ctypes.c_int, [vp, c_i32, c_i32]),
         "bode_order_init": (ctypes.c_int, [vp, c_i64, vp]),
         "bode_repack_by_cost": (ctypes.c_int, [P(A.Problem), c_i64, vp, vp, vp, vp, vp]),
@@ -388,6 +389,17 @@ def lockstep_efficiency(problem: OdeProblem, solver, arith, num: int, stats_ptr:
                                          _arith(arith), num, ctypes.c_void_p(stats_ptr),
                                          ctypes.byref(eff), ctypes.c_void_p(stream or None)))
     return eff.value
+
+
+def stats_summary(stats: np.ndarray) -> dict:
+    """Straggler report over per-system stats (bode_stats_summary): attempt
+    totals, the costliest system, underflow / budget counts and the lockstep
+    efficiency of consecutive 32-system warps."""
+    st = np.ascontiguousarray(stats, dtype=A.STATS_DTYPE)
+    out = A.StatsSummary()
+    check(lib().bode_stats_summary(st.ctypes.data_as(ctypes.c_void_p), st.size,
+                                   ctypes.byref(out)))
+    return {k: getattr(out, k) for k, _ in A.StatsSummary._fields_}
 
 
 # ------------------------------------------------------------- problems ----

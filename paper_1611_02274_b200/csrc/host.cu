@@ -876,6 +876,37 @@ int bode_problem_supported(const bode_problem_t* p, int32_t solver, int32_t arit
     return (p && find_entry(p, solver, arith)) ? 1 : 0;
 }
 
+int bode_stats_summary(const bode_stats_t* st, int64_t num, bode_stats_summary_t* out) {
+    if (st == nullptr || out == nullptr || num < 1)
+        return fail(BODE_E_INVALID_SHAPE, "stats summary: NULL pointer or num < 1");
+    bode_stats_summary_t r{};
+    r.num = num;
+    r.attempts_argmax = 0;
+    double warp_max_sum = 0.0;
+    for (int64_t w = 0; w < num; w += 32) {
+        int64_t wmax = 0;
+        const int64_t wend = std::min<int64_t>(num, w + 32);
+        for (int64_t i = w; i < wend; ++i) {
+            const int64_t a = st[i].steps_accepted + st[i].steps_rejected;
+            r.attempts_total += a;
+            if (a > r.attempts_max) {
+                r.attempts_max = a;
+                r.attempts_argmax = i;
+            }
+            r.rhs_evals_total += st[i].rhs_evals;
+            r.rhs_evals_max = std::max<int64_t>(r.rhs_evals_max, st[i].rhs_evals);
+            wmax = std::max<int64_t>(wmax, st[i].rhs_evals);
+            r.underflow_count += st[i].underflow ? 1 : 0;
+            r.budget_exhausted_count += st[i].budget_exhausted ? 1 : 0;
+        }
+        warp_max_sum += (double)(wend - w) * (double)wmax;
+    }
+    r.attempts_mean = (double)r.attempts_total / (double)num;
+    r.lockstep_efficiency = warp_max_sum > 0 ? (double)r.rhs_evals_total / warp_max_sum : 1.0;
+    *out = r;
+    return BODE_OK;
+}
+
 int64_t bode_num_windows(double t0, double t_end, double h_outer) {
     const double ratio = (t_end - t0) / h_outer;  // batch_driver.cpp:99-100
     const long n = static_cast<long>(std::ceil(ratio - 1e-9));

@@ -150,3 +150,25 @@ def test_scheduling_knob_validation():
                                   None) == A.E_INVALID_SHAPE
     assert L.bode_repack_by_param(ctypes.byref(prob), 8, ctypes.c_void_p(8), ctypes.c_void_p(8),
                                   None, ctypes.c_void_p(8), 1, None) == A.E_INVALID_SHAPE
+
+
+def test_stats_summary_straggler_report():
+    """bode_stats_summary (host-side): the costliest system, totals, flag counts
+    and the lockstep efficiency of consecutive 32-system warps."""
+    st = np.zeros(40, dtype=A.STATS_DTYPE)
+    st["steps_accepted"] = 8
+    st["steps_rejected"] = 1
+    st["rhs_evals"] = 50
+    st["steps_accepted"][37] = 900  # a straggler in the second (partial) warp
+    st["rhs_evals"][37] = 5000
+    st["underflow"][3] = 1
+    st["budget_exhausted"][37] = 1
+    r = B.stats_summary(st)
+    assert r["num"] == 40 and r["attempts_max"] == 901 and r["attempts_argmax"] == 37
+    assert r["attempts_total"] == 39 * 9 + 901
+    assert r["underflow_count"] == 1 and r["budget_exhausted_count"] == 1
+    assert r["rhs_evals_max"] == 5000
+    expect = (39 * 50 + 5000) / (32 * 50 + 8 * 5000)
+    assert abs(r["lockstep_efficiency"] - expect) < 1e-15
+    with pytest.raises(B.InvalidShape):
+        B.stats_summary(st[:0])

@@ -66,3 +66,32 @@ for p in $PARTS; do
     lat) [ -x tools/fp64_latency ] && timeout 120 tools/fp64_latency > $OUT/fp64_latency.json 2>&1; echo "lat rc=$?" >> $OUT/status.txt ;;
   esac
 done
+# ncu with on-box post-processing: only summaries come back (gpurun_out <= 64 MiB)
+for p in $PARTS; do
+  case $p in
+    ncu2)
+      NCUP=/tmp/ncu_$TAG; mkdir -p $NCUP
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file $NCUP/launches.csv python bench.py --steps 20 --warmup 5 > $OUT/ncu_launches_bench.txt 2>&1
+      echo "ncu_launches rc=$?" >> $OUT/status.txt
+      python tools/ncu_summary.py --launches $NCUP/launches.csv $OUT/launches > /dev/null 2>&1
+      gzip -c $NCUP/launches.csv > $OUT/launches.csv.gz
+      cap() {  # name regex skip systems args...
+        local n=$1 k=$2 s=$3 sys=$4; shift 4
+        timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+          -k regex:$k -s $s -c 1 -o $NCUP/$n python bench.py "$@" > $OUT/ncu_full_$n.txt 2>&1
+        echo "ncu_$n rc=$?" >> $OUT/status.txt
+        python tools/ncu_lines.py $NCUP/$n.ncu-rep 60 > $OUT/lines_$n.txt 2>&1
+        SPECS="$SPECS $n=$NCUP/$n.ncu-rep:$sys"
+      }
+      SPECS=""
+      cap rkck_fast Pleiades 1 16777216 --steps 2 --warmup 1 --systems 16777216 --no-secondary --no-e2e --no-cpu
+      cap rkck_exact Pleiades 1 4194304 --arith exact --steps 2 --warmup 1 --systems 4194304 --no-secondary --no-e2e --no-cpu
+      cap heat_exact Heat 1 4194304 --steps 2 --warmup 1 --systems 4096 --rkc-systems 4194304 --aux-systems 0 --no-e2e --no-cpu
+      cap heat_fast Heat 4 4194304 --steps 2 --warmup 1 --systems 4096 --rkc-systems 4194304 --aux-systems 0 --no-e2e --no-cpu
+      python tools/ncu_summary.py $OUT/ncu $SPECS > $OUT/ncu_summary.txt 2>&1
+      echo "ncu_summary rc=$?" >> $OUT/status.txt
+      ls -la $NCUP > $OUT/ncu_reports_ls.txt ;;
+    newtests) timeout 1200 python -m pytest tests -x -q -m gpu -k "wide or budget" > $OUT/pytest_new.txt 2>&1; echo "newtests rc=$?" >> $OUT/status.txt ;;
+  esac
+done
