@@ -1156,7 +1156,8 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
                                                 cudaMemcpyHostToDevice, s));
             }
             if (presort) {
-                if ((r = bode::repack_by(N, P, cnt, B.y, B.g, B.st, B.ord, presort_row, s)))
+                // before window 1 the stats hold nothing yet (window 1 overwrites them)
+                if ((r = bode::repack_by(N, P, cnt, B.y, B.g, nullptr, B.ord, presort_row, s)))
                     return fail(r, "presort failed");
                 repacked[si] = 1;
             }

@@ -120,10 +120,22 @@ struct RkcCoefGen {
 // the 128-register cap.
 // Lane groups (L > 1) add C doubles of scratch for the sequential sums
 // (rkc_seq_sum): each lane posts its terms there for its group.
+// Lane groups also keep the controller scalars that live across the whole
+// window but are touched once per attempt (kRkcCtrl doubles: cbrt(errOld),
+// hOld, the rejected step, the spectral radius, cbrt(uround)) in the row, so
+// they hold no registers (or spill slots) through the stage loop.
+#ifndef BODE_RKC_CTRL_SMEM
+#define BODE_RKC_CTRL_SMEM 1
+#endif
+constexpr int kRkcCtrl = BODE_RKC_CTRL_SMEM ? 5 : 0;
 template <int C, int L = 1>
-__host__ __device__ constexpr int kRkcSmemStride() { return ((L > 1 ? 4 : 3) * C + 8) | 1; }
+__host__ __device__ constexpr int kRkcSmemStride() {
+    return ((L > 1 ? 4 : 3) * C + 8 + (L > 1 ? kRkcCtrl : 0)) | 1;
+}
 template <int C>
 __host__ __device__ constexpr int kRkcTermsOffset() { return 3 * C + 8; }
+template <int C>
+__host__ __device__ constexpr int kRkcCtrlOffset() { return 4 * C + 8; }
 
 // Per-device coefficient table for s = 2..kRkcTableMaxS: row(s) holds
 // muTilde_1 followed by (mu_j, nu_j, muTilde_j, gammaTilde_j, c_{j-1}) for
@@ -715,9 +727,24 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
     long long mMax = llround(val(sqrt_(relTol / (R(10.0) * uround))));
     if (mMax < 2) mMax = 2;
 
-    R wsErrOld(0.0), wsHOld(0.0), wsH(0.0), wsSpecRad(0.0);  // Workspace::reset
+    R wsErrOld(0.0), wsH(0.0);  // Workspace::reset
+#if BODE_RKC_CTRL_SMEM
+    double* const ctrl = bode_smem + threadIdx.x * kRkcSmemStride<C, L>() + kRkcCtrlOffset<C>();
+    R& cbErrOld = *reinterpret_cast<R*>(ctrl);      // cbrt(wsErrOld), once a step was accepted
+    R& wsHOld = *reinterpret_cast<R*>(ctrl + 1);
+    R& hNewRej = *reinterpret_cast<R*>(ctrl + 2);
+    R& wsSpecRad = *reinterpret_cast<R*>(ctrl + 3);
+    R& cbrtU = *reinterpret_cast<R*>(ctrl + 4);     // cbrt(errOld) when errOld is floored at uround
+    cbErrOld = R(0.0);
+    wsHOld = R(0.0);
+    hNewRej = R(0.0);
+    wsSpecRad = R(0.0);
+    cbrtU = cbrt_(uround);
+#else
+    R wsHOld(0.0), wsSpecRad(0.0), hNewRej(0.0);
     R cbErrOld(0.0);  // cbrt(wsErrOld), valid once a step was accepted
     const R cbrtU = cbrt_(uround);  // cbrt(errOld) when errOld is floored at uround
+#endif
     long long numStep = 0;
     // f0 and the power-method eigenvector live in this lane's shared-memory
     // row (stride kRkcSmemStride<C, L>, odd => conflict-free): f0 is read once
@@ -739,7 +766,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
     ++st.rhs_evals;
 
     int state = kTop;
-    R hMin(0.0), hNewRej(0.0);
+    R hMin(0.0);
     // The scalar transitions (no shuffles): the tail of a rejection
     // (rkc.cpp:255-264) and the top of the loop (rkc.cpp:223-229).
     auto advance = [&]() {

@@ -49,8 +49,12 @@ __device__ __forceinline__ void stats_merge(DevStats& a, const DevStats& b) {
 // The opt-in per-window attempt budget (bode_set_attempt_budget; not in the
 // reference, off by default): true once this window's attempts reach it. The
 // caller then freezes the system at its last accepted state, as on underflow.
+#ifndef BODE_ATTEMPT_BUDGET
+#define BODE_ATTEMPT_BUDGET 1
+#endif
 __device__ __forceinline__ bool budget_spent(DevStats& st, const DevTol& tol) {
-    if (tol.max_attempts > 0 && st.steps_accepted + st.steps_rejected >= tol.max_attempts) {
+    if (BODE_ATTEMPT_BUDGET && tol.max_attempts > 0 &&
+        st.steps_accepted + st.steps_rejected >= tol.max_attempts) {
         st.budget_exhausted = 1;
         return true;
     }

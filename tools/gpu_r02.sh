@@ -95,3 +95,21 @@ for p in $PARTS; do
     newtests) timeout 1200 python -m pytest tests -x -q -m gpu -k "wide or budget" > $OUT/pytest_new.txt 2>&1; echo "newtests rc=$?" >> $OUT/status.txt ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    ab_ctrl)  # RKC controller scalars in shared memory (new) vs registers (lib/ab/ctrl0), alternating
+      I=0; for V in ctrl0 nobudget new ctrl0 nobudget new; do I=$((I+1))
+        if [ $V = new ]; then LP=; else LP=$PWD/paper_1611_02274_b200/lib/ab/$V/libbode.so; fi
+        BODE_LIB_PATH=$LP timeout 600 python bench.py --steps 5 --warmup 1 --systems 4096 --rkc-systems 4194304 \
+          --aux-systems 4194304 --no-e2e --no-cpu > $OUT/ab_ctrl_${I}_$V.txt 2>&1; done
+      echo "ab_ctrl rc=$?" >> $OUT/status.txt ;;
+    ncuheat)
+      NCUP=/tmp/ncu_$TAG; mkdir -p $NCUP
+      timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+        -k regex:Heat -s 1 -c 1 -o $NCUP/heat_exact python bench.py --steps 2 --warmup 1 --systems 4096 \
+        --rkc-systems 4194304 --aux-systems 0 --no-e2e --no-cpu > $OUT/ncu_full_heat_exact.txt 2>&1
+      echo "ncuheat rc=$?" >> $OUT/status.txt
+      python tools/ncu_lines.py $NCUP/heat_exact.ncu-rep 60 > $OUT/lines_heat_exact.txt 2>&1
+      python tools/ncu_summary.py $OUT/ncu_heat heat_exact=$NCUP/heat_exact.ncu-rep:4194304 > /dev/null 2>&1 ;;
+  esac
+done

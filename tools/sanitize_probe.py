@@ -46,6 +46,18 @@ def main():
                  sink=lambda t, s: snaps.append(t))
     B.outer_loop(pl, b, 0.0, 0.3, 0.1, solver="rkck", arith="fast", gpus=2,
                  sink=lambda t, s: snaps.append(t))
+    # heat with a run-time dimension: one system per block (csrc/wide.cuh), vectors
+    # in shared memory (n = 100) and in the per-block global scratch (n = 4000)
+    for n, t1 in ((100, 1e-3), (4000, 1e-5)):
+        hw = B.problems.heat_equation(n)
+        wb = B.problems.perturb_initial_conditions(heat_ic(n), 0.01, 3, 20)
+        for solver in ("rkc", "rkck"):
+            B.integrate_batch(hw, wb, 0.0, t1, solver=solver, arith="exact")
+        B.integrate_batch(hw, wb, 0.0, t1, solver="rkc", arith="fast")
+    L.bode_set_attempt_budget(5)
+    B.integrate_batch(pl, b, 0.0, 0.1, solver="rkck", arith="fast")
+    B.integrate_batch(heat, hb, 0.0, 0.1, solver="rkc", arith="exact")
+    L.bode_set_attempt_budget(0)
     B.integrate_fixed(pl, b, 0.0, 0.1, 10, solver="rkck")
     B.integrate_fixed(heat, hb, 0.0, 0.01, 4, solver="rkc", stages=5)
     assert len(snaps) == 6
