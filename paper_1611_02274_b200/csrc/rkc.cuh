@@ -563,6 +563,8 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
     R cbErrOld(0.0);  // cbrt(wsErrOld), valid once a step was accepted
     const R cbrtU = cbrt_(uround);  // cbrt(errOld) when errOld is floored at uround
     long long numStep = 0;
+    AttemptBudget bud;
+    bud.init(tol);
     // f0 and the power-method eigenvector live in this lane's shared-memory
     // row (stride kRkcSmemStride<C>, odd => conflict-free): f0 is read once
     // per element per stage, eig only by the power method; registers go to
@@ -590,7 +592,7 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
         BODE_PHASE_CTRL_END
         if (state == kTop) {
             if (!(tEnd - t > uround * fabs_(tEnd))) break;
-            if (budget_spent(st, tol)) break;
+            if (bud.spent(st)) break;
             hMin = R(10.0) * uround * fmax_(fabs_(t), hMax);
             if (R(1.1) * wsH >= fabs_(tEnd - t)) wsH = fabs_(tEnd - t);
             state = (numStep % 25 == 0) ? kSrThenAttempt : kAttempt;
@@ -746,6 +748,8 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
     const R cbrtU = cbrt_(uround);  // cbrt(errOld) when errOld is floored at uround
 #endif
     long long numStep = 0;
+    AttemptBudget bud;
+    bud.init(tol);
     // f0 and the power-method eigenvector live in this lane's shared-memory
     // row (stride kRkcSmemStride<C, L>, odd => conflict-free): f0 is read once
     // per element per stage, eig only by the power method; registers go to
@@ -782,7 +786,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
         if (live && state == kTop) {
             if (!(tEnd - t > uround * fabs_(tEnd))) {
                 live = false;
-            } else if (budget_spent(st, tol)) {
+            } else if (bud.spent(st)) {
                 live = false;
             } else {
                 hMin = R(10.0) * uround * fmax_(fabs_(t), hMax);

@@ -47,19 +47,38 @@ __device__ __forceinline__ void stats_merge(DevStats& a, const DevStats& b) {
 }
 
 // The opt-in per-window attempt budget (bode_set_attempt_budget; not in the
-// reference, off by default): true once this window's attempts reach it. The
-// caller then freezes the system at its last accepted state, as on underflow.
+// reference, off by default). A register countdown: no stats loads on the
+// serial controller path. When it runs out, the caller freezes the system at
+// its last accepted state, as on underflow.
 #ifndef BODE_ATTEMPT_BUDGET
 #define BODE_ATTEMPT_BUDGET 1
 #endif
-__device__ __forceinline__ bool budget_spent(DevStats& st, const DevTol& tol) {
-    if (BODE_ATTEMPT_BUDGET && tol.max_attempts > 0 &&
-        st.steps_accepted + st.steps_rejected >= tol.max_attempts) {
-        st.budget_exhausted = 1;
-        return true;
+struct AttemptBudget {
+    long long left;  // attempts still allowed (no budget: more than any window makes)
+    __device__ __forceinline__ void init(const DevTol& tol) {
+        left = tol.max_attempts > 0 ? tol.max_attempts : 0x7fffffffffffffffll;
     }
-    return false;
-}
+    // before an attempt: true (and the stats flag) if none is left, else charges one
+    __device__ __forceinline__ bool spent(DevStats& st) {
+        if (!BODE_ATTEMPT_BUDGET) return false;
+        if (left <= 0) {
+            st.budget_exhausted = 1;
+            return true;
+        }
+        --left;
+        return false;
+    }
+    // after an attempt of a system that is still live: charges it and reports
+    // whether that was the last one allowed
+    __device__ __forceinline__ bool spent_after(DevStats& st) {
+        if (!BODE_ATTEMPT_BUDGET) return false;
+        if (--left <= 0) {
+            st.budget_exhausted = 1;
+            return true;
+        }
+        return false;
+    }
+};
 
 // Cash-Karp tableau (rkck.cpp:8-27), evaluated as the same double quotients.
 namespace ck {
@@ -146,10 +165,12 @@ __device__ __forceinline__ void rkck_system(const Group<L>& G, double t_in, doub
     R f0[C];
     KStore<R, C, KSMEM> K;
     bool haveF = false;
+    AttemptBudget bud;
+    bud.init(tol);
 
 #pragma unroll 1
     while (tEnd - t > uround * fabs_(tEnd)) {
-        if (budget_spent(st, tol)) break;
+        if (bud.spent(st)) break;
         h = fmin_(tEnd - t, h);
         R arg[C], out[C];
         if (!haveF) {  // rejected retries reuse f(t, y) (rkck.cpp:133-137)

@@ -105,6 +105,7 @@ struct NystromRkck {
     R t, tEnd, hMax, h;
     bool haveF, live;
     DevStats st;
+    AttemptBudget bud;  // bode_set_attempt_budget (off by default)
     double* ks;         // this lane's shared-memory row (k2..k5 / k6)
     const R* gp = nullptr;  // the system's parameters (problems with P > 0)
 
@@ -125,6 +126,7 @@ struct NystromRkck {
         h = R(0.5) * fabs_(tEnd - t);
         haveF = false;
         live = tEnd - t > R(tol.uround) * fabs_(tEnd);  // rkck.cpp:131
+        bud.init(tol);
     }
 
     // one pass of the while loop of rkck.cpp:131-157
@@ -341,7 +343,7 @@ struct NystromRkck {
             }
             h = R(hNew);
         }
-        if (live && budget_spent(st, tol)) live = false;
+        if (live && bud.spent_after(st)) live = false;
     }
 
     // error norm, controller and the accept/reject update of one attempt
@@ -474,7 +476,7 @@ struct NystromRkck {
             }
             h = hNew;
         }
-        if (live && budget_spent(st, tol)) live = false;
+        if (live && bud.spent_after(st)) live = false;
     }
 };
 

@@ -122,6 +122,8 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
     R A0[M];
     bool haveF = false;
     bool live = tEnd - t > uround * fabs_(tEnd);  // rkck.cpp:131
+    AttemptBudget bud;
+    bud.init(tol);
 
     // Warp-uniform loop: the warp iterates while any of its systems is live,
     // so every shuffle runs with the full mask (no collective fix-up code).
@@ -323,7 +325,7 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
             h = hNew;
         }
         if (live) live = tEnd - t > uround * fabs_(tEnd);
-        if (live && budget_spent(st, tol)) live = false;
+        if (live && bud.spent_after(st)) live = false;
     }
 }
 

@@ -142,9 +142,11 @@ __device__ void rkck_wide_system(const WideVecs& V, double t_in, double tEnd_in,
     R h = R(0.5) * fabs_(tEnd - t);
     const R uround(tol.uround), eps(tol.eps), tiny(tol.tiny);
     bool haveF = false;
+    AttemptBudget bud;
+    bud.init(tol);
 #pragma unroll 1
     while (tEnd - t > uround * fabs_(tEnd)) {
-        if (budget_spent(st, tol)) break;
+        if (bud.spent(st)) break;
         h = fmin_(tEnd - t, h);
         if (!haveF) {  // rejected retries reuse f(t, y) (rkck.cpp:133-137)
             wide_rhs<Prob, R>(V, t, y, f0);
@@ -287,6 +289,8 @@ __device__ void rkc_wide_system(const WideVecs& V, double t_in, double tEnd_in,
     const R cbrtU = cbrt_(uround);
     long long numStep = 0;
     const R nR = R(static_cast<double>(n));
+    AttemptBudget bud;
+    bud.init(tol);
 
     wide_rhs<Prob, R>(V, t, y, f0);  // rkc.cpp:209-212
     ++st.rhs_evals;
@@ -301,7 +305,7 @@ __device__ void rkc_wide_system(const WideVecs& V, double t_in, double tEnd_in,
     };
 #pragma unroll 1
     while (tEnd - t > uround * fabs_(tEnd)) {
-        if (budget_spent(st, tol)) break;
+        if (bud.spent(st)) break;
         const R hMin = R(10.0) * uround * fmax_(fabs_(t), hMax);
         if (R(1.1) * wsH >= fabs_(tEnd - t)) wsH = fabs_(tEnd - t);
         if (numStep % 25 == 0) estimate();

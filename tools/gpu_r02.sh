@@ -113,3 +113,12 @@ for p in $PARTS; do
       python tools/ncu_summary.py $OUT/ncu_heat heat_exact=$NCUP/heat_exact.ncu-rep:4194304 > /dev/null 2>&1 ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    ab_budget)  # attempt-budget countdown (new) vs compiled out (lib/ab/nobudget), full default sizes
+      I=0; for V in nobudget new nobudget new; do I=$((I+1))
+        if [ $V = new ]; then LP=; else LP=$PWD/paper_1611_02274_b200/lib/ab/$V/libbode.so; fi
+        BODE_LIB_PATH=$LP timeout 900 python bench.py --steps 5 --warmup 1 --no-e2e --no-cpu > $OUT/ab_budget_${I}_$V.txt 2>&1; done
+      echo "ab_budget rc=$?" >> $OUT/status.txt ;;
+  esac
+done
