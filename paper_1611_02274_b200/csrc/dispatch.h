@@ -77,6 +77,10 @@ struct KernelEntry {
     // 1: one system per thread block for any dimension (wide.cuh), dim == 0;
     // chosen when no lane-group kernel is compiled for the problem's dim
     int wide = 0;
+    // instances with the attempt-budget check (bode_set_attempt_budget), launched
+    // in place of fn / pfn while a budget is set
+    const void* bfn = nullptr;
+    const void* bpfn = nullptr;
 };
 
 const KernelEntry* kernel_table(int* count);

@@ -366,7 +366,10 @@ int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double*
     const long long grid = (threads + block - 1) / block;
     const size_t smem = (size_t)e->smem_per_thread * block;
     const bool persistent = e->launch_persistent != nullptr && g_persistent.load();
-    const void* fn = persistent ? e->pfn : e->fn;
+    const bool budget = tol.max_attempts > 0;
+    const void* fn = persistent ? (budget ? e->bpfn : e->pfn) : (budget ? e->bfn : e->fn);
+    if (fn == nullptr)
+        return fail(BODE_E_UNSUPPORTED, "no kernel instance with the attempt-budget check");
     {
         // current device and the per-device smem attribute, in the runtime that
         // owns the kernel (idempotent and cheap, so done on every launch)

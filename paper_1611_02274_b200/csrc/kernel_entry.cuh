@@ -34,7 +34,7 @@ __device__ __forceinline__ int comp_index(int lane, int c) {
 
 // MAXREG > 0 caps registers per thread (__maxnreg__) to reach a target
 // occupancy; 0 leaves ptxas the full 255 (launch bound kMaxBlock threads).
-template <class P, class R, int L, int SOLVER, bool KSMEM, int MAXREG>
+template <class P, class R, int L, int SOLVER, bool KSMEM, int MAXREG, bool BUDGET>
 __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
     integrate_kernel(const double* __restrict__ g_soa, double* __restrict__ y_soa,
                      DevStats* __restrict__ stats, long long num, double t, double tEnd,
@@ -60,15 +60,15 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
         g[p] = R(P::P > 0 && inRange ? g_soa[sys + ld * (long long)p] : 0.0);
     DevStats st;
     if constexpr (SOLVER == 0 && is_pleiades<P> && L == 2)
-        rkck_pleiades2_system<R>(G, t, tEnd, y, tol, st);
+        rkck_pleiades2_system<R, BUDGET>(G, t, tEnd, y, tol, st);
     else if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1)
-        rkck_nystrom_system<P, R>(t, tEnd, y, g, tol, st);
+        rkck_nystrom_system<P, R, BUDGET>(t, tEnd, y, g, tol, st);
     else if constexpr (SOLVER == 0)
-        rkck_system<P, R, L, KSMEM>(G, t, tEnd, y, g, tol, st);
+        rkck_system<P, R, L, KSMEM, BUDGET>(G, t, tEnd, y, g, tol, st);
     else if constexpr (L == 1)
-        rkc_system_lane<P, R>(G, t, tEnd, y, g, tol, st);
+        rkc_system_lane<P, R, BUDGET>(G, t, tEnd, y, g, tol, st);
     else
-        rkc_system<P, R, L>(G, inRange, t, tEnd, y, g, tol, st);
+        rkc_system<P, R, L, BUDGET>(G, inRange, t, tEnd, y, g, tol, st);
     if (!inRange) return;
 #pragma unroll
     for (int c = 0; c < C; ++c) y_soa[sys + ld * (long long)comp_index<P, L>(G.lane, c)] = val(y[c]);
@@ -84,12 +84,12 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
 }
 
 // Persistent-grid RKCK for second-order problems, one lane per system.
-template <class P, class R>
+template <class P, class R, bool BUDGET>
 __global__ void __launch_bounds__(kMaxBlock)
     persistent_kernel(const double* __restrict__ g_soa, double* __restrict__ y_soa,
                       DevStats* __restrict__ stats, long long num, double t, double tEnd,
                       DevTol tol, int merge, unsigned long long* counter) {
-    rkck_nystrom_persistent<P, R>(g_soa, y_soa, stats, num, t, tEnd, tol, merge, counter,
+    rkck_nystrom_persistent<P, R, BUDGET>(g_soa, y_soa, stats, num, t, tEnd, tol, merge, counter,
                                   tol.refill_min);
 }
 
@@ -110,7 +110,8 @@ static KernelEntry make_entry(int kind, int arith) {
         e.smem_per_thread = SOLVER == 1 ? kRkcSmemStride<C_of<P, L>(), L>() * (int)sizeof(double)
                             : KSMEM     ? kSmemStride<C_of<P, L>()>() * (int)sizeof(double)
                                         : 0;
-    e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG>;
+    e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG, false>;
+    e.bfn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG, true>;
     e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                   const double* g, double* y, DevStats* st, long long num, double t,
                   double tEnd, DevTol tol, int merge) -> int {
@@ -141,7 +142,8 @@ static KernelEntry make_entry(int kind, int arith) {
     if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1 && P::P == 0) {
         // (routing static launches through this instance with counter == nullptr
         // removes the spills but measured 9% slower: the any_sync loop costs more)
-        e.pfn = (const void*)&persistent_kernel<P, R>;
+        e.pfn = (const void*)&persistent_kernel<P, R, false>;
+        e.bpfn = (const void*)&persistent_kernel<P, R, true>;
         e.launch_persistent = [](const void* fn, dim3 grid, dim3 block, size_t smem,
                                  cudaStream_t s, const double* g, double* y, DevStats* st,
                                  long long num, double t, double tEnd, DevTol tol, int merge,
@@ -176,6 +178,7 @@ static KernelEntry make_wide_entry(int kind, int arith) {
     e.default_block = 0;
     e.wide = 1;
     e.fn = (const void*)&wide_kernel<Prob, R, SOLVER>;
+    e.bfn = e.fn;  // the block kernels always carry the (cheap, per-block) check
     e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                   const double* g, double* y, DevStats* st, long long num, double t,
                   double tEnd, DevTol tol, int merge) -> int {

@@ -1,13 +1,19 @@
 // kernels.cu -- the built-in dispatch table: one entry per (problem, solver,
 // arithmetic policy, lane-group width, register cap) compiled for sm_100a.
 // The kernel templates themselves are in kernel_entry.cuh.
+#include <vector>
+
 #include "kernel_entry.cuh"
 
 namespace bode {
 
 long long rkc_table_doubles() { return kRkcTableDoubles; }
 
-const KernelEntry* kernel_table(int* count) {
+// kernels_rkc.cu: the RKC entries and the one-system-per-block heat kernels
+// (a second translation unit, so the two halves compile in parallel)
+const KernelEntry* kernel_table_rkc(int* count);
+
+static const KernelEntry* kernel_table_rkck(int* count) {
     static const KernelEntry table[] = {
         // RKCK (nonstiff): Pleiades stages in shared memory, small systems in registers
         // Pleiades: FAST defaults to one lane per system (255 registers, 8 warps/SM);
@@ -28,40 +34,23 @@ const KernelEntry* kernel_table(int* count) {
         BODE_BOTH_ARITH(Const<1>, 1, 0, false, 7),
         BODE_BOTH_ARITH(SinT, 1, 0, false, 8),
         BODE_BOTH_ARITH(Heat<8>, 1, 0, false, 1),
-        // RKC (moderately stiff)
-        // heat64: 8 lanes per system capped at 128 registers (16 warps/SM) is
-        // the default -- measured 16% over 4 lanes at 254 registers (8 warps/SM)
-        BODE_BOTH_ARITH_R(Heat<64>, 8, 1, false, 1, 128),
-        BODE_BOTH_ARITH(Heat<64>, 4, 1, false, 1),
-        BODE_BOTH_ARITH_R(Heat<64>, 4, 1, false, 1, 168),
-        BODE_BOTH_ARITH_R(Heat<64>, 8, 1, false, 1, 168),
-        BODE_BOTH_ARITH_R(Heat<64>, 8, 1, false, 1, 112),
-        BODE_BOTH_ARITH_R(Heat<64>, 8, 1, false, 1, 96),
-        BODE_BOTH_ARITH_R(Heat<64>, 16, 1, false, 1, 96),
-        BODE_BOTH_ARITH_R(Heat<64>, 16, 1, false, 1, 128),
-        BODE_BOTH_ARITH(Heat<32>, 4, 1, false, 1),
-        BODE_BOTH_ARITH(Heat<16>, 2, 1, false, 1),
-        BODE_BOTH_ARITH(Heat<8>, 1, 1, false, 1),
-        // expDecay (config 4, controller bound): 80 registers, 24 warps/SM --
-        // measured 1.63e8 vs 1.48e8 (128) and 1.23e8 (uncapped, 131) system-windows/s
-        BODE_BOTH_ARITH_R(ExpDecay, 1, 1, false, 2, 80),
-        BODE_BOTH_ARITH(ExpDecay, 1, 1, false, 2),
-        BODE_BOTH_ARITH_R(ExpDecay, 1, 1, false, 2, 128),
-        BODE_BOTH_ARITH_R(ExpDecay, 1, 1, false, 2, 96),
-        BODE_BOTH_ARITH_R(ExpDecay, 1, 1, false, 2, 64),
-        BODE_BOTH_ARITH(Harmonic, 1, 1, false, 3),
-        BODE_BOTH_ARITH(Zero<2>, 1, 1, false, 4),
-        BODE_BOTH_ARITH(Zero<1>, 1, 1, false, 4),
-        BODE_BOTH_ARITH(Diag<3>, 1, 1, false, 6),
-        BODE_BOTH_ARITH(Const<1>, 1, 1, false, 7),
-        // heatEquation(n) for any other n >= 2: one system per thread block
-        make_wide_entry<HeatWide, xd, 0>(1, 0),
-        make_wide_entry<HeatWide, double, 0>(1, 1),
-        make_wide_entry<HeatWide, xd, 1>(1, 0),
-        make_wide_entry<HeatWide, double, 1>(1, 1),
     };
     *count = (int)(sizeof(table) / sizeof(table[0]));
     return table;
+}
+
+const KernelEntry* kernel_table(int* count) {
+    static const std::vector<KernelEntry> all = [] {
+        std::vector<KernelEntry> v;
+        int n = 0;
+        const KernelEntry* a = kernel_table_rkck(&n);
+        v.insert(v.end(), a, a + n);
+        const KernelEntry* b = kernel_table_rkc(&n);
+        v.insert(v.end(), b, b + n);
+        return v;
+    }();
+    *count = (int)all.size();
+    return all.data();
 }
 
 }  // namespace bode

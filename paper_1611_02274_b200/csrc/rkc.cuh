@@ -542,7 +542,7 @@ __device__ __forceinline__ bool rkc_finish_attempt(R err, R h, R hMin, R hMax, R
 // machine as rkc_system below, each lane branching on its own state. (The
 // warp-uniform form measured 5% slower here: with no shuffles to save, its
 // extra predication only costs.)
-template <class P, class R>
+template <class P, class R, bool BUDGET>
 __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, double tEnd_in,
                                                 R (&y)[P::N], const R* g, const DevTol& tol,
                                                 DevStats& st_out) {
@@ -563,7 +563,7 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
     R cbErrOld(0.0);  // cbrt(wsErrOld), valid once a step was accepted
     const R cbrtU = cbrt_(uround);  // cbrt(errOld) when errOld is floored at uround
     long long numStep = 0;
-    AttemptBudget bud;
+    AttemptBudget<BUDGET> bud;
     bud.init(tol);
     // f0 and the power-method eigenvector live in this lane's shared-memory
     // row (stride kRkcSmemStride<C>, odd => conflict-free): f0 is read once
@@ -712,7 +712,7 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
 // (power method, initial step, stage loop, error norm), each group doing or
 // discarding the work by its own state. Groups with `live` clear (finished,
 // frozen, or past the batch's end) ride along; G carries the full warp mask.
-template <class P, class R, int L>
+template <class P, class R, int L, bool BUDGET>
 __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double t_in,
                                            double tEnd_in, R (&y)[P::N / L], const R* g,
                                            const DevTol& tol, DevStats& st_out) {
@@ -748,7 +748,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
     const R cbrtU = cbrt_(uround);  // cbrt(errOld) when errOld is floored at uround
 #endif
     long long numStep = 0;
-    AttemptBudget bud;
+    AttemptBudget<BUDGET> bud;
     bud.init(tol);
     // f0 and the power-method eigenvector live in this lane's shared-memory
     // row (stride kRkcSmemStride<C, L>, odd => conflict-free): f0 is read once

@@ -53,6 +53,10 @@ __device__ __forceinline__ void stats_merge(DevStats& a, const DevStats& b) {
 #ifndef BODE_ATTEMPT_BUDGET
 #define BODE_ATTEMPT_BUDGET 1
 #endif
+// Kernels are compiled with and without it (BUDGET template flag; the host
+// launches the budgeted instance only while a budget is set), so the default
+// path carries no budget code at all.
+template <bool ON = true>
 struct AttemptBudget {
     long long left;  // attempts still allowed (no budget: more than any window makes)
     __device__ __forceinline__ void init(const DevTol& tol) {
@@ -78,6 +82,12 @@ struct AttemptBudget {
         }
         return false;
     }
+};
+template <>
+struct AttemptBudget<false> {
+    __device__ __forceinline__ void init(const DevTol&) {}
+    __device__ __forceinline__ bool spent(DevStats&) { return false; }
+    __device__ __forceinline__ bool spent_after(DevStats&) { return false; }
 };
 
 // Cash-Karp tableau (rkck.cpp:8-27), evaluated as the same double quotients.
@@ -148,7 +158,7 @@ __device__ __forceinline__ bool rkck_adjust(R h, R err, bool nanFlag, R hMin, R 
 
 // One system (this lane's slice) from t to tEnd: rkck::driver (rkck.cpp:115-159).
 // y is updated in place; returns the window's stats.
-template <class P, class R, int L, bool KSMEM>
+template <class P, class R, int L, bool KSMEM, bool BUDGET>
 __device__ __forceinline__ void rkck_system(const Group<L>& G, double t_in, double tEnd_in,
                                             R (&y)[P::N / L], const R* g, const DevTol& tol,
                                             DevStats& st) {
@@ -165,7 +175,7 @@ __device__ __forceinline__ void rkck_system(const Group<L>& G, double t_in, doub
     R f0[C];
     KStore<R, C, KSMEM> K;
     bool haveF = false;
-    AttemptBudget bud;
+    AttemptBudget<BUDGET> bud;
     bud.init(tol);
 
 #pragma unroll 1

@@ -97,7 +97,7 @@ __device__ __forceinline__ void pleiades_accel_pair(const Group<2>& G, const R* 
     }
 }
 
-template <class R>
+template <class R, bool BUDGET>
 __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double t_in,
                                                       double tEnd_in, R (&y)[14],
                                                       const DevTol& tol, DevStats& st) {
@@ -122,7 +122,7 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
     R A0[M];
     bool haveF = false;
     bool live = tEnd - t > uround * fabs_(tEnd);  // rkck.cpp:131
-    AttemptBudget bud;
+    AttemptBudget<BUDGET> bud;
     bud.init(tol);
 
     // Warp-uniform loop: the warp iterates while any of its systems is live,

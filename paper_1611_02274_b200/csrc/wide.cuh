@@ -142,7 +142,7 @@ __device__ void rkck_wide_system(const WideVecs& V, double t_in, double tEnd_in,
     R h = R(0.5) * fabs_(tEnd - t);
     const R uround(tol.uround), eps(tol.eps), tiny(tol.tiny);
     bool haveF = false;
-    AttemptBudget bud;
+    AttemptBudget<true> bud;
     bud.init(tol);
 #pragma unroll 1
     while (tEnd - t > uround * fabs_(tEnd)) {
@@ -289,7 +289,7 @@ __device__ void rkc_wide_system(const WideVecs& V, double t_in, double tEnd_in,
     const R cbrtU = cbrt_(uround);
     long long numStep = 0;
     const R nR = R(static_cast<double>(n));
-    AttemptBudget bud;
+    AttemptBudget<true> bud;
     bud.init(tol);
 
     wide_rhs<Prob, R>(V, t, y, f0);  // rkc.cpp:209-212
