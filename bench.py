@@ -695,6 +695,11 @@ def main():
         "work_per_system_window": {
             "attempts": float((stats["steps_accepted"] + stats["steps_rejected"]).sum()) / (num * args.steps),
             "rhs_evals": float(stats["rhs_evals"].sum()) / (num * args.steps)},
+        # bode_stats_summary over the headline's stats (merged over the timed windows)
+        "straggler": {k: v for k, v in P.stats_summary(stats).items()
+                      if k in ("attempts_max", "attempts_argmax", "attempts_mean",
+                               "underflow_count", "budget_exhausted_count",
+                               "lockstep_efficiency")},
         "skipped_over_budget": skipped,
         "wall_s": time.monotonic() - T_START,
     }
