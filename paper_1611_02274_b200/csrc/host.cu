@@ -398,7 +398,10 @@ int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double*
     return BODE_OK;
 }
 
-constexpr int kMaxChunks = 32;  // host-pointer pipeline depth per shard
+#ifndef BODE_MAX_CHUNKS
+#define BODE_MAX_CHUNKS 32
+#endif
+constexpr int kMaxChunks = BODE_MAX_CHUNKS;  // host-pointer pipeline depth per shard
 
 // Device buffers, streams and events of one shard, leased exclusively for one
 // call: concurrent or nested calls (from another host thread, or from a sink)

@@ -122,3 +122,12 @@ for p in $PARTS; do
       echo "ab_budget rc=$?" >> $OUT/status.txt ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    ab_chunks)  # host-pointer pipeline depth: 32 (default) vs 64 / 128 chunks, e2e only matters
+      I=0; for V in new chunks64 chunks128 new chunks64 chunks128; do I=$((I+1))
+        if [ $V = new ]; then LP=; else LP=$PWD/paper_1611_02274_b200/lib/ab/$V/libbode.so; fi
+        BODE_LIB_PATH=$LP timeout 900 python bench.py --steps 10 --warmup 3 --no-secondary --no-cpu > $OUT/ab_chunks_${I}_$V.txt 2>&1; done
+      echo "ab_chunks rc=$?" >> $OUT/status.txt ;;
+  esac
+done
