@@ -61,3 +61,20 @@ def test_reference_ic_asset_matches_embedded(ref):
     out = np.empty(28)
     assert ref.lib.ref_load_pleiades_ic(path, A.dptr(out)) == 0
     assert np.array_equal(out, PLEIADES_IC)
+
+
+@pytest.mark.parametrize("n,solver,t1", [(2, A.SOLVER_RKC, 0.2), (5, A.SOLVER_RKCK, 0.05),
+                                         (100, A.SOLVER_RKC, 0.02), (513, A.SOLVER_RKC, 0.02),
+                                         (17, A.SOLVER_RKCK, 0.01), (4000, A.SOLVER_RKC, 1e-3)])
+def test_oracle_matches_reference_any_heat_dim(oracle, ref, n, solver, t1):
+    """heatEquation(n) at the dimensions the GPU runs on one-system-per-block
+    kernels (tests/test_gpu_wide.py checks those against this oracle)."""
+    num = 24
+    prob = A.make_problem(A.HEAT, n)
+    y0 = perturb(heat_ic(n), 0.01, 3 + n, num)
+    a = oracle.outer_loop(prob, solver, 0.0, t1, t1 / 2, y0)
+    b = ref.outer_loop(prob, solver, 0.0, t1, t1 / 2, y0)
+    assert a[0] == b[0] == 0
+    assert np.array_equal(a[1].view(np.uint64), b[1].view(np.uint64))
+    for k in COUNTS:
+        assert np.array_equal(a[2][k], b[2][k]), k
