@@ -81,6 +81,11 @@ struct KernelEntry {
     // in place of fn / pfn while a budget is set
     const void* bfn = nullptr;
     const void* bpfn = nullptr;
+    // one-system-per-block fixed-step harness (wide entries; ffn is its kernel)
+    int (*launch_fixed_wide)(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             const double* g, double* y, long long num, double t0, double tEnd,
+                             long long numSteps, long long stages, double kappa, int dim,
+                             double* scratch) = nullptr;
 };
 
 const KernelEntry* kernel_table(int* count);

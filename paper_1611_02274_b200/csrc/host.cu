@@ -1277,6 +1277,44 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
 }
 
 // Fixed-step harnesses (rkck.cpp:168-181, rkc.cpp:290-306), host pointers.
+// integrateFixed on a one-system-per-block kernel: vectors in shared memory
+// when they fit, else a per-block global scratch (as launch_wide).
+int fixed_wide(const KernelEntry* e, const bode_problem_t* p, double t0, double t_end,
+               int64_t num_steps, int32_t stages, double kappa, int64_t num, const double* g,
+               double* y) {
+    const int n = p->dim;
+    int dev = 0, sms = 0;
+    BODE_CUDA(cudaGetDevice(&dev));
+    BODE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int block = bode::wide_block(n);
+    const size_t vec_bytes = (size_t)bode::kWideVecs * (size_t)n * sizeof(double);
+    const bool in_smem = vec_bytes <= (size_t)bode::kWideSmemMax;
+    const size_t smem = in_smem ? vec_bytes : 0;
+    BODE_CUDA((cudaError_t)e->prepare(e->ffn, dev, (int)smem));
+    long long grid = 1;
+    if (in_smem) {
+        int per_sm = 0;
+        BODE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, e->ffn, block, smem));
+        grid = std::min<long long>(num, (long long)std::max(per_sm, 1) * sms);
+    } else {
+        const long long budget = std::max<long long>(1, (4LL << 30) / (long long)vec_bytes);
+        grid = std::min<long long>(num, std::min<long long>(2LL * sms, budget));
+    }
+    double *dy = nullptr, *scratch = nullptr;
+    BODE_CUDA(cudaMalloc(&dy, (size_t)num * n * sizeof(double)));
+    if (!in_smem) BODE_CUDA(cudaMalloc(&scratch, (size_t)grid * vec_bytes));
+    BODE_CUDA(cudaMemcpy(dy, y, (size_t)num * n * sizeof(double), cudaMemcpyHostToDevice));
+    cudaError_t le = (cudaError_t)e->launch_fixed_wide(e->ffn, dim3((unsigned)grid), dim3(block),
+                                                       smem, 0, nullptr, dy, num, t0, t_end, num_steps,
+                                                       stages, kappa, n, scratch);
+    g_launches.fetch_add(1);
+    if (le == cudaSuccess) le = cudaMemcpy(y, dy, (size_t)num * n * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(dy);
+    if (scratch) cudaFree(scratch);
+    BODE_CUDA(le);
+    return BODE_OK;
+}
+
 int bode_integrate_fixed(const bode_problem_t* p, int32_t solver, int32_t arith, double t0,
                          double t_end, int64_t num_steps, int32_t stages, double kappa,
                          int64_t num, const double* g, double* y) {
@@ -1289,6 +1327,10 @@ int bode_integrate_fixed(const bode_problem_t* p, int32_t solver, int32_t arith,
     const KernelEntry* e = nullptr;
     int rc = validate_call(p, solver, arith, t0, t_end, num, g, y, &tol, &e);
     if (rc) return rc;
+    if (e->wide) {  // one system per block (wide.cuh), any dimension
+        if ((rc = check_devices(1))) return rc;
+        return fixed_wide(e, p, t0, t_end, num_steps, stages, kappa, num, g, y);
+    }
     if (e->launch_fixed == nullptr) {  // e.g. the lane-pair Pleiades kernel: try the others
         int n = 0;
         const KernelEntry* tab = bode::kernel_table(&n);

@@ -179,6 +179,16 @@ static KernelEntry make_wide_entry(int kind, int arith) {
     e.wide = 1;
     e.fn = (const void*)&wide_kernel<Prob, R, SOLVER>;
     e.bfn = e.fn;  // the block kernels always carry the (cheap, per-block) check
+    e.ffn = (const void*)&wide_fixed_kernel<Prob, R, SOLVER>;
+    e.launch_fixed_wide = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             const double* g, double* y, long long num, double t0, double tEnd,
+                             long long numSteps, long long stages, double kappa, int dim,
+                             double* scratch) -> int {
+        auto k = (void (*)(const double*, double*, long long, double, double, long long,
+                           long long, double, int, double*))fn;
+        k<<<grid, block, smem, s>>>(g, y, num, t0, tEnd, numSteps, stages, kappa, dim, scratch);
+        return (int)cudaGetLastError();
+    };
     e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                   const double* g, double* y, DevStats* st, long long num, double t,
                   double tEnd, DevTol tol, int merge) -> int {

@@ -125,6 +125,43 @@ __device__ __forceinline__ void wide_rhs(const WideVecs& V, R t, const double* u
     __syncthreads();
 }
 
+// rkck::step's five stage evaluations (rkck.cpp:42-64): k2..k6 in V.a..V.e
+// from y and f0 = f(t, y), the stage argument in V.f.
+template <class Prob, class R>
+__device__ __forceinline__ void rkck_wide_stages(const WideVecs& V, R t, R h, const double* y,
+                                                 const double* f0) {
+    using namespace ck;
+    const int n = V.n;
+    double *k2 = V.a, *k3 = V.b, *k4 = V.c, *k5 = V.d, *k6 = V.e, *yt = V.f;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        yt[i] = val(R(y[i]) + h * R(b21) * R(f0[i]));
+    wide_rhs<Prob, R>(V, t + R(a2) * h, yt, k2);
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        yt[i] = val(R(y[i]) + h * (R(b31) * R(f0[i]) + R(b32) * R(k2[i])));
+    wide_rhs<Prob, R>(V, t + R(a3) * h, yt, k3);
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        yt[i] = val(R(y[i]) + h * (R(b41) * R(f0[i]) + R(b42) * R(k2[i]) + R(b43) * R(k3[i])));
+    wide_rhs<Prob, R>(V, t + R(a4) * h, yt, k4);
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        yt[i] = val(R(y[i]) + h * (R(b51) * R(f0[i]) + R(b52) * R(k2[i]) + R(b53) * R(k3[i]) +
+                                   R(b54) * R(k4[i])));
+    wide_rhs<Prob, R>(V, t + R(a5) * h, yt, k5);
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        yt[i] = val(R(y[i]) + h * (R(b61) * R(f0[i]) + R(b62) * R(k2[i]) + R(b63) * R(k3[i]) +
+                                   R(b64) * R(k4[i]) + R(b65) * R(k5[i])));
+    wide_rhs<Prob, R>(V, t + R(a6) * h, yt, k6);
+}
+
+// yNext (rkck.cpp:74) over y in place
+template <class R>
+__device__ __forceinline__ void rkck_wide_update(const WideVecs& V, R h, double* y,
+                                                 const double* f0) {
+    using namespace ck;
+    for (int i = threadIdx.x; i < V.n; i += blockDim.x)
+        y[i] = val(R(y[i]) + h * (R(c1) * R(f0[i]) + R(c3) * R(V.b[i]) + R(c4) * R(V.c[i]) +
+                                  R(c6) * R(V.e[i])));
+}
+
 // rkck::driver (rkck.cpp:115-159) over the block. Vectors: y, f0, and
 // k2..k6 in a..e, the stage argument in f.
 template <class Prob, class R>
@@ -132,8 +169,7 @@ __device__ void rkck_wide_system(const WideVecs& V, double t_in, double tEnd_in,
                                  const DevTol& tol, DevStats& st) {
     using namespace ck;
     const int n = V.n;
-    double *y = V.y, *f0 = V.f0, *k2 = V.a, *k3 = V.b, *k4 = V.c, *k5 = V.d, *k6 = V.e,
-           *yt = V.f;
+    double *y = V.y, *f0 = V.f0, *k3 = V.b, *k4 = V.c, *k5 = V.d, *k6 = V.e;
     stats_init(st);
     const R tEnd(tEnd_in);
     R t(t_in);
@@ -153,24 +189,7 @@ __device__ void rkck_wide_system(const WideVecs& V, double t_in, double tEnd_in,
             ++st.rhs_evals;
             haveF = true;
         }
-        // rkck::step (rkck.cpp:42-64)
-        for (int i = threadIdx.x; i < n; i += blockDim.x)
-            yt[i] = val(R(y[i]) + h * R(b21) * R(f0[i]));
-        wide_rhs<Prob, R>(V, t + R(a2) * h, yt, k2);
-        for (int i = threadIdx.x; i < n; i += blockDim.x)
-            yt[i] = val(R(y[i]) + h * (R(b31) * R(f0[i]) + R(b32) * R(k2[i])));
-        wide_rhs<Prob, R>(V, t + R(a3) * h, yt, k3);
-        for (int i = threadIdx.x; i < n; i += blockDim.x)
-            yt[i] = val(R(y[i]) + h * (R(b41) * R(f0[i]) + R(b42) * R(k2[i]) + R(b43) * R(k3[i])));
-        wide_rhs<Prob, R>(V, t + R(a4) * h, yt, k4);
-        for (int i = threadIdx.x; i < n; i += blockDim.x)
-            yt[i] = val(R(y[i]) + h * (R(b51) * R(f0[i]) + R(b52) * R(k2[i]) + R(b53) * R(k3[i]) +
-                                       R(b54) * R(k4[i])));
-        wide_rhs<Prob, R>(V, t + R(a5) * h, yt, k5);
-        for (int i = threadIdx.x; i < n; i += blockDim.x)
-            yt[i] = val(R(y[i]) + h * (R(b61) * R(f0[i]) + R(b62) * R(k2[i]) + R(b63) * R(k3[i]) +
-                                       R(b64) * R(k4[i]) + R(b65) * R(k5[i])));
-        wide_rhs<Prob, R>(V, t + R(a6) * h, yt, k6);
+        rkck_wide_stages<Prob, R>(V, t, h, y, f0);  // rkck::step (rkck.cpp:42-64)
         st.rhs_evals += 5;
         st.stages_total += 6;
         // yErr (rkck.cpp:75-76) folded into errorNorm (rkck.cpp:88-98); the
@@ -191,9 +210,7 @@ __device__ void rkck_wide_system(const WideVecs& V, double t_in, double tEnd_in,
         if (accepted) {
             t += h;
             stats_accept(st, val(h));
-            for (int i = threadIdx.x; i < n; i += blockDim.x)  // yNext (rkck.cpp:74)
-                y[i] = val(R(y[i]) + h * (R(c1) * R(f0[i]) + R(c3) * R(k3[i]) + R(c4) * R(k4[i]) +
-                                          R(c6) * R(k6[i])));
+            rkck_wide_update<R>(V, h, y, f0);  // yNext (rkck.cpp:74)
             haveF = false;
             h = hNew;
         } else {
@@ -267,6 +284,61 @@ __device__ int power_method_wide(const WideVecs& V, R t, const double* y, const 
     return iters;
 }
 
+// rkc::step (rkc.cpp:82-117) over the block: the s-stage recurrence from y and
+// f0 with the stage pair in wA/wB and the stage RHS in fs; returns the vector
+// holding y_trial. Coefficients (rkc.cpp:29-69) from the device table for
+// s <= kRkcTableMaxS (tab non-null), else the generator.
+template <class Prob, class R>
+__device__ double* rkc_wide_stages(const WideVecs& V, R t, R h, long long s, R kappa,
+                                   const double* tab, const double* y, const double* f0,
+                                   double* wA, double* wB, double* fs) {
+    const int n = V.n;
+    const double* crow = (tab != nullptr && s <= kRkcTableMaxS) ? tab + rkc_table_row(s) : nullptr;
+    RkcCoefGen<R> gen;
+    R mu1;
+    if (crow != nullptr) {
+        mu1 = R(crow[0]);
+    } else {
+        gen.init(s, kappa);
+        mu1 = gen.mu1;
+    }
+    double *wjm1 = wA, *wjm2 = wB;
+    {
+        const R mu1h = mu1 * h;
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            wjm1[i] = val(R(y[i]) + mu1h * R(f0[i]));
+    }
+#pragma unroll 1
+    for (long long j = 2; j <= s; ++j) {
+        R muj, nuj, muTj, gTj, cjm1;
+        if (crow != nullptr) {
+            const double* e = crow + 1 + 5 * (j - 2);
+            muj = R(e[0]);
+            nuj = R(e[1]);
+            muTj = R(e[2]);
+            gTj = R(e[3]);
+            cjm1 = R(e[4]);
+        } else {
+            gen.next(j, muj, nuj, muTj, gTj, cjm1);
+        }
+        wide_rhs<Prob, R>(V, t + cjm1 * h, wjm1, fs);
+        const R mujh = muTj * h, gjh = gTj * h;
+        if (j == 2) {
+            for (int i = threadIdx.x; i < n; i += blockDim.x)
+                wjm2[i] = val(R(y[i]) + muj * (R(wjm1[i]) - R(y[i])) + mujh * R(fs[i]) +
+                              gjh * R(f0[i]));
+        } else {
+            for (int i = threadIdx.x; i < n; i += blockDim.x)
+                wjm2[i] = val(R(y[i]) + muj * (R(wjm1[i]) - R(y[i])) +
+                              nuj * (R(wjm2[i]) - R(y[i])) + mujh * R(fs[i]) + gjh * R(f0[i]));
+        }
+        double* sw = wjm1;
+        wjm1 = wjm2;
+        wjm2 = sw;
+    }
+    return wjm1;
+}
+
 // rkc::driver (rkc.cpp:193-281) over the block. Vectors: y, f0, the
 // eigenvector in a, the stage pair w_{j-1}/w_{j-2} in b/c, the stage RHS in
 // d, the trial RHS in e, sum terms in f. The power method borrows b (v) and
@@ -330,53 +402,8 @@ __device__ void rkc_wide_system(const WideVecs& V, double t_in, double tEnd_in,
         }
         const long long s = rkc_stage_count(wsSpecRad, mMax, wsH);  // sigma non-finite -> 0
         const R h = wsH;
-        // rkc::step (rkc.cpp:82-117), coefficients (rkc.cpp:29-69) from the
-        // device table for s <= kRkcTableMaxS, else the generator
-        const double* crow =
-            (tol.rkc_coef != nullptr && s <= kRkcTableMaxS) ? tol.rkc_coef + rkc_table_row(s) : nullptr;
-        RkcCoefGen<R> gen;
-        R mu1;
-        if (crow != nullptr) {
-            mu1 = R(crow[0]);
-        } else {
-            gen.init(s, kappa);
-            mu1 = gen.mu1;
-        }
-        double *wjm1 = wA, *wjm2 = wB;
-        {
-            const R mu1h = mu1 * h;
-            for (int i = threadIdx.x; i < n; i += blockDim.x)
-                wjm1[i] = val(R(y[i]) + mu1h * R(f0[i]));
-        }
-#pragma unroll 1
-        for (long long j = 2; j <= s; ++j) {
-            R muj, nuj, muTj, gTj, cjm1;
-            if (crow != nullptr) {
-                const double* e = crow + 1 + 5 * (j - 2);
-                muj = R(e[0]);
-                nuj = R(e[1]);
-                muTj = R(e[2]);
-                gTj = R(e[3]);
-                cjm1 = R(e[4]);
-            } else {
-                gen.next(j, muj, nuj, muTj, gTj, cjm1);
-            }
-            wide_rhs<Prob, R>(V, t + cjm1 * h, wjm1, fs);
-            const R mujh = muTj * h, gjh = gTj * h;
-            if (j == 2) {
-                for (int i = threadIdx.x; i < n; i += blockDim.x)
-                    wjm2[i] = val(R(y[i]) + muj * (R(wjm1[i]) - R(y[i])) + mujh * R(fs[i]) +
-                                  gjh * R(f0[i]));
-            } else {
-                for (int i = threadIdx.x; i < n; i += blockDim.x)
-                    wjm2[i] = val(R(y[i]) + muj * (R(wjm1[i]) - R(y[i])) +
-                                  nuj * (R(wjm2[i]) - R(y[i])) + mujh * R(fs[i]) + gjh * R(f0[i]));
-            }
-            double* sw = wjm1;
-            wjm1 = wjm2;
-            wjm2 = sw;
-        }
-        double* yTrial = wjm1;
+        // rkc::step (rkc.cpp:82-117)
+        double* yTrial = rkc_wide_stages<Prob, R>(V, t, h, s, kappa, tol.rkc_coef, y, f0, wA, wB, fs);
         st.rhs_evals += s - 1;
         st.stages_total += s;
         wide_rhs<Prob, R>(V, t + h, yTrial, ft);  // rkc.cpp:247
@@ -456,6 +483,53 @@ __global__ void __launch_bounds__(kWideMaxBlock)
             }
         }
         __syncthreads();  // the vectors are reused by the next system
+    }
+}
+
+// rkck::integrateFixed (rkck.cpp:168-181) / rkc::integrateFixed (rkc.cpp:290-306)
+// for one system per block: numSteps steps of (tEnd - t0) / numSteps, no
+// controller. Vectors in shared memory, or in this block's slice of scratch.
+template <class Prob, class R, int SOLVER>
+__global__ void __launch_bounds__(kWideMaxBlock)
+    wide_fixed_kernel(const double* __restrict__ g_soa, double* __restrict__ y_soa, long long num,
+                      double t0, double tEnd, long long numSteps, long long stages, double kappa,
+                      int n, double* scratch) {
+    extern __shared__ double bode_smem[];
+    __shared__ double red[33];
+    double* base = scratch != nullptr ? scratch + (long long)blockIdx.x * kWideVecs * n : bode_smem;
+    WideVecs V;
+    V.y = base;
+    V.f0 = base + (long long)n;
+    V.a = base + 2LL * n;
+    V.b = base + 3LL * n;
+    V.c = base + 4LL * n;
+    V.d = base + 5LL * n;
+    V.e = base + 6LL * n;
+    V.f = base + 7LL * n;
+    V.n = n;
+    V.inv = Prob::inv_dx2(n);
+    V.red = red;
+    (void)g_soa;
+    const R h = (R(tEnd) - R(t0)) / R(double(numSteps));  // rkck.cpp:174, rkc.cpp:298
+#pragma unroll 1
+    for (long long sys = blockIdx.x; sys < num; sys += gridDim.x) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) V.y[i] = y_soa[sys + num * (long long)i];
+#pragma unroll 1
+        for (long long k = 0; k < numSteps; ++k) {
+            const R t = R(t0) + R(double(k)) * h;  // rkck.cpp:176, rkc.cpp:301
+            wide_rhs<Prob, R>(V, t, V.y, V.f0);
+            if constexpr (SOLVER == 0) {
+                rkck_wide_stages<Prob, R>(V, t, h, V.y, V.f0);
+                rkck_wide_update<R>(V, h, V.y, V.f0);
+            } else {
+                const double* yt = rkc_wide_stages<Prob, R>(V, t, h, stages, R(kappa), nullptr, V.y,
+                                                            V.f0, V.b, V.c, V.d);
+                for (int i = threadIdx.x; i < n; i += blockDim.x) V.y[i] = yt[i];
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x) y_soa[sys + num * (long long)i] = V.y[i];
+        __syncthreads();
     }
 }
 

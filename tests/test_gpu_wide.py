@@ -108,3 +108,20 @@ def test_heat_dim_1e6_smoke(gpu, oracle):
     rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKC, 0.0, t1, t1, y0)
     assert st["steps_accepted"][0] >= 5 and st["stages_total"][0] > 400
     _bitwise(y, st, yo, so)
+
+
+@pytest.mark.parametrize("n,solver,t1,steps", [(5, "rkck", 0.05, 40), (100, "rkck", 1e-4, 20),
+                                               (5, "rkc", 0.05, 10), (100, "rkc", 1e-3, 10),
+                                               (4000, "rkc", 1e-7, 3)])
+def test_heat_any_n_fixed_step_bitwise(gpu, oracle, n, solver, t1, steps):
+    """integrateFixed (rkck.cpp:168-181, rkc.cpp:290-306) on the block kernels,
+    including the global-scratch path (n = 4000)."""
+    from test_gpu_fixed import oracle_fixed
+    num = 12
+    prob = A.make_problem(A.HEAT, n)
+    y0 = perturb(heat_ic(n), 0.01, 5, num)
+    batch = B.BatchStates(num, n, 0, y0.copy(), np.zeros(0))
+    out = B.integrate_fixed(B.OdeProblem(prob.kind, n, 0), batch, 0.0, t1, steps, solver=solver,
+                            stages=9)
+    ref = oracle_fixed(oracle, prob, solver, y0, None, num, 0.0, t1, steps, stages=9)
+    assert np.array_equal(out.values.view(np.uint64), ref.view(np.uint64))
