@@ -31,7 +31,11 @@
 
 namespace {
 
+using bode::CompactStats;
 using bode::DevStats;
+using bode::kCompactBudget;
+using bode::kCompactSaturated;
+using bode::kCompactUnderflow;
 using bode::DevTol;
 using bode::KernelEntry;
 
@@ -402,6 +406,10 @@ int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double*
 #define BODE_MAX_CHUNKS 32
 #endif
 constexpr int kMaxChunks = BODE_MAX_CHUNKS;  // host-pointer pipeline depth per shard
+#ifndef BODE_COMPACT_STATS_D2H
+#define BODE_COMPACT_STATS_D2H 1
+#endif
+constexpr bool kCompactStatsD2H = BODE_COMPACT_STATS_D2H;  // 40-byte stats over PCIe (see below)
 
 // Device buffers, streams and events of one shard, leased exclusively for one
 // call: concurrent or nested calls (from another host thread, or from a sink)
@@ -417,6 +425,9 @@ struct Lease {
     size_t y_cap = 0, g_cap = 0, st_cap = 0, ord_cap = 0, ysnap_cap[2] = {0, 0};
     cudaStream_t streams[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
     cudaEvent_t events[2 * kMaxChunks] = {};                 // per chunk: H2D done, kernel done
+    cudaEvent_t out_done[kMaxChunks] = {};                   // per chunk: D2H done
+    CompactStats* cst = nullptr;  // host-pointer pipeline: stats in the 40-byte transfer format
+    size_t cst_cap = 0;
     cudaEvent_t snap_ready[2] = {};   // snapshot slot staged in ysnap (compute stream)
     cudaEvent_t snap_copied[2] = {};  // snapshot slot's D2H finished (D2H stream)
 };
@@ -438,6 +449,8 @@ class LeasePool {
         for (auto& s : L->streams)
             BODE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         for (auto& ev : L->events) BODE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        for (auto& ev : L->out_done)
+            BODE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         for (int i = 0; i < 2; ++i) {
             BODE_CUDA(cudaEventCreateWithFlags(&L->snap_ready[i], cudaEventDisableTiming));
             BODE_CUDA(cudaEventCreateWithFlags(&L->snap_copied[i], cudaEventDisableTiming));
@@ -588,6 +601,37 @@ int check_devices(int gpus) {
     return BODE_OK;
 }
 
+// Expands one chunk's 40-byte stats records, which the D2H copy placed at the
+// end of the chunk's region of the caller's bode_stats_t array, into that
+// region in place. Front to back is safe: record i's 64 bytes end before
+// compact record i + 1 begins (24 nk >= 24 (i + 1)); record i itself is read
+// before it is overwritten. A saturated record (a count above 2^32 - 1) is
+// fetched whole from the device copy, which outlives the call's pipeline.
+int expand_stats_chunk(bode_stats_t* out, int64_t nk, const DevStats* dev_st, int device) {
+    const char* base = reinterpret_cast<const char*>(out) + 24 * nk;
+    for (int64_t i = 0; i < nk; ++i) {
+        CompactStats c;
+        std::memcpy(&c, base + 40 * i, sizeof(c));
+        if (c.flags & kCompactSaturated) {
+            BODE_CUDA(cudaSetDevice(device));
+            BODE_CUDA(cudaMemcpy(&out[i], dev_st + i, sizeof(DevStats), cudaMemcpyDeviceToHost));
+            continue;
+        }
+        bode_stats_t r;
+        r.steps_accepted = c.steps_accepted;
+        r.steps_rejected = c.steps_rejected;
+        r.rhs_evals = c.rhs_evals;
+        r.spec_rad_evals = c.spec_rad_evals;
+        r.stages_total = c.stages_total;
+        r.h_min_seen = c.h_min_seen;
+        r.h_max_seen = c.h_max_seen;
+        r.underflow = (c.flags & kCompactUnderflow) ? 1 : 0;
+        r.budget_exhausted = (c.flags & kCompactBudget) ? 1 : 0;
+        std::memcpy(&out[i], &r, sizeof(r));
+    }
+    return BODE_OK;
+}
+
 // One shard of a host-pointer window, pipelined in chunks over three streams
 // with one role each: H2D copies back to back on streams[0], the kernels on
 // streams[1] (chunk k waits for its H2D), D2H copies on streams[2] (chunk k
@@ -612,6 +656,13 @@ int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard&
     const int nchunks =
         pinned ? (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, sh.count / min_chunk)) : 1;
     const int64_t cbase = sh.count / nchunks, crem = sh.count % nchunks;
+    // With a pinned stats array the stats cross PCIe in the 40-byte format and
+    // host threads expand each chunk as its copy lands (D2H is the direction
+    // that bounds this path: 264 instead of 288 bytes per system).
+    const bool compact = kCompactStatsD2H && stats != nullptr && pinned && nchunks > 1 &&
+                         host_pinned(stats);
+    if (compact && (rc = ensure(&B.cst, &B.cst_cap, (size_t)sh.count))) return rc;
+    std::vector<int64_t> chunk_off(nchunks), chunk_len(nchunks);
     cudaStream_t sh2d = B.streams[0], sk = B.streams[1], sd2h = B.streams[2];
     int64_t off = 0;
     for (int k = 0; k < nchunks; ++k) {
@@ -630,14 +681,44 @@ int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard&
         BODE_CUDA(cudaStreamWaitEvent(sk, in_done, 0));
         rc = launch_window(e, sk, dg, dy, dst, nk, t, tEnd, tol, 0);
         if (rc) return rc;
+        if (compact && (rc = bode::pack_stats(dst, B.cst + off, nk, sk))) return fail(rc, "pack_stats");
         BODE_CUDA(cudaEventRecord(k_done, sk));
         BODE_CUDA(cudaStreamWaitEvent(sd2h, k_done, 0));
         BODE_CUDA(cudaMemcpy2DAsync(y + src, num * sizeof(double), dy, nk * sizeof(double),
                                     nk * sizeof(double), N, cudaMemcpyDeviceToHost, sd2h));
-        if (stats)
+        if (compact) {
+            char* land = reinterpret_cast<char*>(stats + src) + 24 * nk;
+            BODE_CUDA(cudaMemcpyAsync(land, B.cst + off, nk * sizeof(CompactStats),
+                                      cudaMemcpyDeviceToHost, sd2h));
+            BODE_CUDA(cudaEventRecord(B.out_done[k], sd2h));
+        } else if (stats) {
             BODE_CUDA(cudaMemcpyAsync(stats + src, dst, nk * sizeof(DevStats),
                                       cudaMemcpyDeviceToHost, sd2h));
+        }
+        chunk_off[k] = off;
+        chunk_len[k] = nk;
         off += nk;
+    }
+    if (compact) {
+        // expanders: thread t takes chunks t, t + T, ... as their copies land
+        const int T = std::min(nchunks, 8);
+        std::atomic<int> err{BODE_OK};
+        std::vector<std::thread> ts;
+        for (int t = 0; t < T; ++t)
+            ts.emplace_back([&, t]() {
+                cudaSetDevice(sh.device);
+                for (int k = t; k < nchunks; k += T) {
+                    if (cudaEventSynchronize(B.out_done[k]) != cudaSuccess) {
+                        err.store(BODE_E_CUDA);
+                        return;
+                    }
+                    const int r = expand_stats_chunk(stats + sh.begin + chunk_off[k], chunk_len[k],
+                                                     B.st + chunk_off[k], sh.device);
+                    if (r) err.store(r);
+                }
+            });
+        for (auto& th : ts) th.join();
+        if (err.load()) return fail(err.load(), "stats expansion failed");
     }
     for (auto& s : B.streams) BODE_CUDA(cudaStreamSynchronize(s));
     return BODE_OK;

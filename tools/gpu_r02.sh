@@ -92,7 +92,7 @@ for p in $PARTS; do
       python tools/ncu_summary.py $OUT/ncu $SPECS > $OUT/ncu_summary.txt 2>&1
       echo "ncu_summary rc=$?" >> $OUT/status.txt
       ls -la $NCUP > $OUT/ncu_reports_ls.txt ;;
-    newtests) timeout 1200 python -m pytest tests -x -q -m gpu -k "wide or budget" > $OUT/pytest_new.txt 2>&1; echo "newtests rc=$?" >> $OUT/status.txt ;;
+    newtests) timeout 1200 python -m pytest tests -x -q -m gpu -k "wide or budget or fixed" > $OUT/pytest_new.txt 2>&1; echo "newtests rc=$?" >> $OUT/status.txt ;;
   esac
 done
 for p in $PARTS; do
@@ -129,5 +129,15 @@ for p in $PARTS; do
         if [ $V = new ]; then LP=; else LP=$PWD/paper_1611_02274_b200/lib/ab/$V/libbode.so; fi
         BODE_LIB_PATH=$LP timeout 900 python bench.py --steps 10 --warmup 3 --no-secondary --no-cpu > $OUT/ab_chunks_${I}_$V.txt 2>&1; done
       echo "ab_chunks rc=$?" >> $OUT/status.txt ;;
+  esac
+done
+for p in $PARTS; do
+  case $p in
+    ab_stats)  # 40-byte stats over PCIe (new) vs 64-byte records (lib/ab/fullstats): e2e
+      I=0; for V in fullstats new fullstats new fullstats new; do I=$((I+1))
+        if [ $V = new ]; then LP=; else LP=$PWD/paper_1611_02274_b200/lib/ab/$V/libbode.so; fi
+        BODE_LIB_PATH=$LP timeout 900 python bench.py --steps 10 --warmup 3 --no-secondary --no-cpu > $OUT/ab_stats_${I}_$V.txt 2>&1; done
+      echo "ab_stats rc=$?" >> $OUT/status.txt ;;
+    tcompact) timeout 1200 python -m pytest tests -x -q -m gpu -k "compact or shards or budget" > $OUT/pytest_compact.txt 2>&1; echo "tcompact rc=$?" >> $OUT/status.txt ;;
   esac
 done
