@@ -681,7 +681,10 @@ int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard&
         BODE_CUDA(cudaStreamWaitEvent(sk, in_done, 0));
         rc = launch_window(e, sk, dg, dy, dst, nk, t, tEnd, tol, 0);
         if (rc) return rc;
-        if (compact && (rc = bode::pack_stats(dst, B.cst + off, nk, sk))) return fail(rc, "pack_stats");
+        if (compact) {
+            if ((rc = bode::pack_stats(dst, B.cst + off, nk, sk))) return fail(rc, "pack_stats");
+            g_launches.fetch_add(1);
+        }
         BODE_CUDA(cudaEventRecord(k_done, sk));
         BODE_CUDA(cudaStreamWaitEvent(sd2h, k_done, 0));
         BODE_CUDA(cudaMemcpy2DAsync(y + src, num * sizeof(double), dy, nk * sizeof(double),

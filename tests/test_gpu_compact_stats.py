@@ -48,12 +48,18 @@ def run(case, num, pinned, budget=0):
 @pytest.mark.parametrize("case,budget", [("pleiades", 0), ("heat64", 0), ("pleiades", 30)])
 def test_compact_stats_equal_full_records(gpu, case, budget):
     num = 300_001  # 4 pipeline chunks, a ragged last one
+    L = B.lib()
+    n0 = L.bode_launch_count()
     yp, sp = run(case, num, True, budget)
+    n1 = L.bode_launch_count()
     yf, sf = run(case, num, False, budget)
+    n2 = L.bode_launch_count()
+    # pinned: 4 chunk kernels + 4 stats packs; pageable: one launch, 64-byte records
+    assert n1 - n0 == 8 and n2 - n1 == 1, (n1 - n0, n2 - n1)
     assert np.array_equal(yp.view(np.uint64), yf.view(np.uint64))
     for k in ALL:
-        assert np.array_equal(sp[k].view(np.uint64) if sp[k].dtype == np.float64 else sp[k],
-                              sf[k].view(np.uint64) if sf[k].dtype == np.float64 else sf[k]), k
+        assert np.array_equal(np.ascontiguousarray(sp[k]).view(np.uint8),
+                              np.ascontiguousarray(sf[k]).view(np.uint8)), k
     if budget:
         assert sp["budget_exhausted"].any()
 
@@ -79,5 +85,6 @@ def test_compact_stats_saturated_records_fetched_whole(gpu):
     assert (sf["rhs_evals"] > 20).mean() > 0.9  # the fallback path really ran
     assert np.array_equal(yp.view(np.uint64), yf.view(np.uint64))
     for k in ALL:
-        assert np.array_equal(np.asarray(sp[k]).view(np.uint8), np.asarray(sf[k]).view(np.uint8)), k
+        assert np.array_equal(np.ascontiguousarray(sp[k]).view(np.uint8),
+                              np.ascontiguousarray(sf[k]).view(np.uint8)), k
     assert att.min() >= 1

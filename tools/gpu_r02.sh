@@ -141,3 +141,8 @@ for p in $PARTS; do
     tcompact) timeout 1200 python -m pytest tests -x -q -m gpu -k "compact or shards or budget" > $OUT/pytest_compact.txt 2>&1; echo "tcompact rc=$?" >> $OUT/status.txt ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    pcie) timeout 600 python tools/pcie.py --num 16777216 --stats-sweep > $OUT/pcie_sweep.json 2>&1; echo "pcie rc=$?" >> $OUT/status.txt ;;
+  esac
+done

@@ -15,6 +15,7 @@ import torch
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--num", type=int, default=1 << 22)
+    ap.add_argument("--stats-sweep", action="store_true")
     args = ap.parse_args()
     nin, nout = args.num * 28 * 8, args.num * (28 * 8 + 64)
     import os
@@ -22,6 +23,16 @@ def main():
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from bench import gpu_local_memory
     res = {}
+    if args.stats_sweep:  # marginal cost of the per-system stats bytes on the D2H side
+        with gpu_local_memory(torch, 0):
+            hi = torch.zeros(nin, dtype=torch.uint8).pin_memory()
+            for sb in (0, 40, 64):
+                no = args.num * (28 * 8 + sb)
+                ho = torch.zeros(no, dtype=torch.uint8).pin_memory()
+                res[f"stats_{sb}B"] = measure(torch, hi, ho, nin, no)
+                del ho
+        print(json.dumps(res))
+        return
     for placement in ("default", "gpu_local"):
         if placement == "gpu_local":
             with gpu_local_memory(torch, 0) as g:
