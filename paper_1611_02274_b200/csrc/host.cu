@@ -425,9 +425,11 @@ struct Lease {
     size_t y_cap = 0, g_cap = 0, st_cap = 0, ord_cap = 0, ysnap_cap[2] = {0, 0};
     cudaStream_t streams[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
     cudaEvent_t events[2 * kMaxChunks] = {};                 // per chunk: H2D done, kernel done
-    cudaEvent_t out_done[kMaxChunks] = {};                   // per chunk: D2H done
+    cudaEvent_t out_done[kMaxChunks] = {};                   // per chunk: stats D2H done
     CompactStats* cst = nullptr;  // host-pointer pipeline: stats in the 40-byte transfer format
     size_t cst_cap = 0;
+    CompactStats* hst = nullptr;  // ... and their pinned host landing buffer
+    size_t hst_cap = 0;
     cudaEvent_t snap_ready[2] = {};   // snapshot slot staged in ysnap (compute stream)
     cudaEvent_t snap_copied[2] = {};  // snapshot slot's D2H finished (D2H stream)
 };
@@ -540,6 +542,18 @@ int ensure(T** p, size_t* cap, size_t count) {
     return BODE_OK;
 }
 
+// Pinned host buffer of at least `count` elements (kept with the lease).
+template <class T>
+int ensure_pinned(T** p, size_t* cap, size_t count) {
+    if (count <= *cap) return BODE_OK;
+    if (*p) cudaFreeHost(*p);
+    *p = nullptr;
+    *cap = 0;
+    BODE_CUDA(cudaHostAlloc((void**)p, std::max<size_t>(count, 1) * sizeof(T), cudaHostAllocDefault));
+    *cap = count;
+    return BODE_OK;
+}
+
 bool host_pinned(const void* ptr) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
@@ -601,17 +615,13 @@ int check_devices(int gpus) {
     return BODE_OK;
 }
 
-// Expands one chunk's 40-byte stats records, which the D2H copy placed at the
-// end of the chunk's region of the caller's bode_stats_t array, into that
-// region in place. Front to back is safe: record i's 64 bytes end before
-// compact record i + 1 begins (24 nk >= 24 (i + 1)); record i itself is read
-// before it is overwritten. A saturated record (a count above 2^32 - 1) is
+// Expands 40-byte stats records (landed in the lease's pinned buffer) into the
+// caller's bode_stats_t array. A saturated record (a count above 2^32 - 1) is
 // fetched whole from the device copy, which outlives the call's pipeline.
-int expand_stats_chunk(bode_stats_t* out, int64_t nk, const DevStats* dev_st, int device) {
-    const char* base = reinterpret_cast<const char*>(out) + 24 * nk;
+int expand_stats(bode_stats_t* out, const CompactStats* in, int64_t nk, const DevStats* dev_st,
+                 int device) {
     for (int64_t i = 0; i < nk; ++i) {
-        CompactStats c;
-        std::memcpy(&c, base + 40 * i, sizeof(c));
+        const CompactStats c = in[i];
         if (c.flags & kCompactSaturated) {
             BODE_CUDA(cudaSetDevice(device));
             BODE_CUDA(cudaMemcpy(&out[i], dev_st + i, sizeof(DevStats), cudaMemcpyDeviceToHost));
@@ -627,7 +637,7 @@ int expand_stats_chunk(bode_stats_t* out, int64_t nk, const DevStats* dev_st, in
         r.h_max_seen = c.h_max_seen;
         r.underflow = (c.flags & kCompactUnderflow) ? 1 : 0;
         r.budget_exhausted = (c.flags & kCompactBudget) ? 1 : 0;
-        std::memcpy(&out[i], &r, sizeof(r));
+        out[i] = r;
     }
     return BODE_OK;
 }
@@ -661,7 +671,9 @@ int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard&
     // that bounds this path: 264 instead of 288 bytes per system).
     const bool compact = kCompactStatsD2H && stats != nullptr && pinned && nchunks > 1 &&
                          host_pinned(stats);
-    if (compact && (rc = ensure(&B.cst, &B.cst_cap, (size_t)sh.count))) return rc;
+    if (compact && ((rc = ensure(&B.cst, &B.cst_cap, (size_t)sh.count)) ||
+                    (rc = ensure_pinned(&B.hst, &B.hst_cap, (size_t)sh.count))))
+        return rc;
     std::vector<int64_t> chunk_off(nchunks), chunk_len(nchunks);
     cudaStream_t sh2d = B.streams[0], sk = B.streams[1], sd2h = B.streams[2];
     int64_t off = 0;
@@ -690,8 +702,7 @@ int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard&
         BODE_CUDA(cudaMemcpy2DAsync(y + src, num * sizeof(double), dy, nk * sizeof(double),
                                     nk * sizeof(double), N, cudaMemcpyDeviceToHost, sd2h));
         if (compact) {
-            char* land = reinterpret_cast<char*>(stats + src) + 24 * nk;
-            BODE_CUDA(cudaMemcpyAsync(land, B.cst + off, nk * sizeof(CompactStats),
+            BODE_CUDA(cudaMemcpyAsync(B.hst + off, B.cst + off, nk * sizeof(CompactStats),
                                       cudaMemcpyDeviceToHost, sd2h));
             BODE_CUDA(cudaEventRecord(B.out_done[k], sd2h));
         } else if (stats) {
@@ -703,20 +714,24 @@ int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard&
         off += nk;
     }
     if (compact) {
-        // expanders: thread t takes chunks t, t + T, ... as their copies land
-        const int T = std::min(nchunks, 8);
+        // expanders: every thread takes its slice of each chunk as the chunk's
+        // copy lands, so the expansion keeps pace with the copies and the
+        // last chunk adds only a slice to the tail
+        const int T = 8;
         std::atomic<int> err{BODE_OK};
         std::vector<std::thread> ts;
         for (int t = 0; t < T; ++t)
             ts.emplace_back([&, t]() {
                 cudaSetDevice(sh.device);
-                for (int k = t; k < nchunks; k += T) {
+                for (int k = 0; k < nchunks; ++k) {
                     if (cudaEventSynchronize(B.out_done[k]) != cudaSuccess) {
                         err.store(BODE_E_CUDA);
                         return;
                     }
-                    const int r = expand_stats_chunk(stats + sh.begin + chunk_off[k], chunk_len[k],
-                                                     B.st + chunk_off[k], sh.device);
+                    const int64_t n = chunk_len[k], b = n * t / T, e2 = n * (t + 1) / T;
+                    const int64_t o = chunk_off[k] + b;
+                    const int r = expand_stats(stats + sh.begin + o, B.hst + o, e2 - b, B.st + o,
+                                               sh.device);
                     if (r) err.store(r);
                 }
             });
