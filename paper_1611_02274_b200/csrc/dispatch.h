@@ -27,18 +27,6 @@ struct DevStats {  // bode_stats_t, per system (AoS, 64 bytes)
 };
 static_assert(sizeof(DevStats) == 64, "DevStats must match bode_stats_t");
 
-// 40-byte transfer format of DevStats for the host-pointer pipeline (the D2H
-// direction bounds bode_int_driver end to end): 32-bit counts, the two step
-// sizes, flags. A count that does not fit sets kCompactSaturated and the host
-// fetches that system's full record instead.
-struct CompactStats {
-    double h_min_seen, h_max_seen;
-    unsigned steps_accepted, steps_rejected, rhs_evals, spec_rad_evals, stages_total, flags;
-};
-static_assert(sizeof(CompactStats) == 40, "CompactStats is the 40-byte transfer format");
-constexpr unsigned kCompactUnderflow = 1u, kCompactBudget = 2u, kCompactSaturated = 0x80000000u;
-int pack_stats(const DevStats* st, CompactStats* out, long long num, cudaStream_t s);
-
 template <class P, int L>
 constexpr int C_of() { return P::N / L; }
 

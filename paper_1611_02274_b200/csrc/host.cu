@@ -31,11 +31,7 @@
 
 namespace {
 
-using bode::CompactStats;
 using bode::DevStats;
-using bode::kCompactBudget;
-using bode::kCompactSaturated;
-using bode::kCompactUnderflow;
 using bode::DevTol;
 using bode::KernelEntry;
 
@@ -406,10 +402,6 @@ int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double*
 #define BODE_MAX_CHUNKS 32
 #endif
 constexpr int kMaxChunks = BODE_MAX_CHUNKS;  // host-pointer pipeline depth per shard
-#ifndef BODE_COMPACT_STATS_D2H
-#define BODE_COMPACT_STATS_D2H 1
-#endif
-constexpr bool kCompactStatsD2H = BODE_COMPACT_STATS_D2H;  // 40-byte stats over PCIe (see below)
 
 // Device buffers, streams and events of one shard, leased exclusively for one
 // call: concurrent or nested calls (from another host thread, or from a sink)
@@ -425,11 +417,6 @@ struct Lease {
     size_t y_cap = 0, g_cap = 0, st_cap = 0, ord_cap = 0, ysnap_cap[2] = {0, 0};
     cudaStream_t streams[3] = {nullptr, nullptr, nullptr};  // H2D, compute, D2H
     cudaEvent_t events[2 * kMaxChunks] = {};                 // per chunk: H2D done, kernel done
-    cudaEvent_t out_done[kMaxChunks] = {};                   // per chunk: stats D2H done
-    CompactStats* cst = nullptr;  // host-pointer pipeline: stats in the 40-byte transfer format
-    size_t cst_cap = 0;
-    CompactStats* hst = nullptr;  // ... and their pinned host landing buffer
-    size_t hst_cap = 0;
     cudaEvent_t snap_ready[2] = {};   // snapshot slot staged in ysnap (compute stream)
     cudaEvent_t snap_copied[2] = {};  // snapshot slot's D2H finished (D2H stream)
 };
@@ -451,8 +438,6 @@ class LeasePool {
         for (auto& s : L->streams)
             BODE_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         for (auto& ev : L->events) BODE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        for (auto& ev : L->out_done)
-            BODE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         for (int i = 0; i < 2; ++i) {
             BODE_CUDA(cudaEventCreateWithFlags(&L->snap_ready[i], cudaEventDisableTiming));
             BODE_CUDA(cudaEventCreateWithFlags(&L->snap_copied[i], cudaEventDisableTiming));
@@ -542,18 +527,6 @@ int ensure(T** p, size_t* cap, size_t count) {
     return BODE_OK;
 }
 
-// Pinned host buffer of at least `count` elements (kept with the lease).
-template <class T>
-int ensure_pinned(T** p, size_t* cap, size_t count) {
-    if (count <= *cap) return BODE_OK;
-    if (*p) cudaFreeHost(*p);
-    *p = nullptr;
-    *cap = 0;
-    BODE_CUDA(cudaHostAlloc((void**)p, std::max<size_t>(count, 1) * sizeof(T), cudaHostAllocDefault));
-    *cap = count;
-    return BODE_OK;
-}
-
 bool host_pinned(const void* ptr) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
@@ -615,33 +588,6 @@ int check_devices(int gpus) {
     return BODE_OK;
 }
 
-// Expands 40-byte stats records (landed in the lease's pinned buffer) into the
-// caller's bode_stats_t array. A saturated record (a count above 2^32 - 1) is
-// fetched whole from the device copy, which outlives the call's pipeline.
-int expand_stats(bode_stats_t* out, const CompactStats* in, int64_t nk, const DevStats* dev_st,
-                 int device) {
-    for (int64_t i = 0; i < nk; ++i) {
-        const CompactStats c = in[i];
-        if (c.flags & kCompactSaturated) {
-            BODE_CUDA(cudaSetDevice(device));
-            BODE_CUDA(cudaMemcpy(&out[i], dev_st + i, sizeof(DevStats), cudaMemcpyDeviceToHost));
-            continue;
-        }
-        bode_stats_t r;
-        r.steps_accepted = c.steps_accepted;
-        r.steps_rejected = c.steps_rejected;
-        r.rhs_evals = c.rhs_evals;
-        r.spec_rad_evals = c.spec_rad_evals;
-        r.stages_total = c.stages_total;
-        r.h_min_seen = c.h_min_seen;
-        r.h_max_seen = c.h_max_seen;
-        r.underflow = (c.flags & kCompactUnderflow) ? 1 : 0;
-        r.budget_exhausted = (c.flags & kCompactBudget) ? 1 : 0;
-        out[i] = r;
-    }
-    return BODE_OK;
-}
-
 // One shard of a host-pointer window, pipelined in chunks over three streams
 // with one role each: H2D copies back to back on streams[0], the kernels on
 // streams[1] (chunk k waits for its H2D), D2H copies on streams[2] (chunk k
@@ -666,15 +612,6 @@ int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard&
     const int nchunks =
         pinned ? (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, sh.count / min_chunk)) : 1;
     const int64_t cbase = sh.count / nchunks, crem = sh.count % nchunks;
-    // With a pinned stats array the stats cross PCIe in the 40-byte format and
-    // host threads expand each chunk as its copy lands (D2H is the direction
-    // that bounds this path: 264 instead of 288 bytes per system).
-    const bool compact = kCompactStatsD2H && stats != nullptr && pinned && nchunks > 1 &&
-                         host_pinned(stats);
-    if (compact && ((rc = ensure(&B.cst, &B.cst_cap, (size_t)sh.count)) ||
-                    (rc = ensure_pinned(&B.hst, &B.hst_cap, (size_t)sh.count))))
-        return rc;
-    std::vector<int64_t> chunk_off(nchunks), chunk_len(nchunks);
     cudaStream_t sh2d = B.streams[0], sk = B.streams[1], sd2h = B.streams[2];
     int64_t off = 0;
     for (int k = 0; k < nchunks; ++k) {
@@ -693,50 +630,14 @@ int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard&
         BODE_CUDA(cudaStreamWaitEvent(sk, in_done, 0));
         rc = launch_window(e, sk, dg, dy, dst, nk, t, tEnd, tol, 0);
         if (rc) return rc;
-        if (compact) {
-            if ((rc = bode::pack_stats(dst, B.cst + off, nk, sk))) return fail(rc, "pack_stats");
-            g_launches.fetch_add(1);
-        }
         BODE_CUDA(cudaEventRecord(k_done, sk));
         BODE_CUDA(cudaStreamWaitEvent(sd2h, k_done, 0));
         BODE_CUDA(cudaMemcpy2DAsync(y + src, num * sizeof(double), dy, nk * sizeof(double),
                                     nk * sizeof(double), N, cudaMemcpyDeviceToHost, sd2h));
-        if (compact) {
-            BODE_CUDA(cudaMemcpyAsync(B.hst + off, B.cst + off, nk * sizeof(CompactStats),
-                                      cudaMemcpyDeviceToHost, sd2h));
-            BODE_CUDA(cudaEventRecord(B.out_done[k], sd2h));
-        } else if (stats) {
+        if (stats)
             BODE_CUDA(cudaMemcpyAsync(stats + src, dst, nk * sizeof(DevStats),
                                       cudaMemcpyDeviceToHost, sd2h));
-        }
-        chunk_off[k] = off;
-        chunk_len[k] = nk;
         off += nk;
-    }
-    if (compact) {
-        // expanders: every thread takes its slice of each chunk as the chunk's
-        // copy lands, so the expansion keeps pace with the copies and the
-        // last chunk adds only a slice to the tail
-        const int T = 8;
-        std::atomic<int> err{BODE_OK};
-        std::vector<std::thread> ts;
-        for (int t = 0; t < T; ++t)
-            ts.emplace_back([&, t]() {
-                cudaSetDevice(sh.device);
-                for (int k = 0; k < nchunks; ++k) {
-                    if (cudaEventSynchronize(B.out_done[k]) != cudaSuccess) {
-                        err.store(BODE_E_CUDA);
-                        return;
-                    }
-                    const int64_t n = chunk_len[k], b = n * t / T, e2 = n * (t + 1) / T;
-                    const int64_t o = chunk_off[k] + b;
-                    const int r = expand_stats(stats + sh.begin + o, B.hst + o, e2 - b, B.st + o,
-                                               sh.device);
-                    if (r) err.store(r);
-                }
-            });
-        for (auto& th : ts) th.join();
-        if (err.load()) return fail(err.load(), "stats expansion failed");
     }
     for (auto& s : B.streams) BODE_CUDA(cudaStreamSynchronize(s));
     return BODE_OK;

@@ -16,8 +16,6 @@
 // buffers keep their addresses.
 #include <cuda_runtime.h>
 
-#include <cstdlib>
-
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -334,44 +332,6 @@ int lockstep_efficiency(const DevStats* st, long long num, int group, double* ef
     RP_CUDA(cudaGetLastError());
     RP_CUDA(cudaStreamSynchronize(s));
     *eff = hsum[dev][1] ? (double)hsum[dev][0] / (double)hsum[dev][1] : 1.0;
-    return BODE_OK;
-}
-
-// DevStats -> CompactStats (dispatch.h) for the host-pointer pipeline's D2H.
-__global__ void pack_stats_kernel(const DevStats* __restrict__ st, CompactStats* __restrict__ out,
-                                  long long num, unsigned long long lim) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= num) return;
-    const DevStats a = st[i];
-    CompactStats c;
-    c.h_min_seen = a.h_min_seen;
-    c.h_max_seen = a.h_max_seen;
-    const bool sat = (unsigned long long)a.steps_accepted > lim ||
-                     (unsigned long long)a.steps_rejected > lim ||
-                     (unsigned long long)a.rhs_evals > lim ||
-                     (unsigned long long)a.spec_rad_evals > lim ||
-                     (unsigned long long)a.stages_total > lim;
-    c.steps_accepted = (unsigned)a.steps_accepted;
-    c.steps_rejected = (unsigned)a.steps_rejected;
-    c.rhs_evals = (unsigned)a.rhs_evals;
-    c.spec_rad_evals = (unsigned)a.spec_rad_evals;
-    c.stages_total = (unsigned)a.stages_total;
-    c.flags = (a.underflow ? kCompactUnderflow : 0u) | (a.budget_exhausted ? kCompactBudget : 0u) |
-              (sat ? kCompactSaturated : 0u);
-    out[i] = c;
-}
-
-int pack_stats(const DevStats* st, CompactStats* out, long long num, cudaStream_t s) {
-    if (num < 1) return BODE_OK;
-    // BODE_COMPACT_STATS_LIMIT (tests only): a lower saturation bound, so the
-    // whole-record fallback can be exercised without 2^32 attempts
-    static const unsigned long long lim = [] {
-        const char* e = std::getenv("BODE_COMPACT_STATS_LIMIT");
-        const unsigned long long v = e ? std::strtoull(e, nullptr, 10) : 0ull;
-        return (v > 0 && v < 0xffffffffull) ? v : 0xffffffffull;
-    }();
-    pack_stats_kernel<<<blocks(num, 256), 256, 0, s>>>(st, out, num, lim);
-    RP_CUDA(cudaGetLastError());
     return BODE_OK;
 }
 
