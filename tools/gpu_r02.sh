@@ -146,3 +146,8 @@ for p in $PARTS; do
     pcie) timeout 600 python tools/pcie.py --num 16777216 --stats-sweep > $OUT/pcie_sweep.json 2>&1; echo "pcie rc=$?" >> $OUT/status.txt ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    widebench) timeout 900 python tools/wide_bench.py > $OUT/wide_bench.jsonl 2> $OUT/wide_bench.err; echo "widebench rc=$?" >> $OUT/status.txt ;;
+  esac
+done
