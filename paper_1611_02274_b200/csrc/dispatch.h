@@ -81,6 +81,9 @@ struct KernelEntry {
     // in place of fn / pfn while a budget is set
     const void* bfn = nullptr;
     const void* bpfn = nullptr;
+    // run-time-dimension lane kernels (problems.cuh is_runtime_dim, dim == 0):
+    // the largest dimension they hold; chosen when no exact-dim kernel exists
+    int cap = 0;
     // one-system-per-block fixed-step harness (wide entries; ffn is its kernel)
     int (*launch_fixed_wide)(const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                              const double* g, double* y, long long num, double t0, double tEnd,

@@ -225,7 +225,28 @@ const KernelEntry* find_entry(const bode_problem_t* p, int solver, int arith) {
                 find_in(registry(), p, solver, arith, want_lanes, want_maxreg, &first))
             return e;
     }
-    return first ? first : wide();
+    if (first) return first;
+    // a run-time-dimension lane kernel that holds p->dim (the smallest such
+    // capacity), else one system per block
+    const KernelEntry* pad = nullptr;
+    for (int i = 0; i < n; ++i) {
+        const KernelEntry& e = tab[i];
+        if (e.cap >= p->dim && e.kind == p->kind && e.param_dim == p->param_dim &&
+            e.solver == solver && e.arith == arith && (!pad || e.cap < pad->cap))
+            pad = &e;
+    }
+    return pad ? pad : wide();
+}
+
+// The one-system-per-block entry for (kind, solver, arith), if any.
+const KernelEntry* find_wide(const bode_problem_t* p, int solver, int arith) {
+    int n = 0;
+    const KernelEntry* tab = bode::kernel_table(&n);
+    for (int i = 0; i < n; ++i)
+        if (tab[i].wide && tab[i].kind == p->kind && tab[i].param_dim == p->param_dim &&
+            tab[i].solver == solver && tab[i].arith == arith)
+            return &tab[i];
+    return nullptr;
 }
 
 int check_problem_shape(const bode_problem_t* p) {
@@ -1327,9 +1348,11 @@ int bode_integrate_fixed(const bode_problem_t* p, int32_t solver, int32_t arith,
     const KernelEntry* e = nullptr;
     int rc = validate_call(p, solver, arith, t0, t_end, num, g, y, &tol, &e);
     if (rc) return rc;
-    if (e->wide) {  // one system per block (wide.cuh), any dimension
+    if (e->cap > 0 || e->wide) {  // run-time dimension: the one-system-per-block harness
+        const KernelEntry* w = e->wide ? e : find_wide(p, solver, arith);
+        if (w == nullptr) return fail(BODE_E_UNSUPPORTED, "no fixed-step kernel for this problem");
         if ((rc = check_devices(1))) return rc;
-        return fixed_wide(e, p, t0, t_end, num_steps, stages, kappa, num, g, y);
+        return fixed_wide(w, p, t0, t_end, num_steps, stages, kappa, num, g, y);
     }
     if (e->launch_fixed == nullptr) {  // e.g. the lane-pair Pleiades kernel: try the others
         int n = 0;

@@ -20,6 +20,16 @@
 
 namespace bode {
 
+// Parameter slots a kernel holds per system: the problem's own, or the
+// kernel-generated n and constant of a run-time-dimension problem.
+template <class P>
+__host__ __device__ constexpr int params_of() {
+    if constexpr (is_runtime_dim<P>::value)
+        return P::PG;
+    else
+        return P::P > 0 ? P::P : 1;
+}
+
 // Global component held by lane `lane` of a group in local slot c. Blocks of
 // C consecutive components by default; the 2-lane Pleiades split is by axis:
 // lane l holds positions [7l, 7l+7) and velocities [14+7l, 14+7l+7).
@@ -40,7 +50,7 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
                      DevStats* __restrict__ stats, long long num, double t, double tEnd,
                      DevTol tol, int merge) {
     constexpr int C = P::N / L;
-    constexpr int PP = P::P > 0 ? P::P : 1;
+    constexpr int PP = params_of<P>();
     const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long sys = gt / L;
     // RKC on lane groups runs warp-uniform (rkc.cuh): lanes past the batch's
@@ -52,12 +62,21 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
     Group<L> G(kUniform);
     R y[C];
     R g[PP];
+    const int n = is_runtime_dim<P>::value ? tol.dim : P::N;  // components held (the rest pad)
 #pragma unroll
-    for (int c = 0; c < C; ++c)
-        y[c] = R(inRange ? y_soa[sys + ld * (long long)comp_index<P, L>(G.lane, c)] : 0.0);
+    for (int c = 0; c < C; ++c) {
+        const int ci = comp_index<P, L>(G.lane, c);
+        y[c] = R(inRange && ci < n ? y_soa[sys + ld * (long long)ci] : 0.0);
+    }
 #pragma unroll
     for (int p = 0; p < PP; ++p)
         g[p] = R(P::P > 0 && inRange ? g_soa[sys + ld * (long long)p] : 0.0);
+    if constexpr (is_runtime_dim<P>::value) {
+        double gg[2];
+        P::params(n, gg);
+        g[0] = R(gg[0]);
+        g[1] = R(gg[1]);
+    }
     DevStats st;
     if constexpr (SOLVER == 0 && is_pleiades<P> && L == 2)
         rkck_pleiades2_system<R, BUDGET>(G, t, tEnd, y, tol, st);
@@ -71,7 +90,10 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
         rkc_system<P, R, L, BUDGET>(G, inRange, t, tEnd, y, g, tol, st);
     if (!inRange) return;
 #pragma unroll
-    for (int c = 0; c < C; ++c) y_soa[sys + ld * (long long)comp_index<P, L>(G.lane, c)] = val(y[c]);
+    for (int c = 0; c < C; ++c) {
+        const int ci = comp_index<P, L>(G.lane, c);
+        if (ci < n) y_soa[sys + ld * (long long)ci] = val(y[c]);
+    }
     if (stats != nullptr && G.lane == 0) {
         if (merge) {
             DevStats o = stats[sys];
@@ -98,7 +120,8 @@ template <class P, class R, int L, int SOLVER, bool KSMEM, int MAXREG>
 static KernelEntry make_entry(int kind, int arith) {
     KernelEntry e;
     e.kind = kind;
-    e.dim = P::N;
+    e.dim = is_runtime_dim<P>::value ? 0 : P::N;
+    e.cap = is_runtime_dim<P>::value ? P::N : 0;
     e.param_dim = P::P;
     e.solver = SOLVER;
     e.arith = arith;
@@ -128,7 +151,8 @@ static KernelEntry make_entry(int kind, int arith) {
         return (int)err;
     };
     e.build_rkc_table = nullptr;
-    if constexpr (!(SOLVER == 0 && is_pleiades<P> && L == 2)) {
+    // (run-time-dimension problems take the one-system-per-block fixed-step kernels)
+    if constexpr (!(SOLVER == 0 && is_pleiades<P> && L == 2) && !is_runtime_dim<P>::value) {
         e.ffn = (const void*)&fixed_kernel<P, R, L, SOLVER>;
         e.launch_fixed = [](const void* fn, dim3 grid, dim3 block, cudaStream_t s,
                             const double* g, double* y, long long num, double t0, double tEnd,

@@ -34,6 +34,9 @@ static const KernelEntry* kernel_table_rkck(int* count) {
         BODE_BOTH_ARITH(Const<1>, 1, 0, false, 7),
         BODE_BOTH_ARITH(SinT, 1, 0, false, 8),
         BODE_BOTH_ARITH(Heat<8>, 1, 0, false, 1),
+        // heatEquation(n), n <= 64 without an exact-size kernel (RKCK): padded groups
+        BODE_BOTH_ARITH(HeatPad<16>, 2, 0, false, 1),
+        BODE_BOTH_ARITH_R(HeatPad<64>, 8, 0, false, 1, 128),
     };
     *count = (int)(sizeof(table) / sizeof(table[0]));
     return table;

@@ -34,7 +34,13 @@ const KernelEntry* kernel_table_rkc(int* count) {
         BODE_BOTH_ARITH(Zero<1>, 1, 1, false, 4),
         BODE_BOTH_ARITH(Diag<3>, 1, 1, false, 6),
         BODE_BOTH_ARITH(Const<1>, 1, 1, false, 7),
-        // heatEquation(n) for any other n >= 2: one system per thread block
+        // heatEquation(n) for any other n <= 512: padded lane groups (8 components
+        // per lane as heat64; n > 64 on wider groups)
+        BODE_BOTH_ARITH_R(HeatPad<64>, 8, 1, false, 1, 128),
+        BODE_BOTH_ARITH_R(HeatPad<128>, 16, 1, false, 1, 128),
+        BODE_BOTH_ARITH_R(HeatPad<256>, 32, 1, false, 1, 128),
+        BODE_BOTH_ARITH_R(HeatPad<512>, 32, 1, false, 1, 0),
+        // ... and for any larger n: one system per thread block
         make_wide_entry<HeatWide, xd, 0>(1, 0),
         make_wide_entry<HeatWide, double, 0>(1, 1),
         make_wide_entry<HeatWide, xd, 1>(1, 0),

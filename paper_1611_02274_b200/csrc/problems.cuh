@@ -9,6 +9,8 @@
 // exactly, so with R = xd the result is bitwise the reference's.
 #pragma once
 
+#include <type_traits>
+
 #include "arith.cuh"
 
 namespace bode {
@@ -244,6 +246,65 @@ struct Heat {
                 out[c] = (um - R(2.0) * u[c]) * R(inv);
             else
                 out[c] = (um - R(2.0) * u[c] + up) * R(inv);
+        }
+    }
+};
+
+// Run-time dimension on the lane-group kernels: a problem with
+// `runtime_dim = true` has the compile-time capacity N (lane groups of N/L
+// components) and integrates the first n <= N components, n = tol.dim. The
+// kernel hands n and the problem's constant to rhs() in g[0] and g[1] (the
+// problem has no parameters of its own); the components from n to N are
+// padding that stays exactly +0.0, which leaves every reference sum and max
+// bitwise unchanged (a +0.0 term adds nothing to a sum of squares or a
+// max-norm), so the results are the unpadded reference's.
+template <class P, class = void>
+struct is_runtime_dim : std::false_type {};
+template <class P>
+struct is_runtime_dim<P, decltype((void)P::runtime_dim)> : std::bool_constant<P::runtime_dim> {};
+// the system's dimension (the divisor of the RMS norms, rkc.cpp:128, :164;
+// the flip index of the power method, spectral_radius.cpp:76)
+template <class P, class R>
+__device__ __forceinline__ int dim_of(const R* g) {
+    if constexpr (is_runtime_dim<P>::value)
+        return (int)val(g[0]);
+    else
+        return P::N;
+}
+
+// heatEquation(n) (problems.cpp:94-115) for any n <= CAP on CAP-component lane
+// groups: g[0] = n, g[1] = 1/dx^2 formed as the reference does, in IEEE double.
+template <int CAP>
+struct HeatPad {
+    static constexpr int N = CAP, P = 0, PG = 2;
+    static constexpr bool runtime_dim = true;
+    static constexpr const char* name = "heat";
+    __device__ __forceinline__ static void params(int n, double* g) {
+        g[0] = double(n);
+        const double dx = __ddiv_rn(1.0, double(n + 1));
+        g[1] = __ddiv_rn(1.0, __dmul_rn(dx, dx));
+    }
+    template <class R, int L>
+    __device__ __forceinline__ static void rhs(const Group<L>& G, R, const R (&u)[N / L],
+                                               const R* g, R (&out)[N / L]) {
+        constexpr int C = N / L;
+        const int n = (int)val(g[0]);
+        const R inv = g[1];
+        const R left = R(G.from_prev(val(u[C - 1])));
+        const R right = R(G.from_next(val(u[0])));
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            const int i = G.lane * C + c;
+            const R um = (c > 0) ? u[c - 1] : left;
+            const R up = (c < C - 1) ? u[c + 1] : right;
+            if (i >= n)
+                out[c] = R(0.0);
+            else if (i == 0)
+                out[c] = (R(-2.0) * u[c] + up) * inv;
+            else if (i == n - 1)
+                out[c] = (um - R(2.0) * u[c]) * inv;
+            else
+                out[c] = (um - R(2.0) * u[c] + up) * inv;
         }
     }
 };

@@ -317,13 +317,22 @@ __device__ __forceinline__ bool phase_any(bool b) {
 // two, x * 2^-k rounds the same real number, so the product is bitwise the
 // quotient (subnormals, infinities and NaN included) without a division.
 template <int N, class R>
-__device__ __forceinline__ R div_by_dim(R x) {
+__device__ __forceinline__ R div_by_dim_ct(R x) {
     if constexpr (N == 1)
         return x;
     else if constexpr ((N & (N - 1)) == 0)
         return x * R(1.0 / N);
     else
         return x / R(double(N));
+}
+// x / n for the system's dimension: compile-time, or the run-time n of a
+// padded problem (an IEEE division, as the reference's)
+template <class P, class R>
+__device__ __forceinline__ R div_by_dim(R x, const R* g) {
+    if constexpr (is_runtime_dim<P>::value)
+        return x / R(double(dim_of<P>(g)));
+    else
+        return div_by_dim_ct<P::N>(x);
 }
 
 // Power method (spectral_radius.cpp:17-85) for the groups with `on` set; the
@@ -374,6 +383,11 @@ __device__ __forceinline__ int power_method(const Group<L>& G, bool on, R t, con
         dynrm = kUround;
 #pragma unroll
         for (int c = 0; c < C; ++c) v[c] = kUround;
+        if constexpr (is_runtime_dim<P>::value) {  // padding stays +0.0
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+                if (G.lane * C + c >= dim_of<P>(g)) v[c] = R(0.0);
+        }
     }
     R sigma(0.0);
     int iters = 0;
@@ -401,7 +415,7 @@ __device__ __forceinline__ int power_method(const Group<L>& G, bool on, R t, con
 #pragma unroll
                 for (int c = 0; c < C; ++c) v[c] = y[c] + (fv[c] - f0[c]) * (dynrm / diffNrm);
             } else {  // degenerate direction: flip one component about y
-                const int ind = iter % P::N;
+                const int ind = iter % dim_of<P>(g);
 #pragma unroll
                 for (int c = 0; c < C; ++c)
                     if (G.lane * C + c == ind) v[c] = y[c] - (v[c] - y[c]);
@@ -464,7 +478,7 @@ __device__ __forceinline__ R rkc_initial_step(const Group<L>& G, bool on, R t, c
     for (int c = 0; c < C; ++c) wa[c] = wa[c] * wa[c];
     const R sum = rkc_seq_sum<R, L, C>(G, wa, R(0.0));
     if (!on) return hMax;
-    const R err = h * sqrt_(div_by_dim<P::N>(sum));
+    const R err = h * sqrt_(div_by_dim<P>(sum, g));
     if (R(0.1) * h < hMax * sqrt_(err))
         return fmax_(R(0.1) * h / sqrt_(err), hMin);
     return hMax;
@@ -472,7 +486,8 @@ __device__ __forceinline__ R rkc_initial_step(const Group<L>& G, bool on, R t, c
 
 // errorNorm (rkc.cpp:119-129) of the trial y1 = wa with f(t + h, y1) = wb.
 template <class P, class R, int L, class Y, class F0>
-__device__ __forceinline__ R rkc_error_norm(const Group<L>& G, const Y& ys, const R (&y1)[P::N / L],
+__device__ __forceinline__ R rkc_error_norm(const Group<L>& G, const R* g, const Y& ys,
+                                            const R (&y1)[P::N / L],
                                             const F0& f0, const R (&f1)[P::N / L], R h, R absTol,
                                             R relTol) {
     constexpr int C = P::N / L;
@@ -482,7 +497,7 @@ __device__ __forceinline__ R rkc_error_norm(const Group<L>& G, const Y& ys, cons
         [&](int c) { return absTol + relTol * fmax_abs(ys[c], y1[c]); }, terms);
 #pragma unroll
     for (int c = 0; c < C; ++c) terms[c] = terms[c] * terms[c];
-    return sqrt_(div_by_dim<P::N>(rkc_seq_sum<R, L, C>(G, terms, R(0.0))));
+    return sqrt_(div_by_dim<P>(rkc_seq_sum<R, L, C>(G, terms, R(0.0)), g));
 }
 
 // stageCount (rkc.cpp:131-144) for the spectral radius estimate wsSpecRad
@@ -686,7 +701,7 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
         BODE_PHASE_MARK(2);
         P::template rhs<R, L>(G, t + h, wa, g, wb);  // f_trial (rkc.cpp:247)
         ++st.rhs_evals;
-        const R err = rkc_error_norm<P, R, L>(G, ys, wa, f0, wb, h, absTol, relTol);
+        const R err = rkc_error_norm<P, R, L>(G, g, ys, wa, f0, wb, h, absTol, relTol);
         BODE_PHASE_MARK(3);
         BODE_PHASE_CTRL_BEGIN
         if (rkc_finish_attempt<R>(err, h, hMin, hMax, uround, cbrtU, tol.p1, st, t, numStep,
@@ -899,7 +914,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
         }
         BODE_PHASE_MARK(2);
         P::template rhs<R, L>(G, t + h, wa, g, wb);  // f_trial (rkc.cpp:247)
-        const R err = rkc_error_norm<P, R, L>(G, ys, wa, f0, wb, h, absTol, relTol);
+        const R err = rkc_error_norm<P, R, L>(G, g, ys, wa, f0, wb, h, absTol, relTol);
         BODE_PHASE_MARK(3);
         BODE_PHASE_CTRL_BEGIN
         if (!att) continue;

@@ -17,13 +17,15 @@ from test_gpu_parity import run_gpu
 pytestmark = pytest.mark.gpu
 
 
-def _window(prob, solver, y0, arith, budget, t1):
+def _window(prob, solver, y0, arith, budget, t1, wide=False):
     L = B.lib()
     assert L.bode_set_attempt_budget(budget) == 0
+    L.bode_set_wide(1 if wide else 0)
     try:
         return run_gpu(prob, solver, y0, None, arith, t1=t1, hout=t1)
     finally:
         L.bode_set_attempt_budget(0)
+        L.bode_set_wide(0)
 
 
 @pytest.mark.parametrize("case", ["pleiades_fast", "pleiades_exact", "heat64_rkc", "heat100_wide"])
@@ -41,11 +43,12 @@ def test_budget_freezes_only_the_systems_that_reach_it(gpu, case):
         y0 = perturb(heat_ic(100), 0.01, 9, 256)
         arith, t1 = "exact", 0.1
     num = y0.size // n
-    y_free, st_free = _window(prob, solver, y0, arith, 0, t1)
+    wide = case == "heat100_wide"  # the one-system-per-block kernel (forced)
+    y_free, st_free = _window(prob, solver, y0, arith, 0, t1, wide)
     att = st_free["steps_accepted"] + st_free["steps_rejected"]
     budget = int(np.percentile(att, 90))
     assert att.max() > budget  # some systems must hit it
-    y_b, st_b = _window(prob, solver, y0, arith, budget, t1)
+    y_b, st_b = _window(prob, solver, y0, arith, budget, t1, wide)
     hit = st_b["budget_exhausted"] != 0
     assert not st_free["budget_exhausted"].any()
     # exactly the systems that needed more attempts than the budget

@@ -1,6 +1,7 @@
-"""heatEquation(n) for any n >= 2 (problems.cpp:94-115): the one-system-per-
-block kernels (csrc/wide.cuh) for the dimensions no lane-group kernel is
-compiled for, against the oracle.
+"""heatEquation(n) for any n >= 2 (problems.cpp:94-115) against the oracle:
+padded lane-group kernels (HeatPad, csrc/problems.cuh) for n <= 512 without
+an exact-size kernel, and the one-system-per-block kernels (csrc/wide.cuh)
+beyond that (and for every n under bode_set_wide(1)).
 
 Bars as in test_gpu_parity.py: EXACT bitwise (states and every counter),
 RKCK FAST <= 1e-13 per system with identical counts, RKC FAST reported
@@ -27,29 +28,50 @@ def _bitwise(y, st, yo, so):
     assert np.array_equal(st["h_max_seen"], so["h_max_seen"])
 
 
-@pytest.mark.parametrize("n", [2, 3, 5, 17, 63, 100, 129, 513])
-def test_heat_any_n_rkc_exact_bitwise(gpu, oracle, n):
+class forced_wide:
+    """bode_set_wide(1) for the block: the one-system-per-block kernels even
+    where a (padded) lane-group kernel holds the dimension."""
+    def __init__(self, on):
+        self.on = on
+
+    def __enter__(self):
+        B.lib().bode_set_wide(1 if self.on else 0)
+
+    def __exit__(self, *a):
+        B.lib().bode_set_wide(0)
+
+
+@pytest.mark.parametrize("wide", [False, True], ids=["lanes", "blocks"])
+@pytest.mark.parametrize("n", [2, 3, 5, 17, 63, 100, 129, 300, 512, 513])
+def test_heat_any_n_rkc_exact_bitwise(gpu, oracle, n, wide):
+    """n <= 512 runs on padded lane groups (HeatPad, problems.cuh), larger n
+    on one system per block; forcing the block kernels checks those at small
+    n too."""
     num = 96
     prob = A.make_problem(A.HEAT, n)
     assert B.lib().bode_problem_supported(prob, A.SOLVER_RKC, A.ARITH_EXACT) == 1
     y0 = perturb(heat_ic(n), 0.01, 7 + n, num)
     t1 = 0.2 if n <= 129 else 0.02
-    y, st = run_gpu(prob, A.SOLVER_RKC, y0, None, "exact", t1=t1, hout=t1 / 2)
+    with forced_wide(wide):
+        y, st = run_gpu(prob, A.SOLVER_RKC, y0, None, "exact", t1=t1, hout=t1 / 2)
     rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKC, 0.0, t1, t1 / 2, y0)
     assert rc == 0
     _bitwise(y, st, yo, so)
 
 
+@pytest.mark.parametrize("wide", [False, True], ids=["lanes", "blocks"])
 @pytest.mark.parametrize("n,t1", [(2, 0.1), (5, 0.05), (17, 0.01), (100, 1e-3)])
-def test_heat_any_n_rkck_exact_bitwise_and_fast(gpu, oracle, n, t1):
+def test_heat_any_n_rkck_exact_bitwise_and_fast(gpu, oracle, n, t1, wide):
     num = 64
     prob = A.make_problem(A.HEAT, n)
     y0 = perturb(heat_ic(n), 0.01, 3 + n, num)
     rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKCK, 0.0, t1, t1, y0)
     assert rc == 0
-    y, st = run_gpu(prob, A.SOLVER_RKCK, y0, None, "exact", t1=t1, hout=t1)
+    with forced_wide(wide):
+        y, st = run_gpu(prob, A.SOLVER_RKCK, y0, None, "exact", t1=t1, hout=t1)
     _bitwise(y, st, yo, so)
-    y, st = run_gpu(prob, A.SOLVER_RKCK, y0, None, "fast", t1=t1, hout=t1)
+    with forced_wide(wide):
+        y, st = run_gpu(prob, A.SOLVER_RKCK, y0, None, "fast", t1=t1, hout=t1)
     assert sysrel(y, yo, num, n).max() <= 1e-13
     for k in ("steps_accepted", "steps_rejected", "rhs_evals"):
         assert np.array_equal(st[k], so[k]), k

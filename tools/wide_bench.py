@@ -1,6 +1,6 @@
 #!/usr/bin/env python3
-"""Throughput of the one-system-per-block heat kernels (csrc/wide.cuh) at a few
-dimensions, next to the reference CPU path (oracle/_ref, all host threads) on
+"""Throughput of heatEquation(n) at dimensions without an exact-size kernel
+(padded lane groups for n <= 512, one system per block beyond), next to the reference CPU path (oracle/_ref, all host threads) on
 the same systems, and the forced block kernel at n = 64 next to the 8-lane
 kernel.
 
@@ -59,14 +59,16 @@ def gpu_time(n, num, force_wide=False):
 def main():
     out = []
     ref = RefLib() if ref_available() else None
-    for n, num in ((100, 1 << 16), (1000, 1 << 13), (10000, 1 << 9)):
+    for n, num in ((100, 1 << 16), (300, 1 << 15), (1000, 1 << 13), (10000, 1 << 9)):
         secs, y, st, y0 = gpu_time(n, num)
         row = {"n": n, "systems": num, "window": T1, "gpu_s": secs,
                "gpu_system_windows_per_s": num / secs,
                "stages_per_system": float(st["stages_total"].mean()),
-               "vectors": "shared memory" if 8 * n * 8 <= 200 * 1024 else "global scratch"}
+               "kernel": ("padded lane groups" if n <= 512 else
+                          "one system per block, shared memory" if 8 * n * 8 <= 200 * 1024 else
+                          "one system per block, global scratch")}
         if ref is not None:
-            k = min(num, {100: 8192, 1000: 2048}.get(n, 64))
+            k = min(num, {100: 8192, 300: 4096, 1000: 2048}.get(n, 64))
             t = time.perf_counter()
             rc, yo, so, _ = ref.outer_loop(A.make_problem(A.HEAT, n), A.SOLVER_RKC, 0.0, T1, T1,
                                            np.ascontiguousarray(y0.reshape(n, num)[:, :k]).reshape(-1))
