@@ -128,14 +128,27 @@ struct RkcCoefGen {
 #define BODE_RKC_CTRL_SMEM 1
 #endif
 constexpr int kRkcCtrl = BODE_RKC_CTRL_SMEM ? 5 : 0;
+// Lane groups' row: eig | f0 | stats | y | ctrl | terms (C + L/2, see below).
+template <int C>
+__host__ __device__ constexpr int kRkcCtrlOffset() { return 3 * C + 8; }
+template <int C>
+__host__ __device__ constexpr int kRkcTermsOffset() { return 3 * C + 8 + kRkcCtrl; }
+// The EXACT sum chain reads one address per group (a broadcast within the
+// group). With an odd row stride S the groups of the two half-warps land on
+// the same banks (rows 16 apart: 32 S = 0 mod 32 banks), so the terms of the
+// upper half-warp are shifted by L/2 doubles (L banks): all of a warp's
+// groups then read distinct banks in one wavefront.
+#ifndef BODE_RKC_TERMS_SKEW
+#define BODE_RKC_TERMS_SKEW 1
+#endif
+template <int L>
+__host__ __device__ constexpr int kRkcTermsSkew() {
+    return (BODE_RKC_TERMS_SKEW && L > 1 && L < 32) ? L / 2 : 0;
+}
 template <int C, int L = 1>
 __host__ __device__ constexpr int kRkcSmemStride() {
-    return ((L > 1 ? 4 : 3) * C + 8 + (L > 1 ? kRkcCtrl : 0)) | 1;
+    return L > 1 ? (kRkcTermsOffset<C>() + C + kRkcTermsSkew<L>()) | 1 : (3 * C + 8) | 1;
 }
-template <int C>
-__host__ __device__ constexpr int kRkcTermsOffset() { return 3 * C + 8; }
-template <int C>
-__host__ __device__ constexpr int kRkcCtrlOffset() { return 4 * C + 8; }
 
 // Per-device coefficient table for s = 2..kRkcTableMaxS: row(s) holds
 // muTilde_1 followed by (mu_j, nu_j, muTilde_j, gammaTilde_j, c_{j-1}) for
@@ -274,11 +287,12 @@ __device__ __forceinline__ R rkc_seq_sum(const Group<L>& G, const R (&terms)[C],
     } else if constexpr (is_exact<R>::value) {
         extern __shared__ double bode_smem[];
         constexpr int S = kRkcSmemStride<C, L>();
-        double* mine = bode_smem + threadIdx.x * S + kRkcTermsOffset<C>();
+        const int skew = (threadIdx.x & 16) ? kRkcTermsSkew<L>() : 0;
+        double* mine = bode_smem + threadIdx.x * S + kRkcTermsOffset<C>() + skew;
 #pragma unroll
         for (int c = 0; c < C; ++c) mine[c] = val(terms[c]);
         __syncwarp();
-        const double* grp = bode_smem + (threadIdx.x & ~(L - 1)) * S + kRkcTermsOffset<C>();
+        const double* grp = bode_smem + (threadIdx.x & ~(L - 1)) * S + kRkcTermsOffset<C>() + skew;
         R s = init;
 #pragma unroll
         for (int k = 0; k < L; ++k)

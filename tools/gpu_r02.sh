@@ -151,3 +151,23 @@ for p in $PARTS; do
     widebench) timeout 900 python tools/wide_bench.py > $OUT/wide_bench.jsonl 2> $OUT/wide_bench.err; echo "widebench rc=$?" >> $OUT/status.txt ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    variants)  # compiled lane/register variants of the RKC kernels, current code (BODE_LANES / BODE_MAXREG)
+      for V in "0 -1" "8 112" "8 168" "4 168" "4 255" "8 128" "0 -1"; do set -- $V
+        BODE_LANES=$1 BODE_MAXREG=$2 timeout 600 python bench.py --steps 5 --warmup 1 --systems 4096 \
+          --rkc-systems 4194304 --aux-systems 4194304 --no-e2e --no-cpu > $OUT/variant_L$1_R$2_$RANDOM.txt 2>&1
+      done
+      echo "variants rc=$?" >> $OUT/status.txt ;;
+  esac
+done
+for p in $PARTS; do
+  case $p in
+    ab_skew)  # EXACT sum-chain scratch skewed per half-warp (new) vs not (lib/ab/noskew)
+      I=0; for V in noskew new noskew new; do I=$((I+1))
+        if [ $V = new ]; then LP=; else LP=$PWD/paper_1611_02274_b200/lib/ab/$V/libbode.so; fi
+        BODE_LIB_PATH=$LP timeout 600 python bench.py --steps 5 --warmup 1 --systems 4096 --rkc-systems 4194304 \
+          --aux-systems 4194304 --no-e2e --no-cpu > $OUT/ab_skew_${I}_$V.txt 2>&1; done
+      echo "ab_skew rc=$?" >> $OUT/status.txt ;;
+  esac
+done
