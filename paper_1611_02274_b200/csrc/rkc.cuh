@@ -128,26 +128,27 @@ struct RkcCoefGen {
 #define BODE_RKC_CTRL_SMEM 1
 #endif
 constexpr int kRkcCtrl = BODE_RKC_CTRL_SMEM ? 5 : 0;
-// Lane groups' row: eig | f0 | stats | y | ctrl | terms (C + L/2, see below).
-template <int C>
-__host__ __device__ constexpr int kRkcCtrlOffset() { return 3 * C + 8; }
-template <int C>
-__host__ __device__ constexpr int kRkcTermsOffset() { return 3 * C + 8 + kRkcCtrl; }
-// The EXACT sum chain reads one address per group (a broadcast within the
-// group). With an odd row stride S the groups of the two half-warps land on
-// the same banks (rows 16 apart: 32 S = 0 mod 32 banks), so the terms of the
-// upper half-warp are shifted by L/2 doubles (L banks): all of a warp's
-// groups then read distinct banks in one wavefront.
+// Lane groups' row: eig | f0 | stats | y | ctrl | terms in the lower
+// half-warp, eig | f0 | stats | y | terms | ctrl in the upper one. The EXACT
+// sum chain reads one address per group (a broadcast within the group); with
+// an odd row stride S, groups 16 rows apart would hit the same banks (32 S = 0
+// mod 32), and the swap shifts the upper half-warp's terms by kRkcCtrl doubles
+// (10 banks), so all of a warp's groups read distinct banks in one wavefront
+// without growing the row.
 #ifndef BODE_RKC_TERMS_SKEW
 #define BODE_RKC_TERMS_SKEW 1
 #endif
-template <int L>
-__host__ __device__ constexpr int kRkcTermsSkew() {
-    return (BODE_RKC_TERMS_SKEW && L > 1 && L < 32) ? L / 2 : 0;
+template <int C>
+__device__ __forceinline__ int rkc_ctrl_offset() {
+    return 3 * C + 8 + ((BODE_RKC_TERMS_SKEW && (threadIdx.x & 16)) ? C : 0);
+}
+template <int C>
+__device__ __forceinline__ int rkc_terms_offset() {
+    return 3 * C + 8 + ((BODE_RKC_TERMS_SKEW && (threadIdx.x & 16)) ? 0 : kRkcCtrl);
 }
 template <int C, int L = 1>
 __host__ __device__ constexpr int kRkcSmemStride() {
-    return L > 1 ? (kRkcTermsOffset<C>() + C + kRkcTermsSkew<L>()) | 1 : (3 * C + 8) | 1;
+    return ((L > 1 ? 4 : 3) * C + 8 + (L > 1 ? kRkcCtrl : 0)) | 1;
 }
 
 // Per-device coefficient table for s = 2..kRkcTableMaxS: row(s) holds
@@ -287,12 +288,12 @@ __device__ __forceinline__ R rkc_seq_sum(const Group<L>& G, const R (&terms)[C],
     } else if constexpr (is_exact<R>::value) {
         extern __shared__ double bode_smem[];
         constexpr int S = kRkcSmemStride<C, L>();
-        const int skew = (threadIdx.x & 16) ? kRkcTermsSkew<L>() : 0;
-        double* mine = bode_smem + threadIdx.x * S + kRkcTermsOffset<C>() + skew;
+        const int toff = rkc_terms_offset<C>();  // the same for every lane of a group
+        double* mine = bode_smem + threadIdx.x * S + toff;
 #pragma unroll
         for (int c = 0; c < C; ++c) mine[c] = val(terms[c]);
         __syncwarp();
-        const double* grp = bode_smem + (threadIdx.x & ~(L - 1)) * S + kRkcTermsOffset<C>() + skew;
+        const double* grp = bode_smem + (threadIdx.x & ~(L - 1)) * S + toff;
         R s = init;
 #pragma unroll
         for (int k = 0; k < L; ++k)
@@ -760,7 +761,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
 
     R wsErrOld(0.0), wsH(0.0);  // Workspace::reset
 #if BODE_RKC_CTRL_SMEM
-    double* const ctrl = bode_smem + threadIdx.x * kRkcSmemStride<C, L>() + kRkcCtrlOffset<C>();
+    double* const ctrl = bode_smem + threadIdx.x * kRkcSmemStride<C, L>() + rkc_ctrl_offset<C>();
     R& cbErrOld = *reinterpret_cast<R*>(ctrl);      // cbrt(wsErrOld), once a step was accepted
     R& wsHOld = *reinterpret_cast<R*>(ctrl + 1);
     R& hNewRej = *reinterpret_cast<R*>(ctrl + 2);
