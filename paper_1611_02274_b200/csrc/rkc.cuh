@@ -128,28 +128,14 @@ struct RkcCoefGen {
 #define BODE_RKC_CTRL_SMEM 1
 #endif
 constexpr int kRkcCtrl = BODE_RKC_CTRL_SMEM ? 5 : 0;
-// Lane groups' row: eig | f0 | stats | y | ctrl | terms in the lower
-// half-warp, eig | f0 | stats | y | terms | ctrl in the upper one. The EXACT
-// sum chain reads one address per group (a broadcast within the group); with
-// an odd row stride S, groups 16 rows apart would hit the same banks (32 S = 0
-// mod 32), and the swap shifts the upper half-warp's terms by kRkcCtrl doubles
-// (10 banks), so all of a warp's groups read distinct banks in one wavefront
-// without growing the row.
-#ifndef BODE_RKC_TERMS_SKEW
-#define BODE_RKC_TERMS_SKEW 1
-#endif
-template <int C>
-__device__ __forceinline__ int rkc_ctrl_offset() {
-    return 3 * C + 8 + ((BODE_RKC_TERMS_SKEW && (threadIdx.x & 16)) ? C : 0);
-}
-template <int C>
-__device__ __forceinline__ int rkc_terms_offset() {
-    return 3 * C + 8 + ((BODE_RKC_TERMS_SKEW && (threadIdx.x & 16)) ? 0 : kRkcCtrl);
-}
 template <int C, int L = 1>
 __host__ __device__ constexpr int kRkcSmemStride() {
     return ((L > 1 ? 4 : 3) * C + 8 + (L > 1 ? kRkcCtrl : 0)) | 1;
 }
+template <int C>
+__host__ __device__ constexpr int kRkcTermsOffset() { return 3 * C + 8; }
+template <int C>
+__host__ __device__ constexpr int kRkcCtrlOffset() { return 4 * C + 8; }
 
 // Per-device coefficient table for s = 2..kRkcTableMaxS: row(s) holds
 // muTilde_1 followed by (mu_j, nu_j, muTilde_j, gammaTilde_j, c_{j-1}) for
@@ -288,12 +274,11 @@ __device__ __forceinline__ R rkc_seq_sum(const Group<L>& G, const R (&terms)[C],
     } else if constexpr (is_exact<R>::value) {
         extern __shared__ double bode_smem[];
         constexpr int S = kRkcSmemStride<C, L>();
-        const int toff = rkc_terms_offset<C>();  // the same for every lane of a group
-        double* mine = bode_smem + threadIdx.x * S + toff;
+        double* mine = bode_smem + threadIdx.x * S + kRkcTermsOffset<C>();
 #pragma unroll
         for (int c = 0; c < C; ++c) mine[c] = val(terms[c]);
         __syncwarp();
-        const double* grp = bode_smem + (threadIdx.x & ~(L - 1)) * S + toff;
+        const double* grp = bode_smem + (threadIdx.x & ~(L - 1)) * S + kRkcTermsOffset<C>();
         R s = init;
 #pragma unroll
         for (int k = 0; k < L; ++k)
@@ -761,7 +746,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
 
     R wsErrOld(0.0), wsH(0.0);  // Workspace::reset
 #if BODE_RKC_CTRL_SMEM
-    double* const ctrl = bode_smem + threadIdx.x * kRkcSmemStride<C, L>() + rkc_ctrl_offset<C>();
+    double* const ctrl = bode_smem + threadIdx.x * kRkcSmemStride<C, L>() + kRkcCtrlOffset<C>();
     R& cbErrOld = *reinterpret_cast<R*>(ctrl);      // cbrt(wsErrOld), once a step was accepted
     R& wsHOld = *reinterpret_cast<R*>(ctrl + 1);
     R& hNewRej = *reinterpret_cast<R*>(ctrl + 2);
