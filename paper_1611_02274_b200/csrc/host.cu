@@ -40,6 +40,7 @@ std::atomic<long long> g_launches{0};
 std::atomic<int> g_block_override{0};
 std::atomic<int> g_force_wide{0};  // one-system-per-block kernels even where lane kernels exist
 std::atomic<long long> g_attempt_budget{0};  // per-window attempts per system (0: none)
+std::atomic<int> g_shard_layout{0};  // 0: contiguous shards (the reference's), 1: block-cyclic
 std::atomic<int> g_persistent{0};  // dynamic-refill kernels where compiled (opt-in)
 std::atomic<double> g_repack_threshold{0.7};  // outer loop: re-pack below this efficiency
 std::atomic<int> g_presort_param{-2};  // outer loop: sort by |g[row]| first (-1 off, -2 auto)
@@ -557,27 +558,68 @@ bool host_pinned(const void* ptr) {
     return a.type == cudaMemoryTypeHost;
 }
 
-struct Shard {
-    int device;
-    int64_t begin, count;
+// A run of consecutive systems of the caller's batch [begin, begin + count)
+// held at column `local` of a shard's device SoA arrays.
+struct Range {
+    int64_t begin, count, local;
 };
 
-// Contiguous shards (batch_driver.cpp:68-73), the reference's `workers`: shard
-// d runs on device (current + d) mod device_count, so a one-process-per-GPU
-// caller (torchrun rank r with cuda:r current) and num_gpus = 1 stays on its
-// own GPU, and num_gpus above the device count puts several shards on one
-// device (as workers above the core count share cores). Results are bitwise
-// independent of the shard count (batch_driver.hpp:16-21).
+struct Shard {
+    int device;
+    int64_t begin, count;       // first system and the shard's system count
+    std::vector<Range> ranges;  // one (contiguous) or several (block-cyclic)
+};
+
+// The shard's transfer chunks: each range, the single range of a contiguous
+// shard split into `nch` column chunks (the host-pointer pipeline).
+std::vector<Range> shard_chunks(const Shard& sh, int nch) {
+    if (sh.ranges.size() > 1) return sh.ranges;
+    std::vector<Range> v;
+    const int64_t cb = sh.count / nch, crem = sh.count % nch;
+    int64_t off = 0;
+    for (int c = 0; c < nch; ++c) {
+        const int64_t nk = cb + (c < crem ? 1 : 0);
+        v.push_back({sh.begin + off, nk, off});
+        off += nk;
+    }
+    return v;
+}
+
+// Shards (batch_driver.cpp:68-73), the reference's `workers`: shard d runs on
+// device (current + d) mod device_count, so a one-process-per-GPU caller
+// (torchrun rank r with cuda:r current) and num_gpus = 1 stays on its own GPU,
+// and num_gpus above the device count puts several shards on one device (as
+// workers above the core count share cores). Results are bitwise independent
+// of the shard count and layout (batch_driver.hpp:16-21).
+//  * contiguous (default, the reference's partition): shard d holds one range;
+//  * block-cyclic (bode_set_shard_layout(1)): blocks of B systems dealt round
+//    robin, at most kMaxChunks per shard, so a batch sorted by stiffness (cost)
+//    still gives every device the same mix (SURVEY.md 7.4 hard part 7).
 std::vector<Shard> make_shards(int64_t num, int gpus) {
     std::vector<Shard> v;
     int cur = 0, n = 1;
     if (cudaGetDevice(&cur) != cudaSuccess) cur = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) n = 1;
+    if (gpus > 1 && g_shard_layout.load() == 1) {
+        const int64_t per = (int64_t)gpus * kMaxChunks;
+        const int64_t blk = std::max<int64_t>(4096, (num + per - 1) / per);
+        for (int d = 0; d < gpus; ++d) v.push_back({(cur + d) % n, 0, 0, {}});
+        for (int64_t b = 0, i = 0; b < num; b += blk, ++i) {
+            Shard& sh = v[(size_t)(i % gpus)];
+            const int64_t len = std::min<int64_t>(blk, num - b);
+            if (sh.ranges.empty()) sh.begin = b;
+            sh.ranges.push_back({b, len, sh.count});
+            sh.count += len;
+        }
+        v.erase(std::remove_if(v.begin(), v.end(), [](const Shard& s) { return s.count == 0; }),
+                v.end());
+        return v;
+    }
     const int64_t base = num / gpus, rem = num % gpus;
     int64_t b = 0;
     for (int d = 0; d < gpus; ++d) {
         const int64_t len = base + (d < rem ? 1 : 0);
-        if (len > 0) v.push_back({(cur + d) % n, b, len});
+        if (len > 0) v.push_back({(cur + d) % n, b, len, {{b, len, 0}}});
         b += len;
     }
     return v;
@@ -632,15 +674,14 @@ int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard&
     const int64_t min_chunk = 1 << 16;
     const int nchunks =
         pinned ? (int)std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, sh.count / min_chunk)) : 1;
-    const int64_t cbase = sh.count / nchunks, crem = sh.count % nchunks;
+    const std::vector<Range> chunks = shard_chunks(sh, nchunks);
     cudaStream_t sh2d = B.streams[0], sk = B.streams[1], sd2h = B.streams[2];
-    int64_t off = 0;
-    for (int k = 0; k < nchunks; ++k) {
-        const int64_t nk = cbase + (k < crem ? 1 : 0);
+    for (size_t k = 0; k < chunks.size(); ++k) {
+        const int64_t nk = chunks[k].count, off = chunks[k].local;
         double* dy = B.y + off * N;
         double* dg = P > 0 ? B.g + off * P : nullptr;
         DevStats* dst = stats ? B.st + off : nullptr;
-        const int64_t src = sh.begin + off;
+        const int64_t src = chunks[k].begin;
         cudaEvent_t in_done = B.events[2 * k], k_done = B.events[2 * k + 1];
         BODE_CUDA(cudaMemcpy2DAsync(dy, nk * sizeof(double), y + src, num * sizeof(double),
                                     nk * sizeof(double), N, cudaMemcpyHostToDevice, sh2d));
@@ -658,7 +699,6 @@ int run_shard_window(const KernelEntry* e, const bode_problem_t* p, const Shard&
         if (stats)
             BODE_CUDA(cudaMemcpyAsync(stats + src, dst, nk * sizeof(DevStats),
                                       cudaMemcpyDeviceToHost, sd2h));
-        off += nk;
     }
     for (auto& s : B.streams) BODE_CUDA(cudaStreamSynchronize(s));
     return BODE_OK;
@@ -960,6 +1000,12 @@ int bode_set_attempt_budget(int64_t max_attempts) {
     return BODE_OK;
 }
 
+int bode_set_shard_layout(int32_t layout) {
+    if (layout != 0 && layout != 1) return fail(BODE_E_INVALID_SHAPE, "shard layout must be 0 or 1");
+    g_shard_layout.store(layout);
+    return BODE_OK;
+}
+
 int bode_set_wide(int32_t mode) {
     g_force_wide.store(mode ? 1 : 0);
     return BODE_OK;
@@ -1173,14 +1219,18 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
             const bool chunked_out = last && !repacked[si] && !presort && nch > 1;
             const bool chunked = (first && !presort && nch > 1) || chunked_out;
             int r = BODE_OK;
-            if (first && !chunked) {  // upload in one piece
-                BODE_CUDA(cudaMemcpy2DAsync(B.y, cnt * sizeof(double), y + sh.begin,
-                                            num * sizeof(double), cnt * sizeof(double), N,
-                                            cudaMemcpyHostToDevice, s));
-                if (P > 0)
-                    BODE_CUDA(cudaMemcpy2DAsync(B.g, cnt * sizeof(double), g + sh.begin,
-                                                num * sizeof(double), cnt * sizeof(double), P,
+            if (first && !chunked) {  // upload in one piece (per range)
+                for (const Range& rg : sh.ranges) {
+                    BODE_CUDA(cudaMemcpy2DAsync(B.y + rg.local, cnt * sizeof(double),
+                                                y + rg.begin, num * sizeof(double),
+                                                rg.count * sizeof(double), N,
                                                 cudaMemcpyHostToDevice, s));
+                    if (P > 0)
+                        BODE_CUDA(cudaMemcpy2DAsync(B.g + rg.local, cnt * sizeof(double),
+                                                    g + rg.begin, num * sizeof(double),
+                                                    rg.count * sizeof(double), P,
+                                                    cudaMemcpyHostToDevice, s));
+                }
             }
             if (presort) {
                 // before window 1 the stats hold nothing yet (window 1 overwrites them)
@@ -1189,19 +1239,19 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
                 repacked[si] = 1;
             }
             if (chunked) {
-                const long long cb = cnt / nch, crem = cnt % nch;
-                long long off = 0;
-                for (int c = 0; c < nch; ++c) {
-                    const long long nk = cb + (c < crem ? 1 : 0);
+                const std::vector<Range> chunks = shard_chunks(sh, nch);
+                for (size_t c = 0; c < chunks.size(); ++c) {
+                    const long long nk = chunks[c].count, off = chunks[c].local;
+                    const int64_t src = chunks[c].begin;
                     cudaEvent_t in_done = B.events[2 * c], k_done = B.events[2 * c + 1];
                     if (first) {
                         BODE_CUDA(cudaMemcpy2DAsync(B.y + off, cnt * sizeof(double),
-                                                    y + sh.begin + off, num * sizeof(double),
+                                                    y + src, num * sizeof(double),
                                                     nk * sizeof(double), N,
                                                     cudaMemcpyHostToDevice, sh2d));
                         if (P > 0)
                             BODE_CUDA(cudaMemcpy2DAsync(B.g + off, cnt * sizeof(double),
-                                                        g + sh.begin + off, num * sizeof(double),
+                                                        g + src, num * sizeof(double),
                                                         nk * sizeof(double), P,
                                                         cudaMemcpyHostToDevice, sh2d));
                         BODE_CUDA(cudaEventRecord(in_done, sh2d));
@@ -1213,16 +1263,15 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
                     if (chunked_out) {
                         BODE_CUDA(cudaEventRecord(k_done, s));
                         BODE_CUDA(cudaStreamWaitEvent(sd2h, k_done, 0));
-                        BODE_CUDA(cudaMemcpy2DAsync(y + sh.begin + off, num * sizeof(double),
+                        BODE_CUDA(cudaMemcpy2DAsync(y + src, num * sizeof(double),
                                                     B.y + off, cnt * sizeof(double),
                                                     nk * sizeof(double), N,
                                                     cudaMemcpyDeviceToHost, sd2h));
                         if (stats)
-                            BODE_CUDA(cudaMemcpyAsync(stats + sh.begin + off, B.st + off,
+                            BODE_CUDA(cudaMemcpyAsync(stats + src, B.st + off,
                                                       nk * sizeof(DevStats),
                                                       cudaMemcpyDeviceToHost, sd2h));
                     }
-                    off += nk;
                 }
             } else {
                 r = launch_window(e, s, P > 0 ? B.g : nullptr, B.y, B.st, cnt, t, tk, dt,
@@ -1248,18 +1297,24 @@ int bode_outer_loop(const bode_problem_t* p, int32_t solver, int32_t arith, doub
                 }
                 BODE_CUDA(cudaEventRecord(B.snap_ready[slot], s));
                 BODE_CUDA(cudaStreamWaitEvent(sd2h, B.snap_ready[slot], 0));
-                BODE_CUDA(cudaMemcpy2DAsync(host_snap + sh.begin, num * sizeof(double), ys,
-                                            cnt * sizeof(double), cnt * sizeof(double), N,
-                                            cudaMemcpyDeviceToHost, sd2h));
+                for (const Range& rg : sh.ranges)
+                    BODE_CUDA(cudaMemcpy2DAsync(host_snap + rg.begin, num * sizeof(double),
+                                                ys + rg.local, cnt * sizeof(double),
+                                                rg.count * sizeof(double), N,
+                                                cudaMemcpyDeviceToHost, sd2h));
                 BODE_CUDA(cudaEventRecord(B.snap_copied[slot], sd2h));
             }
             if (last && !chunked_out) {
-                BODE_CUDA(cudaMemcpy2DAsync(y + sh.begin, num * sizeof(double), B.y,
-                                            cnt * sizeof(double), cnt * sizeof(double), N,
-                                            cudaMemcpyDeviceToHost, s));
-                if (stats)
-                    BODE_CUDA(cudaMemcpyAsync(stats + sh.begin, B.st, cnt * sizeof(DevStats),
-                                              cudaMemcpyDeviceToHost, s));
+                for (const Range& rg : sh.ranges) {
+                    BODE_CUDA(cudaMemcpy2DAsync(y + rg.begin, num * sizeof(double),
+                                                B.y + rg.local, cnt * sizeof(double),
+                                                rg.count * sizeof(double), N,
+                                                cudaMemcpyDeviceToHost, s));
+                    if (stats)
+                        BODE_CUDA(cudaMemcpyAsync(stats + rg.begin, B.st + rg.local,
+                                                  rg.count * sizeof(DevStats),
+                                                  cudaMemcpyDeviceToHost, s));
+                }
             }
             if (!last && threshold > 0.0 && cnt >= 1024) {
                 // re-pack when the cost history says warps idle behind stragglers

@@ -202,3 +202,54 @@ def test_multirank_bench_path_shared_gpu(gpu):
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=REPO)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "MULTIRANK_OK" in out.stdout, out.stdout[-3000:]
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_block_cyclic_shards_bitwise(gpu, pinned):
+    """bode_set_shard_layout(1): blocks dealt round robin over the shards (here
+    several shards on one device); int_driver and the outer loop (with a sink,
+    on a batch sorted by stiffness, presorted per shard) equal one shard bitwise."""
+    import torch
+    from paper_1611_02274_b200.api import stiffness_params
+    L = B.lib()
+    num = 300_001
+    g = np.sort(stiffness_params(num))  # sorted by cost: contiguous shards would be unbalanced
+    y0 = perturb(np.array([1.0]), 0.01, 5, num)
+    prob = A.Problem(A.EXPDECAY, 1, 1, 0)
+
+    def run(workers, layout):
+        yb = torch.from_numpy(y0.copy())
+        gb = torch.from_numpy(g.copy())
+        if pinned:
+            yb, gb = yb.pin_memory(), gb.pin_memory()
+        st = A.empty_stats(num)
+        L.bode_set_shard_layout(layout)
+        snaps = []
+        sink = B.api.SINK(lambda t, ys, n, d, u: snaps.append(
+            np.ctypeslib.as_array(ys, shape=(n * d,)).copy()))
+        steps = A.ctypes.c_int32(0)
+        try:
+            B.api.check(L.bode_outer_loop(prob, A.SOLVER_RKC, A.ARITH_EXACT, 0.0, 0.3, 0.1, num,
+                                          A.dptr(gb.numpy()), A.dptr(yb.numpy()), A.default_tol(),
+                                          A.vptr(st), workers, sink, None, A.ctypes.byref(steps)))
+        finally:
+            L.bode_set_shard_layout(0)
+        y1 = yb.numpy().copy()
+        yb.copy_(torch.from_numpy(y0))
+        st1 = A.empty_stats(num)
+        L.bode_set_shard_layout(layout)
+        try:
+            B.api.check(L.bode_int_driver(prob, A.SOLVER_RKC, A.ARITH_EXACT, 0.0, 0.1, num,
+                                          A.dptr(gb.numpy()), A.dptr(yb.numpy()), A.default_tol(),
+                                          A.vptr(st1), workers))
+        finally:
+            L.bode_set_shard_layout(0)
+        return y1, st, snaps, yb.numpy().copy(), st1
+
+    ref = run(1, 0)
+    for workers in (2, 3, 8):
+        got = run(workers, 1)
+        assert same(got[0], ref[0]) and same_stats(got[1], ref[1])
+        assert len(got[2]) == len(ref[2]) == 3
+        assert all(same(a, b) for a, b in zip(got[2], ref[2]))
+        assert same(got[3], ref[3]) and same_stats(got[4], ref[4])
