@@ -171,3 +171,12 @@ for p in $PARTS; do
       echo "ab_skew rc=$?" >> $OUT/status.txt ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    pvariants)  # Pleiades FAST: one lane (RKN) vs the axis-split lane pair
+      for V in 0 2 0 2; do
+        BODE_LANES=$V timeout 600 python bench.py --steps 10 --warmup 3 --no-secondary --no-e2e --no-cpu > $OUT/pvariant_L${V}_$RANDOM.txt 2>&1
+      done
+      echo "pvariants rc=$?" >> $OUT/status.txt ;;
+  esac
+done
