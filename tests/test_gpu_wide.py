@@ -147,3 +147,33 @@ def test_heat_any_n_fixed_step_bitwise(gpu, oracle, n, solver, t1, steps):
                             stages=9)
     ref = oracle_fixed(oracle, prob, solver, y0, None, num, 0.0, t1, steps, stages=9)
     assert np.array_equal(out.values.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("wide", [False, True], ids=["lanes", "blocks"])
+@pytest.mark.parametrize("solver", ["rkc", "rkck"])
+@pytest.mark.parametrize("n", [17, 100])
+def test_heat_any_n_nan_system_freezes(gpu, n, solver, wide):
+    """test_batch.cpp:241-258 on the padded and block kernels: a NaN system
+    freezes at its initial state with the underflow flag; its neighbours are
+    bitwise what they are without it."""
+    num = 40
+    prob = A.make_problem(A.HEAT, n)
+    y0 = perturb(heat_ic(n), 0.01, 5, num)
+    bad = y0.copy()
+    bad[7 + num * 3] = float("nan")  # component 3 of system 7
+    t1 = 1e-3 if solver == "rkck" else 0.05
+
+    def run(y):
+        b = B.BatchStates(num, n, 0, y.copy(), np.zeros(0))
+        with forced_wide(wide):
+            return B.integrate_batch(B.OdeProblem(prob.kind, n, 0), b, 0.0, t1, solver=solver,
+                                     arith="exact")
+
+    ref, got = run(y0), run(bad)
+    assert got.stats["underflow"][7] == 1
+    ys = got.states.values.reshape(n, num)
+    assert np.array_equal(ys[:, 7].view(np.uint64), bad.reshape(n, num)[:, 7].view(np.uint64))
+    others = np.arange(num) != 7
+    assert np.array_equal(ys[:, others].view(np.uint64),
+                          ref.states.values.reshape(n, num)[:, others].view(np.uint64))
+    assert not got.stats["underflow"][others].any()
