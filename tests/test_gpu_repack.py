@@ -155,3 +155,29 @@ def test_repack_by_param_sorts_and_unpacks(gpu):
     B.api.unpack_order(p, num, y.data_ptr(), gd.data_ptr(), 0, order.data_ptr(), s)
     torch.cuda.synchronize()
     assert np.array_equal(gd.cpu().numpy(), g) and np.array_equal(y.cpu().numpy(), y0)
+
+
+@pytest.mark.parametrize("gpus", [1, 3])
+def test_int_driver_presort_is_bitwise_invisible(gpu, gpus):
+    """bode_int_driver sorts a config-4 batch by |g0| around its window (the
+    default presort parameter) and restores the caller's order: bitwise the
+    unsorted run, with one shard or three (several on one device)."""
+    import time
+    L = B.lib()
+    num = 1 << 17
+    prob, solver, y0, g = _config4(num)
+    out, secs = {}, {}
+    for row in (-1, -2):
+        B.api.check(L.bode_set_presort_param(row))
+        batch = B.BatchStates(num, prob.dim, prob.param_dim, y0.copy(), g.copy())
+        t = time.perf_counter()
+        out[row] = B.integrate_batch(B.OdeProblem(prob.kind, prob.dim, prob.param_dim), batch,
+                                     0.0, 0.1, solver="rkc", arith="exact", gpus=gpus)
+        secs[row] = time.perf_counter() - t
+    B.api.check(L.bode_set_presort_param(-2))
+    a, b = out[-1], out[-2]
+    assert np.array_equal(a.states.values.view(np.uint64), b.states.values.view(np.uint64))
+    for k in A.STATS_DTYPE.names:
+        assert np.array_equal(a.stats[k], b.stats[k]), k
+    print(f"int_driver config 4, {num} systems: natural {secs[-1] * 1e3:.1f} ms, "
+          f"presorted {secs[-2] * 1e3:.1f} ms")
