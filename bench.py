@@ -257,6 +257,15 @@ def run_reference_arm(args):
 
 
 # ------------------------------------------------------------- device ----
+def hbm_peak_gbps():
+    """Measured HBM copy bandwidth of this pool (MEASURED_PEAKS.json, driver-written),
+    else the profiling recipe's fallback (6.65 TB/s)."""
+    try:
+        return float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6650.0
+
+
 def measured_traffic(capture: str, num: int):
     """DRAM bytes per launch for `num` systems, from the newest committed ncu
     capture summary (profiles/*_ncu.json: dram read+write per system-window),
@@ -271,7 +280,7 @@ def measured_traffic(capture: str, num: int):
                    "warp_execution_efficiency": tpi / 32.0 if tpi else None,
                    "dram_GBps": ((d["dram_read_bytes"] + d["dram_write_bytes"]) / d["duration_ns"]
                                  if d.get("duration_ns") else None),
-                   "hbm_peak_GBps": 6534.8}
+                   "hbm_peak_GBps": hbm_peak_gbps()}
             return d["dram_bytes_per_system"] * num, os.path.basename(path), ncu
     return None, None, None
 
