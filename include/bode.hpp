@@ -9,6 +9,8 @@
 //                  gatherParams, validate), BatchResult, OuterLoopResult
 //   batch helpers  pack, unpack, fillParams                     (batch.hpp:46-57)
 //   entry points   integrateBatch(...), outerLoop(...)          (batch_driver.hpp:22-43)
+//                  rkck::driver, rkck::integrateFixed, rkc::driver,
+//                  rkc::integrateFixed (one system)       (rkck.hpp:73-83, rkc.hpp:116-128)
 //   problems       pleiades(), heatEquation(n), expDecay(), harmonic(),
 //                  loadPleiadesInitialConditions, fnv1aFileChecksum,
 //                  pleiadesEnergy, pleiadesMomentum, heatSpectralRadius,
@@ -445,5 +447,66 @@ inline OuterLoopResult outerLoop(const OdeProblem& problem, const BatchStates& i
     r.outerSteps = steps;
     return r;
 }
+
+namespace detail {
+// One system (y, g) as a one-column batch through the C ABI.
+inline IntegrationStats driveOne(const OdeProblem& problem, SolverChoice solver, double t,
+                                 double tEnd, std::span<double> y, std::span<const double> g,
+                                 const ToleranceSettings& tol, Arith arith) {
+    if (!(tEnd > t))
+        throw InvalidInterval(solver == SolverChoice::RKCK ? "rkck::driver: tEnd must exceed t"
+                                                           : "rkc::driver: tEnd must exceed t");
+    if (y.size() != std::size_t(problem.dim) || g.size() != std::size_t(problem.paramDim))
+        throw InvalidShape("driver: state/parameter length does not match the problem");
+    tol.validate();
+    std::vector<bode_stats_t> st(1);
+    const bode_tol_t ct = tol.c();
+    const bode_problem_t cp = problem.c();
+    check(bode_int_driver(&cp, int(solver), int(arith), t, tEnd, 1, g.empty() ? nullptr : g.data(),
+                          y.data(), &ct, st.data(), 1));
+    return convert(st)[0];
+}
+inline void fixedOne(const OdeProblem& problem, SolverChoice solver, double t0, double tEnd,
+                     long numSteps, int stages, double kappa, std::span<double> y,
+                     std::span<const double> g, Arith arith) {
+    if (y.size() != std::size_t(problem.dim) || g.size() != std::size_t(problem.paramDim))
+        throw InvalidShape("integrateFixed: state/parameter length does not match the problem");
+    const bode_problem_t cp = problem.c();
+    check(bode_integrate_fixed(&cp, int(solver), int(arith), t0, tEnd, numSteps, stages, kappa, 1,
+                               g.empty() ? nullptr : g.data(), y.data()));
+}
+}  // namespace detail
+
+// The single-system entry points of the reference's solver headers
+// (rkck.hpp:73-83, rkc.hpp:116-128), run on the device as a one-system batch.
+// The Scratch / Workspace / StepObserver overloads have no GPU counterpart:
+// the controller state lives in registers and is not observable per attempt.
+namespace rkck {
+inline IntegrationStats driver(const OdeProblem& problem, double t, double tEnd,
+                               std::span<double> y, std::span<const double> g,
+                               const ToleranceSettings& tol = {}, Arith arith = Arith::Exact) {
+    return detail::driveOne(problem, SolverChoice::RKCK, t, tEnd, y, g, tol, arith);
+}
+// rkck::integrateFixed (rkck.cpp:168-181)
+inline void integrateFixed(const OdeProblem& problem, double t0, double tEnd, long numSteps,
+                           std::span<double> y, std::span<const double> g,
+                           Arith arith = Arith::Exact) {
+    detail::fixedOne(problem, SolverChoice::RKCK, t0, tEnd, numSteps, 0, 0.0, y, g, arith);
+}
+}  // namespace rkck
+
+namespace rkc {
+inline IntegrationStats driver(const OdeProblem& problem, double t, double tEnd,
+                               std::span<double> y, std::span<const double> g,
+                               const ToleranceSettings& tol = {}, Arith arith = Arith::Exact) {
+    return detail::driveOne(problem, SolverChoice::RKC, t, tEnd, y, g, tol, arith);
+}
+// rkc::integrateFixed (rkc.cpp:290-306)
+inline void integrateFixed(const OdeProblem& problem, double t0, double tEnd, long numSteps,
+                           int stages, double kappa, std::span<double> y,
+                           std::span<const double> g, Arith arith = Arith::Exact) {
+    detail::fixedOne(problem, SolverChoice::RKC, t0, tEnd, numSteps, stages, kappa, y, g, arith);
+}
+}  // namespace rkc
 
 }  // namespace bode
