@@ -180,3 +180,13 @@ for p in $PARTS; do
       echo "pvariants rc=$?" >> $OUT/status.txt ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    ab_cbrt)  # FAST cube root: MUFU seed + Newton (new) vs libdevice cbrt (lib/ab/libcbrt)
+      I=0; for V in libcbrt new libcbrt new; do I=$((I+1))
+        if [ $V = new ]; then LP=; else LP=$PWD/paper_1611_02274_b200/lib/ab/$V/libbode.so; fi
+        BODE_LIB_PATH=$LP timeout 600 python bench.py --steps 5 --warmup 1 --systems 4096 --rkc-systems 4194304 \
+          --aux-systems 4194304 --no-e2e --no-cpu > $OUT/ab_cbrt_${I}_$V.txt 2>&1; done
+      echo "ab_cbrt rc=$?" >> $OUT/status.txt ;;
+  esac
+done
