@@ -190,3 +190,13 @@ for p in $PARTS; do
       echo "ab_cbrt rc=$?" >> $OUT/status.txt ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    ab_sqrt)  # FAST sqrt: rsqrt seed + correction (new) vs libdevice sqrt (lib/ab/libsqrt)
+      I=0; for V in libsqrt new libsqrt new; do I=$((I+1))
+        if [ $V = new ]; then LP=; else LP=$PWD/paper_1611_02274_b200/lib/ab/$V/libbode.so; fi
+        BODE_LIB_PATH=$LP timeout 600 python bench.py --steps 5 --warmup 1 --systems 4096 --rkc-systems 4194304 \
+          --aux-systems 4194304 --no-e2e --no-cpu > $OUT/ab_sqrt_${I}_$V.txt 2>&1; done
+      echo "ab_sqrt rc=$?" >> $OUT/status.txt ;;
+  esac
+done
