@@ -135,6 +135,16 @@ static KernelEntry make_entry(int kind, int arith) {
                                         : 0;
     e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG, false>;
     e.bfn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG, true>;
+#ifndef BODE_RKN_BUDGET_INSTANCE
+#define BODE_RKN_BUDGET_INSTANCE 1
+#endif
+    // The FAST one-lane Pleiades (RKN) kernel: ptxas allocates the instance
+    // with the budget countdown without spills (254 registers) and the one
+    // without it with 76 bytes of spills at 255; with no budget set the
+    // countdown never fires, so the spill-free instance serves both.
+    if constexpr (BODE_RKN_BUDGET_INSTANCE && SOLVER == 0 && is_pleiades<P> && L == 1 &&
+                  !is_exact<R>::value)
+        e.fn = e.bfn;
     e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                   const double* g, double* y, DevStats* st, long long num, double t,
                   double tEnd, DevTol tol, int merge) -> int {

@@ -200,3 +200,12 @@ for p in $PARTS; do
       echo "ab_sqrt rc=$?" >> $OUT/status.txt ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    ab_rkn)  # FAST Pleiades on the spill-free budget instance (new) vs the plain instance (lib/ab/rknplain)
+      I=0; for V in rknplain new rknplain new rknplain new; do I=$((I+1))
+        if [ $V = new ]; then LP=; else LP=$PWD/paper_1611_02274_b200/lib/ab/$V/libbode.so; fi
+        BODE_LIB_PATH=$LP timeout 600 python bench.py --steps 20 --warmup 5 --no-secondary --no-e2e --no-cpu > $OUT/ab_rkn_${I}_$V.txt 2>&1; done
+      echo "ab_rkn rc=$?" >> $OUT/status.txt ;;
+  esac
+done
