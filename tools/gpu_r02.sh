@@ -209,3 +209,20 @@ for p in $PARTS; do
       echo "ab_rkn rc=$?" >> $OUT/status.txt ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    ncufast)  # the headline kernel only: full capture at 2^24 + launch list, summarised on the box
+      NCUP=/tmp/ncu_$TAG; mkdir -p $NCUP
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+        --log-file $NCUP/launches.csv python bench.py --steps 20 --warmup 5 > $OUT/ncu_launches_bench.txt 2>&1
+      echo "ncu_launches rc=$?" >> $OUT/status.txt
+      python tools/ncu_summary.py --launches $NCUP/launches.csv $OUT/launches > /dev/null 2>&1
+      gzip -c $NCUP/launches.csv > $OUT/launches.csv.gz
+      timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+        -k regex:Pleiades -s 1 -c 1 -o $NCUP/rkck_fast python bench.py --steps 2 --warmup 1 --systems 16777216 \
+        --no-secondary --no-e2e --no-cpu > $OUT/ncu_full_rkck_fast.txt 2>&1
+      echo "ncu_rkck_fast rc=$?" >> $OUT/status.txt
+      python tools/ncu_lines.py $NCUP/rkck_fast.ncu-rep 60 > $OUT/lines_rkck_fast.txt 2>&1
+      python tools/ncu_summary.py $OUT/ncu rkck_fast=$NCUP/rkck_fast.ncu-rep:16777216 > $OUT/ncu_summary.txt 2>&1 ;;
+  esac
+done
