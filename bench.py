@@ -478,6 +478,7 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     red_dev = "cpu" if share else "cuda"
     L = P.lib()
+    P.api.check(L.bode_use_device(local))  # this rank's GPU for the library's runtime too
     L.bode_set_persistent(1 if args.persistent else 0)
     P.api.check(L.bode_set_block_size(args.block))
     stream = torch.cuda.Stream()

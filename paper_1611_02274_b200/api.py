@@ -95,6 +95,7 @@ def lib():
         "bode_launch_count": (c_i64, []),
         "bode_set_persistent": (ctypes.c_int, [c_i32]),
         "bode_set_wide": (ctypes.c_int, [c_i32]),
+        "bode_use_device": (ctypes.c_int, [c_i32]),
         "bode_set_shard_layout": (ctypes.c_int, [c_i32]),
         "bode_set_attempt_budget": (ctypes.c_int, [c_i64]),
         "bode_stats_summary": (ctypes.c_int, [vp, c_i64, P(A.StatsSummary)]),

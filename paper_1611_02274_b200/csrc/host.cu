@@ -1037,6 +1037,17 @@ int bode_set_attempt_budget(int64_t max_attempts) {
     return BODE_OK;
 }
 
+int bode_use_device(int32_t device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
+        cudaGetLastError();
+        return fail(BODE_E_NO_DEVICE, "no CUDA device available (there is no CPU fallback)");
+    }
+    if (device < 0 || device >= n) return fail(BODE_E_INVALID_SHAPE, "device index out of range");
+    BODE_CUDA(cudaSetDevice(device));
+    return BODE_OK;
+}
+
 int bode_set_shard_layout(int32_t layout) {
     if (layout != 0 && layout != 1) return fail(BODE_E_INVALID_SHAPE, "shard layout must be 0 or 1");
     g_shard_layout.store(layout);

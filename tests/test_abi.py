@@ -134,6 +134,10 @@ def test_scheduling_knob_validation():
     """Host-side setters reject out-of-range values before any device use, and
     the re-pack entry points validate their arguments (include/bode.h)."""
     L = B.lib()
+    if L.bode_device_count() < 1:
+        assert L.bode_use_device(0) == A.E_NO_DEVICE
+    else:
+        assert L.bode_use_device(-1) == A.E_INVALID_SHAPE
     assert L.bode_set_shard_layout(2) == A.E_INVALID_SHAPE
     assert L.bode_set_shard_layout(0) == 0
     assert L.bode_set_attempt_budget(-1) == A.E_INVALID_SHAPE

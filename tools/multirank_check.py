@@ -41,6 +41,7 @@ def main():
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L = P.lib()
+    P.api.check(L.bode_use_device(local))
     num = args.systems
     b, e = D.shard_range(num, world, rank)
     base = np.array(P.problems.pleiades_initial_conditions())
