@@ -226,3 +226,13 @@ for p in $PARTS; do
       python tools/ncu_summary.py $OUT/ncu rkck_fast=$NCUP/rkck_fast.ncu-rep:16777216 > $OUT/ncu_summary.txt 2>&1 ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    ab_div)  # FAST controller/power-method division via rcp_fast (new) vs IEEE division (lib/ab/ieeediv)
+      I=0; for V in ieeediv new ieeediv new; do I=$((I+1))
+        if [ $V = new ]; then LP=; else LP=$PWD/paper_1611_02274_b200/lib/ab/$V/libbode.so; fi
+        BODE_LIB_PATH=$LP timeout 600 python bench.py --steps 5 --warmup 1 --systems 4096 --rkc-systems 4194304 \
+          --aux-systems 4194304 --no-e2e --no-cpu > $OUT/ab_div_${I}_$V.txt 2>&1; done
+      echo "ab_div rc=$?" >> $OUT/status.txt ;;
+  esac
+done
