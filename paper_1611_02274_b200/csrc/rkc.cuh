@@ -370,7 +370,7 @@ __device__ __forceinline__ int power_method(const Group<L>& G, bool on, R t, con
     if (nrmY != R(0.0) && nrmV != R(0.0)) {
         dynrm = nrmY * sqrtU;
 #pragma unroll
-        for (int c = 0; c < C; ++c) v[c] = y[c] + R(eig[c]) * div_(dynrm, nrmV);
+        for (int c = 0; c < C; ++c) v[c] = y[c] + R(eig[c]) * (dynrm / nrmV);
     } else if (nrmY != R(0.0)) {
         dynrm = nrmY * sqrtU;
 #pragma unroll
@@ -378,7 +378,7 @@ __device__ __forceinline__ int power_method(const Group<L>& G, bool on, R t, con
     } else if (nrmV != R(0.0)) {
         dynrm = kUround;
 #pragma unroll
-        for (int c = 0; c < C; ++c) v[c] = R(eig[c]) * div_(dynrm, nrmV);
+        for (int c = 0; c < C; ++c) v[c] = R(eig[c]) * (dynrm / nrmV);
     } else {
         dynrm = kUround;
 #pragma unroll
@@ -407,13 +407,13 @@ __device__ __forceinline__ int power_method(const Group<L>& G, bool on, R t, con
         if (L == 1 || run) {  // one lane per system: always on (rkc_system_lane)
             iters = iter;
             const R sigmaOld = sigma;
-            sigma = div_(diffNrm, dynrm);
+            sigma = diffNrm / dynrm;
             if (iter >= 2 && fabs_(sigma - sigmaOld) <= fmax_(sigma, small) * R(0.01)) {
                 if constexpr (L == 1) break;
                 run = false;
             } else if (diffNrm != R(0.0)) {
 #pragma unroll
-                for (int c = 0; c < C; ++c) v[c] = y[c] + (fv[c] - f0[c]) * div_(dynrm, diffNrm);
+                for (int c = 0; c < C; ++c) v[c] = y[c] + (fv[c] - f0[c]) * (dynrm / diffNrm);
             } else {  // degenerate direction: flip one component about y
                 const int ind = iter % dim_of<P>(g);
 #pragma unroll
@@ -528,7 +528,7 @@ __device__ __forceinline__ bool rkc_finish_attempt(R err, R h, R hMin, R hMax, R
     const R cb = isfinite_(err) ? cbrt_(err) : R(1.0);
     if (!(err <= R(1.0))) {
         ++st.steps_rejected;
-        hNewRej = isfinite_(err) ? div_(R(0.8) * h, cb) : R(p1) * h;
+        hNewRej = isfinite_(err) ? R(0.8) * h / cb : R(p1) * h;
         return false;
     }
     t += h;
@@ -539,11 +539,11 @@ __device__ __forceinline__ bool rkc_finish_attempt(R err, R h, R hMin, R hMax, R
     // accepted step's cbrt(err) unless errOld was floored at uround
     R fac(10.0);
     if (firstAccepted) {
-        if (R(0.8) < fac * cb) fac = div_(R(0.8), cb);
+        if (R(0.8) < fac * cb) fac = R(0.8) / cb;
     } else {
         const R t1 = R(0.8) * h * cbErrOld;
         const R t2 = wsHOld * cb * cb;
-        if (t1 < fac * t2) fac = div_(t1, t2);
+        if (t1 < fac * t2) fac = t1 / t2;
     }
     const R hNew = fmax_(hMin, fmin_(hMax, h * fmax_(R(0.1), fac)));
     wsErrOld = fmax_(err, uround);
