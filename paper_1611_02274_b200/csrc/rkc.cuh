@@ -271,7 +271,7 @@ template <class R, int L, int C>
 __device__ __forceinline__ R rkc_seq_sum(const Group<L>& G, const R (&terms)[C], R init) {
     if constexpr (L == 1 || BODE_RKC_SUM == 0) {
         return seq_sum<R, L, C>(G, terms, init);
-    } else if constexpr (is_exact<R>::value) {
+    } else if constexpr (is_exact<R>::value && BODE_RKC_SUM != 2) {  // 2: experiment only (not bitwise)
         extern __shared__ double bode_smem[];
         constexpr int S = kRkcSmemStride<C, L>();
         double* mine = bode_smem + threadIdx.x * S + kRkcTermsOffset<C>();

@@ -236,3 +236,13 @@ for p in $PARTS; do
       echo "ab_div rc=$?" >> $OUT/status.txt ;;
   esac
 done
+for p in $PARTS; do
+  case $p in
+    exp_treesum)  # experiment: EXACT heat64 with tree sums (not bitwise) -- how much the sequential chain costs
+      I=0; for V in treesum new treesum new; do I=$((I+1))
+        if [ $V = new ]; then LP=; else LP=$PWD/paper_1611_02274_b200/lib/ab/$V/libbode.so; fi
+        BODE_LIB_PATH=$LP timeout 600 python bench.py --steps 5 --warmup 1 --systems 4096 --rkc-systems 4194304 \
+          --aux-systems 0 --no-e2e --no-cpu > $OUT/exp_treesum_${I}_$V.txt 2>&1; done
+      echo "exp_treesum rc=$?" >> $OUT/status.txt ;;
+  esac
+done
