@@ -177,3 +177,22 @@ def test_heat_any_n_nan_system_freezes(gpu, n, solver, wide):
     assert np.array_equal(ys[:, others].view(np.uint64),
                           ref.states.values.reshape(n, num)[:, others].view(np.uint64))
     assert not got.stats["underflow"][others].any()
+
+
+@pytest.mark.parametrize("n", [17, 100, 300])
+def test_padded_heat_block_size_invariance(gpu, n):
+    """The padded lane-group kernels are bitwise independent of the block size
+    (batch_driver.hpp:16-21's partition independence, on the device)."""
+    L = B.lib()
+    num = 333
+    prob = A.make_problem(A.HEAT, n)
+    y0 = perturb(heat_ic(n), 0.01, 2, num)
+    outs = []
+    try:
+        for block in (0, 64, 256):
+            assert L.bode_set_block_size(block) == 0
+            outs.append(run_gpu(prob, A.SOLVER_RKC, y0, None, "exact", t1=0.02, hout=0.02))
+    finally:
+        L.bode_set_block_size(0)
+    for y, st in outs[1:]:
+        _bitwise(y, st, outs[0][0], outs[0][1])
