@@ -4,7 +4,7 @@
 // switches by replacing `batchode::` with `bode::` and linking libbode.so:
 //
 //   types          ToleranceSettings, IntegrationStats (camelCase fields,
-//                  recordAcceptedStep, merge), SolverChoice, StepRecord,
+//                  recordAcceptedStep, merge), SolverChoice, StepRecord, StepObserver,
 //                  OdeProblem, BatchStates (at, gatherState, scatterState,
 //                  gatherParams, validate), BatchResult, OuterLoopResult
 //   batch helpers  pack, unpack, fillParams                     (batch.hpp:46-57)
@@ -136,13 +136,16 @@ struct IntegrationStats {  // ode_problem.hpp:57-81
     }
 };
 
-struct StepRecord {  // ode_problem.hpp:86-93 (the device drivers keep no per-attempt log)
+struct StepRecord {  // ode_problem.hpp:86-93
     double t;
     double h;
     int stages;
     double err;
     bool accepted;
 };
+// ode_problem.hpp:93: the per-attempt hook of the single-system drivers below
+// (recorded on the device by bode_trace_steps and replayed in order).
+using StepObserver = std::function<void(const StepRecord&)>;
 
 // ode_problem.hpp:23-28 with the right-hand side named by a device problem kind.
 struct OdeProblem {
@@ -466,6 +469,37 @@ inline IntegrationStats driveOne(const OdeProblem& problem, SolverChoice solver,
                           y.data(), &ct, st.data(), 1));
     return convert(st)[0];
 }
+// driveOne with a StepObserver: the window runs once on the device with every
+// attempt recorded (bode_trace_steps), then the records replay in order.
+inline IntegrationStats driveObserved(const OdeProblem& problem, SolverChoice solver, double t,
+                                      double tEnd, std::span<double> y,
+                                      std::span<const double> g, const ToleranceSettings& tol,
+                                      const StepObserver& observer, Arith arith) {
+    if (!(tEnd > t))
+        throw InvalidInterval(solver == SolverChoice::RKCK ? "rkck::driver: tEnd must exceed t"
+                                                           : "rkc::driver: tEnd must exceed t");
+    if (y.size() != std::size_t(problem.dim) || g.size() != std::size_t(problem.paramDim))
+        throw InvalidShape("driver: state/parameter length does not match the problem");
+    tol.validate();
+    const bode_tol_t ct = tol.c();
+    const bode_problem_t cp = problem.c();
+    std::vector<bode_stats_t> st(1);
+    std::vector<bode_step_record_t> rec(1024);
+    std::vector<double> y0(y.begin(), y.end());
+    int64_t n = 0;
+    for (;;) {  // grow the record buffer until every attempt fits (re-running from y0)
+        std::copy(y0.begin(), y0.end(), y.begin());
+        check(bode_trace_steps(&cp, int(solver), int(arith), t, tEnd,
+                               g.empty() ? nullptr : g.data(), y.data(), &ct, st.data(),
+                               rec.data(), int64_t(rec.size()), &n));
+        if (n <= int64_t(rec.size())) break;
+        rec.resize(std::size_t(n));
+    }
+    if (observer)
+        for (int64_t i = 0; i < n; ++i)
+            observer(StepRecord{rec[i].t, rec[i].h, rec[i].stages, rec[i].err, rec[i].accepted != 0});
+    return convert(st)[0];
+}
 inline void fixedOne(const OdeProblem& problem, SolverChoice solver, double t0, double tEnd,
                      long numSteps, int stages, double kappa, std::span<double> y,
                      std::span<const double> g, Arith arith) {
@@ -479,9 +513,21 @@ inline void fixedOne(const OdeProblem& problem, SolverChoice solver, double t0, 
 
 // The single-system entry points of the reference's solver headers
 // (rkck.hpp:73-83, rkc.hpp:116-128), run on the device as a one-system batch.
-// The Scratch / Workspace / StepObserver overloads have no GPU counterpart:
-// the controller state lives in registers and is not observable per attempt.
+// Scratch is accepted for source compatibility (the device needs none). The
+// StepObserver overloads record every attempt on the device and replay the
+// records; the RKC Workspace (the controller state left after the window) is
+// not exported, so wsOut must be null.
 namespace rkck {
+struct Scratch {};  // rkck.hpp:22-31: per-thread buffers on the CPU; nothing to hold here
+inline IntegrationStats driver(const OdeProblem& problem, double t, double tEnd,
+                               std::span<double> y, std::span<const double> g,
+                               const ToleranceSettings& tol, Scratch&,
+                               const StepObserver* observer = nullptr,
+                               Arith arith = Arith::Exact) {
+    if (observer == nullptr)
+        return detail::driveOne(problem, SolverChoice::RKCK, t, tEnd, y, g, tol, arith);
+    return detail::driveObserved(problem, SolverChoice::RKCK, t, tEnd, y, g, tol, *observer, arith);
+}
 inline IntegrationStats driver(const OdeProblem& problem, double t, double tEnd,
                                std::span<double> y, std::span<const double> g,
                                const ToleranceSettings& tol = {}, Arith arith = Arith::Exact) {
@@ -496,6 +542,19 @@ inline void integrateFixed(const OdeProblem& problem, double t0, double tEnd, lo
 }  // namespace rkck
 
 namespace rkc {
+struct Scratch {};    // rkc.hpp:52-64: CPU buffers; nothing to hold here
+struct Workspace {};  // rkc.hpp:39-50: the controller state is not exported from the device
+inline IntegrationStats driver(const OdeProblem& problem, double t, double tEnd,
+                               std::span<double> y, std::span<const double> g,
+                               const ToleranceSettings& tol, Scratch&, Workspace* wsOut = nullptr,
+                               const StepObserver* observer = nullptr,
+                               Arith arith = Arith::Exact) {
+    if (wsOut != nullptr)
+        throw InvalidShape("rkc::driver: the device controller state (Workspace) is not exported");
+    if (observer == nullptr)
+        return detail::driveOne(problem, SolverChoice::RKC, t, tEnd, y, g, tol, arith);
+    return detail::driveObserved(problem, SolverChoice::RKC, t, tEnd, y, g, tol, *observer, arith);
+}
 inline IntegrationStats driver(const OdeProblem& problem, double t, double tEnd,
                                std::span<double> y, std::span<const double> g,
                                const ToleranceSettings& tol = {}, Arith arith = Arith::Exact) {

@@ -9,4 +9,5 @@ from .api import (BatchResult, BatchStates, BodeError, CudaError, InvalidInterva
                   InvalidShape, InvalidStageCount, NoDevice, OdeProblem, OuterLoopResult,
                   Unsupported, fill_params, int_driver_device, integrate_batch, integrate_fixed, lib,
                   outer_loop, pack, problems, stats_summary, stiffness_params, tolerance_settings,
+                  trace_steps,
                   unpack)

@@ -68,6 +68,11 @@ class Stats(ctypes.Structure):
 assert ctypes.sizeof(Stats) == 64
 
 
+STEP_DTYPE = np.dtype([("t", "<f8"), ("h", "<f8"), ("err", "<f8"), ("stages", "<i4"),
+                       ("accepted", "<i4")])  # bode_step_record_t (StepRecord)
+assert STEP_DTYPE.itemsize == 32
+
+
 class StatsSummary(ctypes.Structure):  # bode_stats_summary_t
     _fields_ = [("num", ctypes.c_int64), ("attempts_total", ctypes.c_int64),
                 ("attempts_max", ctypes.c_int64), ("attempts_argmax", ctypes.c_int64),

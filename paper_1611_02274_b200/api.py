@@ -96,6 +96,8 @@ def lib():
         "bode_set_persistent": (ctypes.c_int, [c_i32]),
         "bode_set_wide": (ctypes.c_int, [c_i32]),
         "bode_use_device": (ctypes.c_int, [c_i32]),
+        "bode_trace_steps": (ctypes.c_int, [P(A.Problem), c_i32, c_i32, c_d, c_d, PD, PD, P(A.Tol),
+                                            vp, vp, c_i64, P(c_i64)]),
         "bode_set_shard_layout": (ctypes.c_int, [c_i32]),
         "bode_set_attempt_budget": (ctypes.c_int, [c_i64]),
         "bode_stats_summary": (ctypes.c_int, [vp, c_i64, P(A.StatsSummary)]),
@@ -391,6 +393,25 @@ def lockstep_efficiency(problem: OdeProblem, solver, arith, num: int, stats_ptr:
                                          _arith(arith), num, ctypes.c_void_p(stats_ptr),
                                          ctypes.byref(eff), ctypes.c_void_p(stream or None)))
     return eff.value
+
+
+def trace_steps(problem: OdeProblem, y, g=None, t: float = 0.0, t_end: float = 1.0,
+                solver="rkck", arith="exact", tol: Optional[A.Tol] = None,
+                capacity: int = 1 << 16):
+    """rkck::driver / rkc::driver with a StepObserver (ode_problem.hpp:85-94) for one
+    system on the device (bode_trace_steps). Returns (y, stats, records): the final
+    state, the IntegrationStats and one StepRecord (t, h, err, stages, accepted)
+    per attempt, bitwise the reference observer's under EXACT."""
+    y = np.array(y, dtype=np.float64).reshape(-1)
+    gg = None if g is None else np.ascontiguousarray(g, dtype=np.float64).reshape(-1)
+    st = A.empty_stats(1)
+    rec = np.zeros(capacity, dtype=A.STEP_DTYPE)
+    n = ctypes.c_int64()
+    check(lib().bode_trace_steps(ctypes.byref(problem.c()), _solver(solver), _arith(arith),
+                                 t, t_end, A.dptr(gg), A.dptr(y),
+                                 ctypes.byref(tol or A.default_tol()), A.vptr(st),
+                                 rec.ctypes.data_as(ctypes.c_void_p), capacity, ctypes.byref(n)))
+    return y, st[0], rec[:min(n.value, capacity)].copy()
 
 
 def stats_summary(stats: np.ndarray) -> dict:

@@ -7,6 +7,14 @@ namespace bode {
 
 constexpr int kMaxBlock = 256;
 
+// One attempt of the traced system (bode_step_record_t, the reference's
+// StepRecord, ode_problem.hpp:85-91).
+struct StepRec {
+    double t, h, err;
+    int stages, accepted;
+};
+static_assert(sizeof(StepRec) == 32, "StepRec must match bode_step_record_t");
+
 struct DevTol {  // bode_tol_t, by value in the kernel parameters
     double eps, abs_tol, rel_tol, uround, tiny, safety, p1, errcon, pgrow, pshrnk,
         h_min_floor, kappa;
@@ -18,6 +26,9 @@ struct DevTol {  // bode_tol_t, by value in the kernel parameters
     int dim;                 // the problem's dimension (run-time-dimension kernels, wide.cuh)
     double* scratch;         // wide.cuh: per-block vector scratch in global memory, or null
     long long max_attempts;  // per-window attempt budget per system (0: none)
+    StepRec* trace;                  // per-attempt records of a one-system launch, or null
+    long long trace_cap;
+    unsigned long long* trace_count;
 };
 
 struct DevStats {  // bode_stats_t, per system (AoS, 64 bytes)

@@ -96,6 +96,9 @@ DevTol to_dev(const bode_tol_t* t, int dim) {
     d.dim = dim;
     d.scratch = nullptr;
     d.max_attempts = g_attempt_budget.load();
+    d.trace = nullptr;
+    d.trace_cap = 0;
+    d.trace_count = nullptr;
     return d;
 }
 
@@ -387,8 +390,10 @@ int launch_window(const KernelEntry* e, cudaStream_t s, const double* g, double*
     const long long threads = num * e->lanes;
     const long long grid = (threads + block - 1) / block;
     const size_t smem = (size_t)e->smem_per_thread * block;
-    const bool persistent = e->launch_persistent != nullptr && g_persistent.load();
-    const bool budget = tol.max_attempts > 0;
+    // (a traced launch always takes the static schedule)
+    const bool persistent =
+        e->launch_persistent != nullptr && g_persistent.load() && tol.trace == nullptr;
+    const bool budget = tol.max_attempts > 0 || tol.trace != nullptr;  // the instrumented instance
     const void* fn = persistent ? (budget ? e->bpfn : e->pfn) : (budget ? e->bfn : e->fn);
     if (fn == nullptr)
         return fail(BODE_E_UNSUPPORTED, "no kernel instance with the attempt-budget check");
@@ -1035,6 +1040,62 @@ int bode_set_attempt_budget(int64_t max_attempts) {
     if (max_attempts < 0) return fail(BODE_E_INVALID_SHAPE, "attempt budget must be >= 0");
     g_attempt_budget.store(max_attempts);
     return BODE_OK;
+}
+
+// StepObserver for one system (ode_problem.hpp:85-94): the system's window on
+// the device with the instrumented kernel instance recording every attempt.
+int bode_trace_steps(const bode_problem_t* p, int32_t solver, int32_t arith, double t,
+                     double t_end, const double* g, double* y, const bode_tol_t* tol,
+                     bode_stats_t* stats, bode_step_record_t* records, int64_t capacity,
+                     int64_t* count) {
+    const KernelEntry* e = nullptr;
+    int rc = validate_call(p, solver, arith, t, t_end, 1, g, y, tol, &e);
+    if (rc) return rc;
+    if (records == nullptr || capacity < 0 || count == nullptr)
+        return fail(BODE_E_INVALID_SHAPE, "trace: records/count NULL or negative capacity");
+    if ((rc = check_devices(1))) return rc;
+    const int N = p->dim, P = p->param_dim;
+    double *dy = nullptr, *dg = nullptr;
+    DevStats* dst = nullptr;
+    bode::StepRec* drec = nullptr;
+    unsigned long long* dn = nullptr;
+    auto release = [&]() {
+        cudaFree(dy);
+        cudaFree(dg);
+        cudaFree(dst);
+        cudaFree(drec);
+        cudaFree(dn);
+    };
+    cudaError_t ce = cudaMalloc(&dy, N * sizeof(double));
+    if (ce == cudaSuccess && P > 0) ce = cudaMalloc(&dg, P * sizeof(double));
+    if (ce == cudaSuccess) ce = cudaMalloc(&dst, sizeof(DevStats));
+    if (ce == cudaSuccess) ce = cudaMalloc(&drec, std::max<int64_t>(capacity, 1) * sizeof(bode::StepRec));
+    if (ce == cudaSuccess) ce = cudaMalloc(&dn, sizeof(unsigned long long));
+    if (ce == cudaSuccess) ce = cudaMemcpy(dy, y, N * sizeof(double), cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess && P > 0) ce = cudaMemcpy(dg, g, P * sizeof(double), cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) ce = cudaMemset(dn, 0, sizeof(unsigned long long));
+    if (ce != cudaSuccess) {
+        release();
+        return fail(BODE_E_CUDA, std::string("trace setup: ") + cudaGetErrorString(ce));
+    }
+    DevTol dt = to_dev(tol, N);
+    dt.trace = drec;
+    dt.trace_cap = capacity;
+    dt.trace_count = dn;
+    rc = launch_window(e, 0, dg, dy, dst, 1, t, t_end, dt, 0);
+    unsigned long long n = 0;
+    if (rc == BODE_OK) {
+        ce = cudaMemcpy(&n, dn, sizeof(n), cudaMemcpyDeviceToHost);
+        const int64_t kept = std::min<int64_t>((int64_t)n, capacity);
+        if (ce == cudaSuccess && kept > 0)
+            ce = cudaMemcpy(records, drec, kept * sizeof(bode::StepRec), cudaMemcpyDeviceToHost);
+        if (ce == cudaSuccess) ce = cudaMemcpy(y, dy, N * sizeof(double), cudaMemcpyDeviceToHost);
+        if (ce == cudaSuccess && stats) ce = cudaMemcpy(stats, dst, sizeof(DevStats), cudaMemcpyDeviceToHost);
+        if (ce != cudaSuccess) rc = fail(BODE_E_CUDA, std::string("trace: ") + cudaGetErrorString(ce));
+    }
+    release();
+    *count = (int64_t)n;
+    return rc;
 }
 
 int bode_use_device(int32_t device) {

@@ -704,6 +704,7 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
         const R err = rkc_error_norm<P, R, L>(G, g, ys, wa, f0, wb, h, absTol, relTol);
         BODE_PHASE_MARK(3);
         BODE_PHASE_CTRL_BEGIN
+        trace_step<BUDGET>(tol, G.lane == 0, t, h, (int)s, err, err <= R(1.0));
         if (rkc_finish_attempt<R>(err, h, hMin, hMax, uround, cbrtU, tol.p1, st, t, numStep,
                                   wsErrOld, cbErrOld, wsHOld, wsH, hNewRej)) {
 #pragma unroll
@@ -920,6 +921,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
         if (!att) continue;
         st.rhs_evals += s;  // s - 1 stages and f_trial
         st.stages_total += s;
+        trace_step<BUDGET>(tol, G.lane == 0, t, h, (int)s, err, err <= R(1.0));
         if (rkc_finish_attempt<R>(err, h, hMin, hMax, uround, cbrtU, tol.p1, st, t, numStep,
                                   wsErrOld, cbErrOld, wsHOld, wsH, hNewRej)) {
 #pragma unroll

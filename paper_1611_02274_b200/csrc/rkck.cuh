@@ -83,6 +83,21 @@ struct AttemptBudget {
         return false;
     }
 };
+// StepObserver (ode_problem.hpp:85-94, invoked at rkck.cpp:142 and rkc.cpp:253):
+// in the instrumented kernel instances only, the lead lane of a traced
+// one-system launch appends (t, h, stages, err, accepted) for every attempt.
+template <bool ON, class R>
+__device__ __forceinline__ void trace_step(const DevTol& tol, bool lead, R t, R h, int stages,
+                                           R err, bool accepted) {
+    if constexpr (ON) {
+        if (tol.trace != nullptr && lead) {
+            const unsigned long long i = atomicAdd(tol.trace_count, 1ull);
+            if (i < (unsigned long long)tol.trace_cap)
+                tol.trace[i] = StepRec{val(t), val(h), val(err), stages, accepted ? 1 : 0};
+        }
+    }
+}
+
 template <>
 struct AttemptBudget<false> {
     __device__ __forceinline__ void init(const DevTol&) {}
@@ -303,6 +318,7 @@ __device__ __forceinline__ void rkck_system(const Group<L>& G, double t_in, doub
 
         R hNew;
         const bool accepted = rkck_adjust(h, err, nanFlag, hMin, hMax, tol, hNew);
+        trace_step<BUDGET>(tol, G.lane == 0, t, h, 6, err, accepted);
         if (accepted) {
             t += h;
             stats_accept(st, val(h));

@@ -324,6 +324,7 @@ struct NystromRkck {
                 (err > tol.errcon) ? tol.safety * hh * ctrl_pow_fast(err, tol.pgrow) : 5.0 * hh;
             hNew = fmax(tol.h_min_floor, fmin(val(hMax), hn));
         }
+        trace_step<BUDGET>(tol, true, t, h, 6, R(err), accepted);
         if (accepted) {
             t += h;
             stats_accept(st, hh);
@@ -445,6 +446,7 @@ struct NystromRkck {
                 hNew = fmax(val(hMin), fmin(val(hMax), hn));
             }
         }
+        trace_step<BUDGET>(tol, true, t, h, 6, err, accepted);
         if (accepted) {
             t += h;
             stats_accept(st, val(h));

@@ -305,6 +305,7 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
                 hNew = fmax(val(hMin), fmin(val(hMax), hn));
             }
         }
+        trace_step<BUDGET>(tol, live && G.lane == 0, t, h, 6, err, accepted);
         if (live && accepted) {
             t += h;
             stats_accept(st, val(h));

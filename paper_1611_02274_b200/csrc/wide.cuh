@@ -207,6 +207,7 @@ __device__ void rkck_wide_system(const WideVecs& V, double t_in, double tEnd_in,
         err = err / eps;
         R hNew;
         const bool accepted = rkck_adjust(h, err, nanFlag, hMin, hMax, tol, hNew);
+        trace_step<true>(tol, threadIdx.x == 0, t, h, 6, err, accepted);
         if (accepted) {
             t += h;
             stats_accept(st, val(h));
@@ -417,6 +418,7 @@ __device__ void rkc_wide_system(const WideVecs& V, double t_in, double tEnd_in,
         }
         const R err = sqrt_(block_sum<R>(V.red, tmp, n) / nR);
         R hNewRej(0.0);
+        trace_step<true>(tol, threadIdx.x == 0, t, h, (int)s, err, err <= R(1.0));
         if (rkc_finish_attempt<R>(err, h, hMin, hMax, uround, cbrtU, tol.p1, st, t, numStep,
                                   wsErrOld, cbErrOld, wsHOld, wsH, hNewRej)) {
             for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = yTrial[i];
