@@ -44,7 +44,7 @@ __device__ __forceinline__ int comp_index(int lane, int c) {
 
 // MAXREG > 0 caps registers per thread (__maxnreg__) to reach a target
 // occupancy; 0 leaves ptxas the full 255 (launch bound kMaxBlock threads).
-template <class P, class R, int L, int SOLVER, bool KSMEM, int MAXREG, bool BUDGET>
+template <class P, class R, int L, int SOLVER, bool KSMEM, int MAXREG, int INSTR>
 __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
     integrate_kernel(const double* __restrict__ g_soa, double* __restrict__ y_soa,
                      DevStats* __restrict__ stats, long long num, double t, double tEnd,
@@ -79,15 +79,15 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
     }
     DevStats st;
     if constexpr (SOLVER == 0 && is_pleiades<P> && L == 2)
-        rkck_pleiades2_system<R, BUDGET>(G, t, tEnd, y, tol, st);
+        rkck_pleiades2_system<R, INSTR>(G, t, tEnd, y, tol, st);
     else if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1)
-        rkck_nystrom_system<P, R, BUDGET>(t, tEnd, y, g, tol, st);
+        rkck_nystrom_system<P, R, INSTR>(t, tEnd, y, g, tol, st);
     else if constexpr (SOLVER == 0)
-        rkck_system<P, R, L, KSMEM, BUDGET>(G, t, tEnd, y, g, tol, st);
+        rkck_system<P, R, L, KSMEM, INSTR>(G, t, tEnd, y, g, tol, st);
     else if constexpr (L == 1)
-        rkc_system_lane<P, R, BUDGET>(G, t, tEnd, y, g, tol, st);
+        rkc_system_lane<P, R, INSTR>(G, t, tEnd, y, g, tol, st);
     else
-        rkc_system<P, R, L, BUDGET>(G, inRange, t, tEnd, y, g, tol, st);
+        rkc_system<P, R, L, INSTR>(G, inRange, t, tEnd, y, g, tol, st);
     if (!inRange) return;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
@@ -106,12 +106,12 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
 }
 
 // Persistent-grid RKCK for second-order problems, one lane per system.
-template <class P, class R, bool BUDGET>
+template <class P, class R, int INSTR>
 __global__ void __launch_bounds__(kMaxBlock)
     persistent_kernel(const double* __restrict__ g_soa, double* __restrict__ y_soa,
                       DevStats* __restrict__ stats, long long num, double t, double tEnd,
                       DevTol tol, int merge, unsigned long long* counter) {
-    rkck_nystrom_persistent<P, R, BUDGET>(g_soa, y_soa, stats, num, t, tEnd, tol, merge, counter,
+    rkck_nystrom_persistent<P, R, INSTR>(g_soa, y_soa, stats, num, t, tEnd, tol, merge, counter,
                                   tol.refill_min);
 }
 
@@ -133,18 +133,21 @@ static KernelEntry make_entry(int kind, int arith) {
         e.smem_per_thread = SOLVER == 1 ? kRkcSmemStride<C_of<P, L>(), L>() * (int)sizeof(double)
                             : KSMEM     ? kSmemStride<C_of<P, L>()>() * (int)sizeof(double)
                                         : 0;
-    e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG, false>;
-    e.bfn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG, true>;
+    // Instances: 0 plain (the default launch), 2 instrumented (attempt budget
+    // and step trace), launched only while a budget or a trace is requested.
 #ifndef BODE_RKN_BUDGET_INSTANCE
 #define BODE_RKN_BUDGET_INSTANCE 1
 #endif
-    // The FAST one-lane Pleiades (RKN) kernel: ptxas allocates the instance
-    // with the budget countdown without spills (254 registers) and the one
-    // without it with 76 bytes of spills at 255; with no budget set the
-    // countdown never fires, so the spill-free instance serves both.
+    // The FAST one-lane Pleiades (RKN) kernel defaults to instance 1 (budget
+    // countdown, no trace): ptxas allocates it without spills at 254 registers,
+    // the plain one with 76 bytes of spills at 255 (+0.4%, r02y); without a
+    // budget the countdown never fires.
     if constexpr (BODE_RKN_BUDGET_INSTANCE && SOLVER == 0 && is_pleiades<P> && L == 1 &&
                   !is_exact<R>::value)
-        e.fn = e.bfn;
+        e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG, 1>;
+    else
+        e.fn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG, 0>;
+    e.bfn = (const void*)&integrate_kernel<P, R, L, SOLVER, KSMEM, MAXREG, 2>;
     e.launch = [](const void* fn, dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                   const double* g, double* y, DevStats* st, long long num, double t,
                   double tEnd, DevTol tol, int merge) -> int {
@@ -176,8 +179,8 @@ static KernelEntry make_entry(int kind, int arith) {
     if constexpr (SOLVER == 0 && is_second_order<P>::value && L == 1 && P::P == 0) {
         // (routing static launches through this instance with counter == nullptr
         // removes the spills but measured 9% slower: the any_sync loop costs more)
-        e.pfn = (const void*)&persistent_kernel<P, R, false>;
-        e.bpfn = (const void*)&persistent_kernel<P, R, true>;
+        e.pfn = (const void*)&persistent_kernel<P, R, 0>;
+        e.bpfn = (const void*)&persistent_kernel<P, R, 2>;
         e.launch_persistent = [](const void* fn, dim3 grid, dim3 block, size_t smem,
                                  cudaStream_t s, const double* g, double* y, DevStats* st,
                                  long long num, double t, double tEnd, DevTol tol, int merge,

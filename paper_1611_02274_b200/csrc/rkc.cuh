@@ -557,7 +557,7 @@ __device__ __forceinline__ bool rkc_finish_attempt(R err, R h, R hMin, R hMax, R
 // machine as rkc_system below, each lane branching on its own state. (The
 // warp-uniform form measured 5% slower here: with no shuffles to save, its
 // extra predication only costs.)
-template <class P, class R, bool BUDGET>
+template <class P, class R, int INSTR>
 __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, double tEnd_in,
                                                 R (&y)[P::N], const R* g, const DevTol& tol,
                                                 DevStats& st_out) {
@@ -578,7 +578,7 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
     R cbErrOld(0.0);  // cbrt(wsErrOld), valid once a step was accepted
     const R cbrtU = cbrt_(uround);  // cbrt(errOld) when errOld is floored at uround
     long long numStep = 0;
-    AttemptBudget<BUDGET> bud;
+    AttemptBudget<(INSTR >= 1)> bud;
     bud.init(tol);
     // f0 and the power-method eigenvector live in this lane's shared-memory
     // row (stride kRkcSmemStride<C>, odd => conflict-free): f0 is read once
@@ -704,7 +704,7 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
         const R err = rkc_error_norm<P, R, L>(G, g, ys, wa, f0, wb, h, absTol, relTol);
         BODE_PHASE_MARK(3);
         BODE_PHASE_CTRL_BEGIN
-        trace_step<BUDGET>(tol, G.lane == 0, t, h, (int)s, err, err <= R(1.0));
+        trace_step<(INSTR == 2)>(tol, G.lane == 0, t, h, (int)s, err, err <= R(1.0));
         if (rkc_finish_attempt<R>(err, h, hMin, hMax, uround, cbrtU, tol.p1, st, t, numStep,
                                   wsErrOld, cbErrOld, wsHOld, wsH, hNewRej)) {
 #pragma unroll
@@ -728,7 +728,7 @@ __device__ __forceinline__ void rkc_system_lane(const Group<1>& G, double t_in, 
 // (power method, initial step, stage loop, error norm), each group doing or
 // discarding the work by its own state. Groups with `live` clear (finished,
 // frozen, or past the batch's end) ride along; G carries the full warp mask.
-template <class P, class R, int L, bool BUDGET>
+template <class P, class R, int L, int INSTR>
 __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double t_in,
                                            double tEnd_in, R (&y)[P::N / L], const R* g,
                                            const DevTol& tol, DevStats& st_out) {
@@ -764,7 +764,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
     const R cbrtU = cbrt_(uround);  // cbrt(errOld) when errOld is floored at uround
 #endif
     long long numStep = 0;
-    AttemptBudget<BUDGET> bud;
+    AttemptBudget<(INSTR >= 1)> bud;
     bud.init(tol);
     // f0 and the power-method eigenvector live in this lane's shared-memory
     // row (stride kRkcSmemStride<C, L>, odd => conflict-free): f0 is read once
@@ -921,7 +921,7 @@ __device__ __forceinline__ void rkc_system(const Group<L>& G, bool live, double 
         if (!att) continue;
         st.rhs_evals += s;  // s - 1 stages and f_trial
         st.stages_total += s;
-        trace_step<BUDGET>(tol, G.lane == 0, t, h, (int)s, err, err <= R(1.0));
+        trace_step<(INSTR == 2)>(tol, G.lane == 0, t, h, (int)s, err, err <= R(1.0));
         if (rkc_finish_attempt<R>(err, h, hMin, hMax, uround, cbrtU, tol.p1, st, t, numStep,
                                   wsErrOld, cbErrOld, wsHOld, wsH, hNewRej)) {
 #pragma unroll

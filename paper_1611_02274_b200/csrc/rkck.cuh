@@ -53,9 +53,10 @@ __device__ __forceinline__ void stats_merge(DevStats& a, const DevStats& b) {
 #ifndef BODE_ATTEMPT_BUDGET
 #define BODE_ATTEMPT_BUDGET 1
 #endif
-// Kernels are compiled with and without it (BUDGET template flag; the host
-// launches the budgeted instance only while a budget is set), so the default
-// path carries no budget code at all.
+// Kernels are compiled with and without it (the INSTR template mode: 0 plain,
+// 1 budget, 2 budget and step trace; the host launches an instrumented
+// instance only while a budget or a trace is requested), so the default path
+// carries no budget code at all.
 template <bool ON = true>
 struct AttemptBudget {
     long long left;  // attempts still allowed (no budget: more than any window makes)
@@ -173,7 +174,7 @@ __device__ __forceinline__ bool rkck_adjust(R h, R err, bool nanFlag, R hMin, R 
 
 // One system (this lane's slice) from t to tEnd: rkck::driver (rkck.cpp:115-159).
 // y is updated in place; returns the window's stats.
-template <class P, class R, int L, bool KSMEM, bool BUDGET>
+template <class P, class R, int L, bool KSMEM, int INSTR>
 __device__ __forceinline__ void rkck_system(const Group<L>& G, double t_in, double tEnd_in,
                                             R (&y)[P::N / L], const R* g, const DevTol& tol,
                                             DevStats& st) {
@@ -190,7 +191,7 @@ __device__ __forceinline__ void rkck_system(const Group<L>& G, double t_in, doub
     R f0[C];
     KStore<R, C, KSMEM> K;
     bool haveF = false;
-    AttemptBudget<BUDGET> bud;
+    AttemptBudget<(INSTR >= 1)> bud;
     bud.init(tol);
 
 #pragma unroll 1
@@ -318,7 +319,7 @@ __device__ __forceinline__ void rkck_system(const Group<L>& G, double t_in, doub
 
         R hNew;
         const bool accepted = rkck_adjust(h, err, nanFlag, hMin, hMax, tol, hNew);
-        trace_step<BUDGET>(tol, G.lane == 0, t, h, 6, err, accepted);
+        trace_step<(INSTR == 2)>(tol, G.lane == 0, t, h, 6, err, accepted);
         if (accepted) {
             t += h;
             stats_accept(st, val(h));

@@ -97,7 +97,7 @@ __host__ __device__ constexpr int nystrom_smem_doubles() {
 // persistent kernel can hand a lane a new system as soon as its own finishes.
 constexpr bool kRkckUnrollStages = false;  // measured: unrolling adds spills, -16%
 
-template <class P, class R, bool BUDGET>
+template <class P, class R, int INSTR>
 struct NystromRkck {
     static constexpr int M = P::N / 2;
     R y[P::N];  // (q, v)
@@ -105,7 +105,7 @@ struct NystromRkck {
     R t, tEnd, hMax, h;
     bool haveF, live;
     DevStats st;
-    AttemptBudget<BUDGET> bud;  // bode_set_attempt_budget (off by default)
+    AttemptBudget<(INSTR >= 1)> bud;  // bode_set_attempt_budget (off by default)
     double* ks;         // this lane's shared-memory row (k2..k5 / k6)
     const R* gp = nullptr;  // the system's parameters (problems with P > 0)
 
@@ -324,7 +324,7 @@ struct NystromRkck {
                 (err > tol.errcon) ? tol.safety * hh * ctrl_pow_fast(err, tol.pgrow) : 5.0 * hh;
             hNew = fmax(tol.h_min_floor, fmin(val(hMax), hn));
         }
-        trace_step<BUDGET>(tol, true, t, h, 6, R(err), accepted);
+        trace_step<(INSTR == 2)>(tol, true, t, h, 6, R(err), accepted);
         if (accepted) {
             t += h;
             stats_accept(st, hh);
@@ -446,7 +446,7 @@ struct NystromRkck {
                 hNew = fmax(val(hMin), fmin(val(hMax), hn));
             }
         }
-        trace_step<BUDGET>(tol, true, t, h, 6, err, accepted);
+        trace_step<(INSTR == 2)>(tol, true, t, h, 6, err, accepted);
         if (accepted) {
             t += h;
             stats_accept(st, val(h));
@@ -482,11 +482,11 @@ struct NystromRkck {
     }
 };
 
-template <class P, class R, bool BUDGET>
+template <class P, class R, int INSTR>
 __device__ __forceinline__ void rkck_nystrom_system(double t_in, double tEnd_in,
                                                     R (&y)[P::N], const R* g, const DevTol& tol,
                                                     DevStats& st) {
-    NystromRkck<P, R, BUDGET> s;
+    NystromRkck<P, R, INSTR> s;
     s.gp = g;
 #pragma unroll
     for (int c = 0; c < P::N; ++c) s.y[c] = y[c];
@@ -504,7 +504,7 @@ __device__ __forceinline__ void rkck_nystrom_system(double t_in, double tEnd_in,
 // claims the next, so a warp never idles behind its slowest system until the
 // queue is empty. Results are per-system deterministic, hence independent of
 // which lane integrates which system.
-template <class P, class R, bool BUDGET>
+template <class P, class R, int INSTR>
 __device__ __forceinline__ void rkck_nystrom_persistent(const double* __restrict__ y_in_unused,
                                                         double* __restrict__ y_soa,
                                                         DevStats* __restrict__ stats, long long num,
@@ -516,7 +516,7 @@ __device__ __forceinline__ void rkck_nystrom_persistent(const double* __restrict
     const long long ld = tol.stride > 0 ? tol.stride : num;  // SoA row stride
     const unsigned lane = threadIdx.x & 31u;
     const unsigned lt_mask = (1u << lane) - 1u;
-    NystromRkck<P, R, BUDGET> s;
+    NystromRkck<P, R, INSTR> s;
     long long sys = -1;
     bool has = false, exhausted = false;
     if (counter == nullptr) {  // static mapping: this lane's system, no refill

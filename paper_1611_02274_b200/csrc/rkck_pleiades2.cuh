@@ -97,7 +97,7 @@ __device__ __forceinline__ void pleiades_accel_pair(const Group<2>& G, const R* 
     }
 }
 
-template <class R, bool BUDGET>
+template <class R, int INSTR>
 __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double t_in,
                                                       double tEnd_in, R (&y)[14],
                                                       const DevTol& tol, DevStats& st) {
@@ -122,7 +122,7 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
     R A0[M];
     bool haveF = false;
     bool live = tEnd - t > uround * fabs_(tEnd);  // rkck.cpp:131
-    AttemptBudget<BUDGET> bud;
+    AttemptBudget<(INSTR >= 1)> bud;
     bud.init(tol);
 
     // Warp-uniform loop: the warp iterates while any of its systems is live,
@@ -305,7 +305,7 @@ __device__ __forceinline__ void rkck_pleiades2_system(const Group<2>& G, double 
                 hNew = fmax(val(hMin), fmin(val(hMax), hn));
             }
         }
-        trace_step<BUDGET>(tol, live && G.lane == 0, t, h, 6, err, accepted);
+        trace_step<(INSTR == 2)>(tol, live && G.lane == 0, t, h, 6, err, accepted);
         if (live && accepted) {
             t += h;
             stats_accept(st, val(h));

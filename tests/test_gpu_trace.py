@@ -67,7 +67,8 @@ def test_trace_fast_and_capacity(gpu, oracle):
     y, st, rec = B.trace_steps(bp, y0, None, 0.0, 0.1, solver="rkck", arith="fast")
     assert len(rec) == len(ro)
     assert np.array_equal(rec["accepted"], ro["accepted"])
-    assert np.max(np.abs(rec["h"] - ro["h"]) / ro["h"]) < 1e-9
+    # FAST forms err from different (FMA, RKN) arithmetic: h follows err^-0.2
+    assert np.max(np.abs(rec["h"] - ro["h"]) / ro["h"]) < 1e-5
     # a short buffer keeps the first records; the count still reports every attempt
     y2, st2, rec2 = B.trace_steps(bp, y0, None, 0.0, 0.1, solver="rkck", arith="exact",
                                   capacity=3)
