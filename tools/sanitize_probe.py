@@ -54,6 +54,9 @@ def main():
         for solver in ("rkc", "rkck"):
             B.integrate_batch(hw, wb, 0.0, t1, solver=solver, arith="exact")
         B.integrate_batch(hw, wb, 0.0, t1, solver="rkc", arith="fast")
+    # the step trace (instrumented instances): RKCK EXACT lane pair, RKC heat64 lanes
+    B.trace_steps(pl, b.values.reshape(28, -1)[:, 0].copy(), None, 0.0, 0.1, solver="rkck")
+    B.trace_steps(heat, hb.values.reshape(64, -1)[:, 0].copy(), None, 0.0, 0.1, solver="rkc")
     L.bode_set_attempt_budget(5)
     B.integrate_batch(pl, b, 0.0, 0.1, solver="rkck", arith="fast")
     B.integrate_batch(heat, hb, 0.0, 0.1, solver="rkc", arith="exact")
