@@ -596,15 +596,21 @@ def main():
     skipped = []
 
     def secondary(key, problem, solver, arith, dim, make, n_total, label, steps, repack=False,
-                  presort_row=None):
+                  presort_row=None, auto_presort=True):
         if time.monotonic() - T_START > args.budget_s:
             skipped.append(key)
             return
         sb, se = D.shard_range(n_total, world, rank)
         y0s, g0s = make(sb, se - sb)
-        sec, perw, sts, _, _ = measure_device(P, A, torch, problem, solver, arith, dim, y0s, g0s,
-                                              steps, 1, stream, repack=repack,
-                                              presort_row=presort_row)
+        # auto_presort=False: the library's own sort by a stiffness parameter
+        # around each window (bode_set_presort_param, default on) is switched off
+        P.api.check(L.bode_set_presort_param(-2 if auto_presort else -1))
+        try:
+            sec, perw, sts, _, _ = measure_device(P, A, torch, problem, solver, arith, dim, y0s,
+                                                  g0s, steps, 1, stream, repack=repack,
+                                                  presort_row=presort_row)
+        finally:
+            P.api.check(L.bode_set_presort_param(-2))
         f = algorithmic_flops(problem, solver, dim, sts, steps)
         n = se - sb
         extra[key] = {"workload": label, "value": n_total * steps / secs_max(sec),
@@ -635,19 +641,27 @@ def main():
                           f"systems, {ar_.upper()}", w10)
             expd = lambda b0, n: (gen_states(L, np.array([1.0]), 0.01, 42, b0, n),
                                   stiffness_range(b0, n))
+            # natural input order through the default path: bode_int_driver_device
+            # sorts each window by |g0| (the reference's specRadHint) on its own
             secondary("rkc_stiff_expdecay", "expdecay", "rkc", "exact", 1, expd, na,
                       f"RKC expDecay, g0 log-uniform in [1,1e4] (config 4), {na} systems, "
-                      f"EXACT, natural order", w10)
-            # the same natural-order batch, re-packed by its window-1 cost
+                      f"EXACT, natural input order, the library sorting each window by |g0| "
+                      f"(default)", w10)
+            # the same batch with that sort switched off: the raw lockstep cost
+            secondary("rkc_stiff_expdecay_unsorted", "expdecay", "rkc", "exact", 1, expd, na,
+                      f"RKC expDecay config 4, natural order, library sort off, {na} systems, "
+                      f"EXACT", w10, auto_presort=False)
+            # the natural-order batch re-packed by its window-1 cost
             # (bode_repack_by_cost) and restored at the end, inside the timing
             secondary("rkc_stiff_expdecay_repacked", "expdecay", "rkc", "exact", 1, expd, na,
-                      f"RKC expDecay config 4 batch re-packed by cost after window 1, {na} "
-                      f"systems, EXACT", w10, repack=True)
-            # sorted by |g0| (its spectral radius, the reference's specRadHint)
-            # before window 1 (bode_repack_by_param), restored at the end, timed
+                      f"RKC expDecay config 4 batch re-packed by cost after window 1 (library "
+                      f"sort off), {na} systems, EXACT", w10, repack=True, auto_presort=False)
+            # sorted once by |g0| before window 1 (bode_repack_by_param), restored
+            # at the end, timed
             secondary("rkc_stiff_expdecay_presorted", "expdecay", "rkc", "exact", 1, expd, na,
-                      f"RKC expDecay config 4 batch sorted by |g0| before window 1, {na} "
-                      f"systems, EXACT", w10, presort_row=0)
+                      f"RKC expDecay config 4 batch sorted by |g0| once before window 1 "
+                      f"(library sort off), {na} systems, EXACT", w10, presort_row=0,
+                      auto_presort=False)
             bru = lambda lo, hi: (lambda b0, n: (
                 gen_states(L, brusselator_ic(32), 0.01, 7, b0, n),
                 brusselator_params(na, lo, hi).reshape(3, na)[:, b0:b0 + n].copy().reshape(-1)))
@@ -739,7 +753,7 @@ def cpu_leg(args, P, A, torch, stream, extra):
     for key, prob, solver, base, mag, ns, g, gpu_key in (
             ("rkc_heat64", "heat", "rkc", heat_ic(64), 0.01, heat_n, None, "rkc_heat64"),
             ("rkc_stiff_expdecay", "expdecay", "rkc", np.array([1.0]), 0.01, n,
-             stiffness_range(0, n), "rkc_stiff_expdecay_presorted"),
+             stiffness_range(0, n), "rkc_stiff_expdecay"),
             ("rkck_stress", "pleiades", "rkck", PLEIADES_IC, 0.1, n, None, "rkck_stress_fast")):
         if time.monotonic() - T_START > args.budget_s:
             break

@@ -1206,6 +1206,48 @@ int bode_lockstep_efficiency(const bode_problem_t* p, int32_t solver, int32_t ar
     return rc ? fail(rc, "lockstep efficiency failed") : BODE_OK;
 }
 
+// One window of a device-resident batch sorted by a stiffness parameter: the
+// caller's arrays are copied into a stream-ordered scratch, sorted there
+// (bode_repack_by_param), integrated, unpacked and copied back, all on the
+// caller's stream (asynchronous; the caller's g is only read). Bitwise the
+// unsorted window.
+int presorted_device_window(const KernelEntry* e, const bode_problem_t* p, cudaStream_t s,
+                            const double* g_dev, double* y_dev, DevStats* st_dev, int merge,
+                            int64_t num, double t, double t_end, const DevTol& dt, int row) {
+    const int N = p->dim, P = p->param_dim;
+    const size_t n = (size_t)num;
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t by = al(n * N * sizeof(double)), bg = al(n * P * sizeof(double)),
+                 bs = al(n * sizeof(DevStats)), bo = al(n * sizeof(long long));
+    char* base = nullptr;
+    BODE_CUDA(cudaMallocAsync((void**)&base, by + bg + bs + bo, s));
+    double* wy = reinterpret_cast<double*>(base);
+    double* wg = reinterpret_cast<double*>(base + by);
+    DevStats* wst = st_dev ? reinterpret_cast<DevStats*>(base + by + bg) : nullptr;
+    long long* word = reinterpret_cast<long long*>(base + by + bg + bs);
+    int rc = BODE_OK;
+    cudaError_t ce = cudaMemcpyAsync(wy, y_dev, n * N * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (ce == cudaSuccess)
+        ce = cudaMemcpyAsync(wg, g_dev, n * P * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (ce == cudaSuccess && wst && merge)
+        ce = cudaMemcpyAsync(wst, st_dev, n * sizeof(DevStats), cudaMemcpyDeviceToDevice, s);
+    if (ce != cudaSuccess) rc = fail(BODE_E_CUDA, std::string("presort copy: ") + cudaGetErrorString(ce));
+    if (!rc && (rc = bode::init_order(word, num, s))) rc = fail(rc, "order init failed");
+    if (!rc && (rc = bode::repack_by(N, P, num, wy, wg, (wst && merge) ? wst : nullptr, word, row, s)))
+        rc = fail(rc, "presort failed");
+    if (!rc) rc = launch_window(e, s, wg, wy, wst, num, t, t_end, dt, merge);
+    if (!rc && (rc = bode::unpack(N, P, num, wy, nullptr, wst, word, nullptr, s)))
+        rc = fail(rc, "unpack failed");
+    if (!rc) {
+        ce = cudaMemcpyAsync(y_dev, wy, n * N * sizeof(double), cudaMemcpyDeviceToDevice, s);
+        if (ce == cudaSuccess && wst)
+            ce = cudaMemcpyAsync(st_dev, wst, n * sizeof(DevStats), cudaMemcpyDeviceToDevice, s);
+        if (ce != cudaSuccess) rc = fail(BODE_E_CUDA, std::string("presort copy back: ") + cudaGetErrorString(ce));
+    }
+    cudaFreeAsync(base, s);
+    return rc;
+}
+
 int bode_int_driver_device(const bode_problem_t* p, int32_t solver, int32_t arith, double t,
                            double t_end, int64_t num, const double* g_dev, double* y_dev,
                            const bode_tol_t* tol, bode_stats_t* stats_dev, int32_t merge_stats,
@@ -1214,6 +1256,14 @@ int bode_int_driver_device(const bode_problem_t* p, int32_t solver, int32_t arit
     int rc = validate_call(p, solver, arith, t, t_end, num, g_dev, y_dev, tol, &e);
     if (rc) return rc;
     if ((rc = check_devices(1))) return rc;
+    // a stiffness parameter known up front (bode_set_presort_param; expDecay's g0
+    // by default): sort by it around the window
+    const int presort_sel = g_presort_param.load();
+    const int row = presort_sel == -2 ? stiffness_param_row(p) : presort_sel;
+    if (row >= 0 && row < p->param_dim && g_dev != nullptr && num >= 1024)
+        return presorted_device_window(e, p, (cudaStream_t)stream, g_dev, y_dev,
+                                       (DevStats*)stats_dev, merge_stats ? 1 : 0, num, t, t_end,
+                                       to_dev(tol, p->dim), row);
     return launch_window(e, (cudaStream_t)stream, g_dev, y_dev, (DevStats*)stats_dev, num, t,
                          t_end, to_dev(tol, p->dim), merge_stats ? 1 : 0);
 }

@@ -181,3 +181,33 @@ def test_int_driver_presort_is_bitwise_invisible(gpu, gpus):
         assert np.array_equal(a.stats[k], b.stats[k]), k
     print(f"int_driver config 4, {num} systems: natural {secs[-1] * 1e3:.1f} ms, "
           f"presorted {secs[-2] * 1e3:.1f} ms")
+
+
+@pytest.mark.parametrize("merge", [False, True])
+def test_int_driver_device_presort_is_bitwise_invisible(gpu, merge):
+    """bode_int_driver_device sorts a config-4 batch by |g0| around its window
+    in a stream-ordered scratch (the caller's g is only read) and copies the
+    results back in the caller's order: bitwise the unsorted window, stats
+    merged or not."""
+    import torch
+    L = B.lib()
+    num = 100_003
+    prob, solver, y0, g = _config4(num)
+    out = {}
+    for row in (-1, -2):
+        B.api.check(L.bode_set_presort_param(row))
+        yd = torch.from_numpy(y0.copy()).cuda()
+        gd = torch.from_numpy(g.copy()).cuda()
+        st = torch.zeros(num * 8, dtype=torch.int64, device="cuda")
+        p = B.OdeProblem(prob.kind, prob.dim, prob.param_dim)
+        for k in range(2 if merge else 1):
+            B.int_driver_device(p, "rkc", "exact", 0.1 * k, 0.1 * (k + 1), num, gd.data_ptr(),
+                                yd.data_ptr(), A.default_tol(), st.data_ptr(), merge and k > 0, 0)
+        torch.cuda.synchronize()
+        assert np.array_equal(gd.cpu().numpy().view(np.uint64), g.view(np.uint64))  # g untouched
+        out[row] = (yd.cpu().numpy(), st.cpu().numpy().view(A.STATS_DTYPE))
+    B.api.check(L.bode_set_presort_param(-2))
+    (ya, sa), (yb, sb) = out[-1], out[-2]
+    assert np.array_equal(ya.view(np.uint64), yb.view(np.uint64))
+    for k in A.STATS_DTYPE.names:
+        assert np.array_equal(sa[k], sb[k]), k
