@@ -34,12 +34,16 @@ const KernelEntry* kernel_table_rkc(int* count) {
         BODE_BOTH_ARITH(Zero<1>, 1, 1, false, 4),
         BODE_BOTH_ARITH(Diag<3>, 1, 1, false, 6),
         BODE_BOTH_ARITH(Const<1>, 1, 1, false, 7),
-        // heatEquation(n) for any other n <= 512: padded lane groups (8 components
-        // per lane as heat64; n > 64 on wider groups)
+        // heatEquation(n) for any other n <= 1024: padded lane groups (8 components
+        // per lane as heat64; n > 64 on wider groups; 768 and 1024 spill under
+        // EXACT but still beat one system per block: 2.2x at n = 600, 1.4x at
+        // n = 1000, r02al)
         BODE_BOTH_ARITH_R(HeatPad<64>, 8, 1, false, 1, 128),
         BODE_BOTH_ARITH_R(HeatPad<128>, 16, 1, false, 1, 128),
         BODE_BOTH_ARITH_R(HeatPad<256>, 32, 1, false, 1, 128),
         BODE_BOTH_ARITH_R(HeatPad<512>, 32, 1, false, 1, 0),
+        BODE_BOTH_ARITH_R(HeatPad<768>, 32, 1, false, 1, 0),
+        BODE_BOTH_ARITH_R(HeatPad<1024>, 32, 1, false, 1, 0),
         // ... and for any larger n: one system per thread block
         make_wide_entry<HeatWide, xd, 0>(1, 0),
         make_wide_entry<HeatWide, double, 0>(1, 1),

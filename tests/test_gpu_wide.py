@@ -1,5 +1,5 @@
 """heatEquation(n) for any n >= 2 (problems.cpp:94-115) against the oracle:
-padded lane-group kernels (HeatPad, csrc/problems.cuh) for n <= 512 without
+padded lane-group kernels (HeatPad, csrc/problems.cuh) for n <= 1024 without
 an exact-size kernel, and the one-system-per-block kernels (csrc/wide.cuh)
 beyond that (and for every n under bode_set_wide(1)).
 
@@ -42,9 +42,9 @@ class forced_wide:
 
 
 @pytest.mark.parametrize("wide", [False, True], ids=["lanes", "blocks"])
-@pytest.mark.parametrize("n", [2, 3, 5, 17, 63, 100, 129, 300, 512, 513])
+@pytest.mark.parametrize("n", [2, 3, 5, 17, 63, 100, 129, 300, 512, 513, 1000, 1025])
 def test_heat_any_n_rkc_exact_bitwise(gpu, oracle, n, wide):
-    """n <= 512 runs on padded lane groups (HeatPad, problems.cuh), larger n
+    """n <= 1024 runs on padded lane groups (HeatPad, problems.cuh), larger n
     on one system per block; forcing the block kernels checks those at small
     n too."""
     num = 96
