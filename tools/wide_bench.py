@@ -59,16 +59,16 @@ def gpu_time(n, num, force_wide=False):
 def main():
     out = []
     ref = RefLib() if ref_available() else None
-    for n, num in ((100, 1 << 16), (300, 1 << 15), (1000, 1 << 13), (10000, 1 << 9)):
+    for n, num in ((100, 1 << 16), (300, 1 << 15), (1000, 1 << 13), (2000, 1 << 12), (10000, 1 << 9)):
         secs, y, st, y0 = gpu_time(n, num)
         row = {"n": n, "systems": num, "window": T1, "gpu_s": secs,
                "gpu_system_windows_per_s": num / secs,
                "stages_per_system": float(st["stages_total"].mean()),
-               "kernel": ("padded lane groups" if n <= 512 else
+               "kernel": ("padded lane groups" if n <= 1024 else
                           "one system per block, shared memory" if 8 * n * 8 <= 200 * 1024 else
                           "one system per block, global scratch")}
         if ref is not None:
-            k = min(num, {100: 8192, 300: 4096, 1000: 2048}.get(n, 64))
+            k = min(num, {100: 8192, 300: 4096, 1000: 2048, 2000: 512}.get(n, 64))
             t = time.perf_counter()
             rc, yo, so, _ = ref.outer_loop(A.make_problem(A.HEAT, n), A.SOLVER_RKC, 0.0, T1, T1,
                                            np.ascontiguousarray(y0.reshape(n, num)[:, :k]).reshape(-1))
