@@ -133,3 +133,18 @@ def test_rkck_stress_policies(gpu, checker):
     within = ((err <= 1e-13) & same).mean()
     print(f"stress FAST: within {within:.4f}, max {err.max():.3e}, mismatches {(~same).sum()}")
     assert within >= 0.825 and err.max() <= 3e-9 and (~same).sum() <= 1
+
+
+@pytest.mark.parametrize("n", [100, 700])
+def test_rkc_heat_any_n_stride(gpu, checker, n):
+    """heatEquation(n) on the padded lane-group kernels at scale (2^17 systems,
+    the paper's [0, 1] protocol): every 256th system bitwise the reference."""
+    from golden_cases import heat_ic
+    num = 1 << 17 if n <= 128 else 1 << 14
+    prob = A.make_problem(A.HEAT, n)
+    out, yo, so, idx = stride_case(checker, prob, A.SOLVER_RKC, heat_ic(n), 0.01, num,
+                                   256 if n <= 128 else 64, ("exact",))
+    y, st = out["exact"]
+    assert np.array_equal(y.view(np.uint64), yo.view(np.uint64))
+    for k in COUNTS:
+        assert np.array_equal(st[k], so[k]), k
