@@ -7,8 +7,10 @@
 RKCK Pleiades FAST (one lane, RKN) and EXACT (axis-split lane pair), the
 persistent refill kernel, RKC heat n=64 EXACT and FAST (8-lane warp-uniform
 groups), RKC expDecay (one lane, stiffness-varied, presort + re-pack), the
-RKC coefficient-table kernel, the fixed-step harnesses, and the outer loop
-with the asynchronous sink over two shards on one device. Prints PROBE_OK.
+RKC coefficient-table kernel, heat at run-time dimensions (padded lane
+groups, one system per block in shared or global memory), the step trace and
+attempt-budget instances, the fixed-step harnesses, and the outer loop with
+the asynchronous sink over two shards on one device. Prints PROBE_OK.
 """
 import os
 import sys
@@ -46,14 +48,19 @@ def main():
                  sink=lambda t, s: snaps.append(t))
     B.outer_loop(pl, b, 0.0, 0.3, 0.1, solver="rkck", arith="fast", gpus=2,
                  sink=lambda t, s: snaps.append(t))
-    # heat with a run-time dimension: one system per block (csrc/wide.cuh), vectors
-    # in shared memory (n = 100) and in the per-block global scratch (n = 4000)
-    for n, t1 in ((100, 1e-3), (4000, 1e-5)):
+    # heat with a run-time dimension: padded lane groups (n = 100 in HeatPad<128>,
+    # n = 1000 in HeatPad<1024>), one system per block with the vectors in shared
+    # memory (n = 1500, and n = 100 forced onto the block kernels) and in the
+    # per-block global scratch (n = 4000)
+    for n, t1, force in ((100, 1e-3, 0), (1000, 1e-4, 0), (1500, 1e-5, 0), (100, 1e-3, 1),
+                         (4000, 1e-5, 0)):
         hw = B.problems.heat_equation(n)
         wb = B.problems.perturb_initial_conditions(heat_ic(n), 0.01, 3, 20)
+        L.bode_set_wide(force)
         for solver in ("rkc", "rkck"):
             B.integrate_batch(hw, wb, 0.0, t1, solver=solver, arith="exact")
         B.integrate_batch(hw, wb, 0.0, t1, solver="rkc", arith="fast")
+        L.bode_set_wide(0)
     # the step trace (instrumented instances): RKCK EXACT lane pair, RKC heat64 lanes
     B.trace_steps(pl, b.values.reshape(28, -1)[:, 0].copy(), None, 0.0, 0.1, solver="rkck")
     B.trace_steps(heat, hb.values.reshape(64, -1)[:, 0].copy(), None, 0.0, 0.1, solver="rkc")
