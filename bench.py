@@ -633,6 +633,17 @@ def main():
                       f"RKC heat n=64 (config 3/5), {args.rkc_num} systems, EXACT", w10)
             secondary("rkc_heat64_fast", "heat", "rkc", "fast", 64, heat, args.rkc_num,
                       f"RKC heat n=64 (config 3/5), {args.rkc_num} systems, FAST", w10)
+            # heatEquation(n) at dimensions without an exact-size kernel: padded
+            # lane groups (n = 100 in HeatPad<128>) and one system per block (n = 2000)
+            for hn, hk, hcap, label in ((100, "rkc_heat100_padded", 1 << 18,
+                                         "padded 16-lane groups (HeatPad<128>)"),
+                                        (2000, "rkc_heat2000_block", 1 << 10,
+                                         "one system per thread block, vectors in shared memory")):
+                hs = min(args.rkc_num, hcap)
+                hmk = (lambda hn_: lambda b0, n: (gen_states(L, heat_ic(hn_), 0.01, 42, b0, n),
+                                                  None))(hn)
+                secondary(hk, "heat", "rkc", "exact", hn, hmk, hs,
+                          f"RKC heat n={hn}, {label}, {hs} systems, EXACT", w10)
         if args.aux_num > 0:
             na = args.aux_num
             for ar_ in ("fast", "exact"):
@@ -752,6 +763,10 @@ def cpu_leg(args, P, A, torch, stream, extra):
     heat_n = n
     for key, prob, solver, base, mag, ns, g, gpu_key in (
             ("rkc_heat64", "heat", "rkc", heat_ic(64), 0.01, heat_n, None, "rkc_heat64"),
+            ("rkc_heat100_padded", "heat", "rkc", heat_ic(100), 0.01, max(64, n // 16), None,
+             "rkc_heat100_padded"),
+            ("rkc_heat2000_block", "heat", "rkc", heat_ic(2000), 0.01, max(16, n // 2048), None,
+             "rkc_heat2000_block"),
             ("rkc_stiff_expdecay", "expdecay", "rkc", np.array([1.0]), 0.01, n,
              stiffness_range(0, n), "rkc_stiff_expdecay"),
             ("rkck_stress", "pleiades", "rkck", PLEIADES_IC, 0.1, n, None, "rkck_stress_fast")):
