@@ -1,0 +1,41 @@
+// kernels_pad_a.cu -- RKC heatEquation(n) on padded lane groups for n <= 224
+// without an exact-size kernel (HeatPad<CAP>, problems.cuh: the run-time n
+// and 1/dx^2 ride in the kernel's parameter registers, components past n are
+// +0.0 and never enter a sum). kernels_pad_b.cu holds the 32-lane groups; the
+// dispatcher (host.cu find_entry) takes the smallest capacity >= n.
+//
+// Capacity = lanes x components per lane. Fewer lanes per system and a
+// capacity close to n both pay: against round 2's set (8 components per lane,
+// capacities 64/128/256/...) this set measured 1.0x-7x, 1.3x-2.4x over most
+// of 64 < n <= 512 (profiles/r02bc_padded_caps.md). Register caps: 9
+// components fit 128 (16 warps/SM), 10-14 take 168 (12 warps/SM), except
+// FAST at 10 (128 measured 14% faster there).
+#include "kernel_entry.cuh"
+
+namespace bode {
+
+const KernelEntry* kernel_table_pad_a(int* count) {
+    static const KernelEntry table[] = {
+        BODE_BOTH_ARITH(HeatPad<8>, 1, 1, false, 1),
+        BODE_BOTH_ARITH(HeatPad<16>, 2, 1, false, 1),
+        BODE_BOTH_ARITH(HeatPad<32>, 4, 1, false, 1),
+        BODE_BOTH_ARITH_R(HeatPad<48>, 8, 1, false, 1, 128),
+        BODE_BOTH_ARITH_R(HeatPad<64>, 8, 1, false, 1, 128),
+        BODE_BOTH_ARITH_R(HeatPad<72>, 8, 1, false, 1, 128),
+        make_entry<HeatPad<80>, xd, 8, 1, false, 168>(1, 0),
+        make_entry<HeatPad<80>, double, 8, 1, false, 128>(1, 1),
+        BODE_BOTH_ARITH_R(HeatPad<96>, 8, 1, false, 1, 168),
+        BODE_BOTH_ARITH_R(HeatPad<104>, 8, 1, false, 1, 168),
+        BODE_BOTH_ARITH_R(HeatPad<112>, 8, 1, false, 1, 168),
+        BODE_BOTH_ARITH_R(HeatPad<128>, 16, 1, false, 1, 128),
+        BODE_BOTH_ARITH_R(HeatPad<144>, 16, 1, false, 1, 128),
+        BODE_BOTH_ARITH_R(HeatPad<160>, 16, 1, false, 1, 168),
+        BODE_BOTH_ARITH_R(HeatPad<192>, 16, 1, false, 1, 168),
+        BODE_BOTH_ARITH_R(HeatPad<208>, 16, 1, false, 1, 168),
+        BODE_BOTH_ARITH_R(HeatPad<224>, 16, 1, false, 1, 168),
+    };
+    *count = (int)(sizeof(table) / sizeof(table[0]));
+    return table;
+}
+
+}  // namespace bode

@@ -1,7 +1,8 @@
 // kernels_rkc.cu -- the RKC half of the built-in dispatch table (kernels.cu
-// holds the RKCK half and merges both): one entry per (problem, arithmetic
-// policy, lane-group width, register cap), plus the one-system-per-block
-// kernels for heatEquation(n) at any other n (wide.cuh).
+// holds the RKCK half and merges all parts): one entry per (problem,
+// arithmetic policy, lane-group width, register cap), plus the
+// one-system-per-block kernels for heatEquation(n) beyond the padded lane
+// groups (wide.cuh).
 #include "kernel_entry.cuh"
 
 namespace bode {
@@ -34,17 +35,9 @@ const KernelEntry* kernel_table_rkc(int* count) {
         BODE_BOTH_ARITH(Zero<1>, 1, 1, false, 4),
         BODE_BOTH_ARITH(Diag<3>, 1, 1, false, 6),
         BODE_BOTH_ARITH(Const<1>, 1, 1, false, 7),
-        // heatEquation(n) for any other n <= 1024: padded lane groups (8 components
-        // per lane as heat64; n > 64 on wider groups; 768 and 1024 spill under
-        // EXACT but still beat one system per block: 2.2x at n = 600, 1.4x at
-        // n = 1000, r02al)
-        BODE_BOTH_ARITH_R(HeatPad<64>, 8, 1, false, 1, 128),
-        BODE_BOTH_ARITH_R(HeatPad<128>, 16, 1, false, 1, 128),
-        BODE_BOTH_ARITH_R(HeatPad<256>, 32, 1, false, 1, 128),
-        BODE_BOTH_ARITH_R(HeatPad<512>, 32, 1, false, 1, 0),
-        BODE_BOTH_ARITH_R(HeatPad<768>, 32, 1, false, 1, 0),
-        BODE_BOTH_ARITH_R(HeatPad<1024>, 32, 1, false, 1, 0),
-        // ... and for any larger n: one system per thread block
+        // heatEquation(n) for any n without an exact-size kernel: padded lane
+        // groups up to n = 1024 (kernels_pad_a.cu, kernels_pad_b.cu), and for
+        // any larger n one system per thread block
         make_wide_entry<HeatWide, xd, 0>(1, 0),
         make_wide_entry<HeatWide, double, 0>(1, 1),
         make_wide_entry<HeatWide, xd, 1>(1, 0),

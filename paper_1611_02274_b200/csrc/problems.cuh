@@ -297,6 +297,17 @@ struct HeatPad {
             const int i = G.lane * C + c;
             const R um = (c > 0) ? u[c - 1] : left;
             const R up = (c < C - 1) ? u[c + 1] : right;
+#ifndef BODE_HEATPAD_BRANCHY
+            // The boundary and padding cases by selects, not branches (which
+            // diverge inside every lane group: i depends on the lane and the
+            // run-time n). Same IEEE operations per case as the reference:
+            // R(-2.0) * u == -(2u) exactly, so i = 0 is -(2u) + up, the last
+            // point um - 2u, the interior (um - 2u) + up.
+            const R u2 = R(2.0) * u[c];
+            const R a = (i == 0) ? -u2 : um - u2;
+            const R b = (i == n - 1) ? a : a + up;
+            out[c] = (i >= n) ? R(0.0) : b * inv;
+#else
             if (i >= n)
                 out[c] = R(0.0);
             else if (i == 0)
@@ -305,6 +316,7 @@ struct HeatPad {
                 out[c] = (um - R(2.0) * u[c]) * inv;
             else
                 out[c] = (um - R(2.0) * u[c] + up) * inv;
+#endif
         }
     }
 };
