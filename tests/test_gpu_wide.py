@@ -59,6 +59,24 @@ def test_heat_any_n_rkc_exact_bitwise(gpu, oracle, n, wide):
     _bitwise(y, st, yo, so)
 
 
+@pytest.mark.parametrize("n", [9, 12, 40, 70, 78, 90, 104, 110, 120, 140, 150, 180, 200, 210,
+                               220, 250, 280, 310, 350, 400, 420, 440, 500])
+def test_heat_every_padded_capacity_bitwise(gpu, oracle, n):
+    """One n inside every padded RKC capacity (kernels_pad_a.cu / _b.cu: 1, 2,
+    4, 8, 16 and 32 lanes, 6-16 components per lane), EXACT bitwise, and FAST
+    within relTol of the reference."""
+    num = 40
+    prob = A.make_problem(A.HEAT, n)
+    y0 = perturb(heat_ic(n), 0.01, 13 + n, num)
+    t1 = 0.02 if n <= 128 else 0.005
+    y, st = run_gpu(prob, A.SOLVER_RKC, y0, None, "exact", t1=t1, hout=t1)
+    rc, yo, so, _ = oracle.outer_loop(prob, A.SOLVER_RKC, 0.0, t1, t1, y0)
+    assert rc == 0
+    _bitwise(y, st, yo, so)
+    yf, _ = run_gpu(prob, A.SOLVER_RKC, y0, None, "fast", t1=t1, hout=t1)
+    assert sysrel(yf, yo, num, n).max() <= 1e-6
+
+
 @pytest.mark.parametrize("wide", [False, True], ids=["lanes", "blocks"])
 @pytest.mark.parametrize("n,t1", [(2, 0.1), (5, 0.05), (17, 0.01), (100, 1e-3)])
 def test_heat_any_n_rkck_exact_bitwise_and_fast(gpu, oracle, n, t1, wide):
