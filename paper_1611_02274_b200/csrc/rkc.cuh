@@ -220,7 +220,9 @@ struct F0Store<R, C, true> {
 // out[c] = num(c) / den(c) for the lane's C components. EXACT: IEEE
 // division; FAST: reciprocal multiply.
 constexpr bool kRkcStraightDiv = true;
-template <class R, int C, class Num, class Den>
+// ZERO_OK (run-time-dimension problems): +0 numerators, the padding, stay on
+// the straight-line path (arith.cuh div_rn_nv).
+template <class R, int C, bool ZERO_OK = false, class Num, class Den>
 __device__ __forceinline__ void elementwise_quotients(Num num, Den den, R (&out)[C]) {
     if constexpr (is_exact<R>::value && kRkcStraightDiv) {
         // straight-line quotients (arith.cuh div_rn_nv: the intrinsic's own fast
@@ -236,6 +238,17 @@ __device__ __forceinline__ void elementwise_quotients(Num num, Den den, R (&out)
             const double q = div_rn_nv(a[c], b[c], fast);
             ok = ok && fast;
             out[c] = R(q);
+        }
+        if constexpr (ZERO_OK) {
+            // a lane holding padding (+0 numerators) lands here every time:
+            // accept +0 / b in this cold re-test rather than in the loop above,
+            // which leaves lanes without padding exactly the plain code
+            if (!ok) {
+                ok = true;
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+                    ok = ok && (div_fast_path(a[c], b[c], val(out[c])) || div_zero_num(a[c], b[c]));
+            }
         }
         if (!ok) {
 #pragma unroll
@@ -472,7 +485,7 @@ __device__ __forceinline__ R rkc_initial_step(const Group<L>& G, bool on, R t, c
 #pragma unroll
     for (int c = 0; c < C; ++c) wa[c] = ys[c] + h * f0[c];
     P::template rhs<R, L>(G, t + h, wa, g, wb);
-    elementwise_quotients<R, C>([&](int c) { return wb[c] - f0[c]; },
+    elementwise_quotients<R, C, is_runtime_dim<P>::value>([&](int c) { return wb[c] - f0[c]; },
                                 [&](int c) { return absTol + relTol * fabs_(ys[c]); }, wa);
 #pragma unroll
     for (int c = 0; c < C; ++c) wa[c] = wa[c] * wa[c];
@@ -492,7 +505,7 @@ __device__ __forceinline__ R rkc_error_norm(const Group<L>& G, const R* g, const
                                             R relTol) {
     constexpr int C = P::N / L;
     R terms[C];
-    elementwise_quotients<R, C>(
+    elementwise_quotients<R, C, is_runtime_dim<P>::value>(
         [&](int c) { return R(0.8) * (ys[c] - y1[c]) + R(0.4) * h * (f0[c] + f1[c]); },
         [&](int c) { return absTol + relTol * fmax_abs(ys[c], y1[c]); }, terms);
 #pragma unroll

@@ -138,7 +138,7 @@ __global__ void exact_math_kernel(const double* __restrict__ x, long long n, int
         const double a = v, b = x[i + 1];
         ref = __ddiv_rn(a, b);
         bool fast;
-        got = bode::div_rn_nv(a, b, fast);
+        got = bode::div_rn_nv<true>(a, b, fast);  // (false only narrows `fast`)
         if (!fast) return;
     } else if (op == 3) {  // the EXACT policy's sqrt_ on every input (fallback included)
         ref = __dsqrt_rn(v);

@@ -61,3 +61,18 @@ def test_branch_free_matches_ieee(gpu, op):
         gpu.api.check(gpu.lib().bode_selftest_exact_math(A.dptr(x), x.size, op,
                                                          ctypes.byref(bad), ctypes.byref(first)))
         assert bad.value == 0, f"{bad.value} mismatches, first x = {x[first.value]!r}"
+
+
+def test_div_zero_numerator(gpu):
+    """+0 / b takes the straight-line division for every positive normal b
+    (the padding of run-time-dimension systems); -0 / b, +0 / subnormal, Inf,
+    NaN and negative b must still report the slow path or agree bitwise."""
+    from paper_1611_02274_b200 import _abi as A
+    bad, first = ctypes.c_int64(), ctypes.c_int64()
+    b = np.concatenate([full_range_cases(2_000_000, 77), cases(1_000_000, 78)])
+    for a in (0.0, -0.0):
+        x = np.empty(2 * b.size)
+        x[0::2], x[1::2] = a, b
+        gpu.api.check(gpu.lib().bode_selftest_exact_math(A.dptr(x), x.size, 2,
+                                                         ctypes.byref(bad), ctypes.byref(first)))
+        assert bad.value == 0, f"{bad.value} mismatches, first pair at {first.value}"
