@@ -39,6 +39,9 @@ static const KernelEntry* kernel_table_rkck(int* count) {
         BODE_BOTH_ARITH(Heat<8>, 1, 0, false, 1),
         // heatEquation(n), n <= 64 without an exact-size kernel (RKCK): padded groups
         BODE_BOTH_ARITH(HeatPad<16>, 2, 0, false, 1),
+        // (32 and 48: 1.3-2.2x over padding to 64 at n = 17-48, r02bl)
+        BODE_BOTH_ARITH_R(HeatPad<32>, 4, 0, false, 1, 128),
+        BODE_BOTH_ARITH_R(HeatPad<48>, 8, 0, false, 1, 128),
         BODE_BOTH_ARITH_R(HeatPad<64>, 8, 0, false, 1, 128),
     };
     *count = (int)(sizeof(table) / sizeof(table[0]));

@@ -78,7 +78,8 @@ def test_heat_every_padded_capacity_bitwise(gpu, oracle, n):
 
 
 @pytest.mark.parametrize("wide", [False, True], ids=["lanes", "blocks"])
-@pytest.mark.parametrize("n,t1", [(2, 0.1), (5, 0.05), (17, 0.01), (100, 1e-3)])
+@pytest.mark.parametrize("n,t1", [(2, 0.1), (5, 0.05), (17, 0.01), (40, 5e-3), (60, 2e-3),
+                                  (100, 1e-3)])
 def test_heat_any_n_rkck_exact_bitwise_and_fast(gpu, oracle, n, t1, wide):
     num = 64
     prob = A.make_problem(A.HEAT, n)

@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--num", type=int, default=1 << 18)
     ap.add_argument("--t1", type=float, default=0.1)
     ap.add_argument("--wide", type=int, default=0)
+    ap.add_argument("--solver", default="rkc", choices=["rkc", "rkck"])
     a = ap.parse_args()
     L = B.lib()
     L.bode_set_wide(a.wide)
@@ -43,7 +44,7 @@ def main():
             p = B.OdeProblem(A.HEAT, n, 0)
 
             def run():
-                B.int_driver_device(p, "rkc", arith, 0.0, a.t1, a.num, 0, yd.data_ptr(),
+                B.int_driver_device(p, a.solver, arith, 0.0, a.t1, a.num, 0, yd.data_ptr(),
                                     A.default_tol(), st.data_ptr(), 0, 0)
 
             run()
@@ -54,7 +55,7 @@ def main():
             torch.cuda.synchronize()
             dt = time.perf_counter() - t
             h = hashlib.sha1(yd.cpu().numpy().tobytes() + st.cpu().numpy().tobytes()).hexdigest()
-            print(json.dumps({"n": n, "arith": arith, "num": a.num, "t1": a.t1,
+            print(json.dumps({"n": n, "arith": arith, "solver": a.solver, "num": a.num, "t1": a.t1,
                               "system_windows_per_s": a.num / dt, "ms": dt * 1e3,
                               "state_hash": h[:16], "lib": os.environ.get("BODE_LIB_PATH", "")}),
                   flush=True)
