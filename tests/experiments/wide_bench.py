@@ -4,7 +4,7 @@
 the same systems, and the forced block kernel at n = 64 next to the 8-lane
 kernel.
 
-    python tools/wide_bench.py
+    python tests/experiments/wide_bench.py
 
 One window [0, 0.01] of RKC EXACT from the perturbed initial condition
 (problems.cpp:124-132, 0.01, seed 42); device time by CUDA events around
@@ -17,7 +17,7 @@ import time
 
 import numpy as np
 
-REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path[:0] = [REPO, os.path.join(REPO, "tests")]
 
 import torch  # noqa: E402

@@ -10,7 +10,7 @@ Bars: RKCK EXACT and RKC EXACT bitwise with every counter; RKCK FAST
 perturbation (0.01). At the 0.1 stress perturbation the FAST bar is asserted
 at the bound measured on B200 (regression guard): there, even the reference's
 own source compiled with FMA contraction misses 1e-13 on 13% of the systems
-(tools/fma_sensitivity.py, profiles/r02_fma_sensitivity.txt), so EXACT is
+(tests/experiments/fma_sensitivity.py, profiles/r02_fma_sensitivity.txt), so EXACT is
 the parity policy for that config.
 """
 import numpy as np

@@ -148,7 +148,7 @@ for p in $PARTS; do
 done
 for p in $PARTS; do
   case $p in
-    widebench) timeout 900 python tools/wide_bench.py > $OUT/wide_bench.jsonl 2> $OUT/wide_bench.err; echo "widebench rc=$?" >> $OUT/status.txt ;;
+    widebench) timeout 900 python tests/experiments/wide_bench.py > $OUT/wide_bench.jsonl 2> $OUT/wide_bench.err; echo "widebench rc=$?" >> $OUT/status.txt ;;
   esac
 done
 for p in $PARTS; do
