@@ -342,6 +342,20 @@ int block_for(const KernelEntry* e) {
 // kWideVecs state-length vectors in dynamic shared memory when they fit,
 // otherwise in a stream-ordered per-block scratch; a grid-stride loop over
 // the systems with the grid sized to the resident capacity.
+// Threads per block of the one-system-per-block kernels: one per component
+// up to 512 (wide_block), but 256 when shared memory then admits two or more
+// blocks per SM -- 1.14-1.51x for 1024 < n <= 1750 (r02bt/r02bu); with one
+// block per SM, or the vectors in the global scratch, 512 stays faster.
+int wide_threads(const void* fn, int n, size_t smem, bool in_smem, int* block) {
+    *block = bode::wide_block(n);
+    if (in_smem && *block > 256) {
+        int per_sm = 0;
+        BODE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem));
+        if (per_sm >= 2) *block = 256;
+    }
+    return BODE_OK;
+}
+
 int launch_wide(const KernelEntry* e, cudaStream_t s, const double* g, double* y, DevStats* st,
                 long long num, double t, double tEnd, DevTol tol, int merge) {
     const int n = tol.dim;
@@ -349,11 +363,12 @@ int launch_wide(const KernelEntry* e, cudaStream_t s, const double* g, double* y
     int dev = 0, sms = 0;
     BODE_CUDA(cudaGetDevice(&dev));
     BODE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int block = bode::wide_block(n);
     const size_t vec_bytes = (size_t)bode::kWideVecs * (size_t)n * sizeof(double);
     const bool in_smem = vec_bytes <= (size_t)bode::kWideSmemMax;
     const size_t smem = in_smem ? vec_bytes : 0;
     BODE_CUDA((cudaError_t)e->prepare(e->fn, dev, (int)smem));
+    int block = 0;
+    if (int rc = wide_threads(e->fn, n, smem, in_smem, &block)) return rc;
     long long grid = 1;
     if (in_smem) {
         int per_sm = 0;
@@ -1521,11 +1536,12 @@ int fixed_wide(const KernelEntry* e, const bode_problem_t* p, double t0, double 
     int dev = 0, sms = 0;
     BODE_CUDA(cudaGetDevice(&dev));
     BODE_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int block = bode::wide_block(n);
     const size_t vec_bytes = (size_t)bode::kWideVecs * (size_t)n * sizeof(double);
     const bool in_smem = vec_bytes <= (size_t)bode::kWideSmemMax;
     const size_t smem = in_smem ? vec_bytes : 0;
     BODE_CUDA((cudaError_t)e->prepare(e->ffn, dev, (int)smem));
+    int block = 0;
+    if (int rc = wide_threads(e->ffn, n, smem, in_smem, &block)) return rc;
     long long grid = 1;
     if (in_smem) {
         int per_sm = 0;
