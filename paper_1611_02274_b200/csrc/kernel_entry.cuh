@@ -42,6 +42,15 @@ __device__ __forceinline__ int comp_index(int lane, int c) {
         return lane * C + c;
 }
 
+// blockIdx.x * blockDim.x + threadIdx.x, read afresh (see integrate_kernel)
+__device__ __forceinline__ long long fresh_thread_index() {
+    unsigned tid, ctaid, ntid;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+    asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(ctaid));
+    asm volatile("mov.u32 %0, %%ntid.x;" : "=r"(ntid));
+    return (long long)ctaid * ntid + tid;
+}
+
 // MAXREG > 0 caps registers per thread (__maxnreg__) to reach a target
 // occupancy; 0 leaves ptxas the full 255 (launch bound kMaxBlock threads).
 template <class P, class R, int L, int SOLVER, bool KSMEM, int MAXREG, int INSTR>
@@ -88,19 +97,23 @@ __global__ void __maxnreg__(MAXREG > 0 ? MAXREG : 255)
         rkc_system_lane<P, R, INSTR>(G, t, tEnd, y, g, tol, st);
     else
         rkc_system<P, R, L, INSTR>(G, inRange, t, tEnd, y, g, tol, st);
-    if (!inRange) return;
+    // RKC lane groups: the system index again from the special registers
+    // (volatile reads, so it is recomputed here rather than kept live -- and
+    // spilled -- across the whole integration; the heat kernels' last spills).
+    const long long sys_out = kUniform ? fresh_thread_index() / L : sys;
+    if (kUniform ? sys_out >= num : !inRange) return;
 #pragma unroll
     for (int c = 0; c < C; ++c) {
         const int ci = comp_index<P, L>(G.lane, c);
-        if (ci < n) y_soa[sys + ld * (long long)ci] = val(y[c]);
+        if (ci < n) y_soa[sys_out + ld * (long long)ci] = val(y[c]);
     }
     if (stats != nullptr && G.lane == 0) {
         if (merge) {
-            DevStats o = stats[sys];
+            DevStats o = stats[sys_out];
             stats_merge(o, st);
-            stats[sys] = o;
+            stats[sys_out] = o;
         } else {
-            stats[sys] = st;
+            stats[sys_out] = st;
         }
     }
 }
