@@ -8,9 +8,10 @@
 // capacity close to n both pay: against round 2's set (8 components per lane,
 // capacities 64/128/256/...) this set measured 1.0x-7x, 1.3x-2.4x over most
 // of 64 < n <= 512 (profiles/r02bc_padded_caps.md). Register caps: 9
-// components fit 128 (16 warps/SM), 10-14 take 168 (12 warps/SM), except
-// FAST at 10 (128 measured 14% faster there) and EXACT at 13-14, uncapped
-// (+2-6%; 200 or uncapped costs 5-17% elsewhere, r02bo).
+// components fit 128 (16 warps/SM) under FAST, 168 under EXACT at 8 lanes;
+// 10-14 take 168 (12 warps/SM), except FAST at 10 (128 measured 14% faster
+// there) and EXACT at 13-14, uncapped (+2-6%; 200 or uncapped costs 5-17%
+// elsewhere, r02bo).
 #include "kernel_entry.cuh"
 
 #ifndef BODE_PAD_R168
@@ -26,7 +27,8 @@ const KernelEntry* kernel_table_pad_a(int* count) {
         BODE_BOTH_ARITH(HeatPad<32>, 4, 1, false, 1),
         BODE_BOTH_ARITH_R(HeatPad<48>, 8, 1, false, 1, 128),
         BODE_BOTH_ARITH_R(HeatPad<64>, 8, 1, false, 1, 128),
-        BODE_BOTH_ARITH_R(HeatPad<72>, 8, 1, false, 1, 128),
+        make_entry<HeatPad<72>, xd, 8, 1, false, 168>(1, 0),  // (128: 3-8% slower, r02by)
+        make_entry<HeatPad<72>, double, 8, 1, false, 128>(1, 1),
         make_entry<HeatPad<80>, xd, 8, 1, false, BODE_PAD_R168>(1, 0),
         make_entry<HeatPad<80>, double, 8, 1, false, 128>(1, 1),
         BODE_BOTH_ARITH_R(HeatPad<96>, 8, 1, false, 1, BODE_PAD_R168),
