@@ -73,6 +73,14 @@ def test_criterion4_rkc_beyond_euler_limit(gpu):  # acceptance.cpp:168-203
     batch = B.BatchStates(1, n, 0, heat_ic(n).copy(), np.zeros(0))
     r = B.integrate_batch(B.problems.heat_equation(n), batch, 0.0, 1.0, solver="rkc", tol=tol)
     assert r.stats["h_max_seen"][0] >= 100.0 * 2.0 / sigma   # 100x the explicit Euler limit
+    # the criterion's StepObserver (acceptance.cpp:175-182) through the device
+    # step trace: max accepted h and max accepted err <= 1, under both policies
+    for arith in ("exact", "fast"):
+        _, st, rec = B.trace_steps(B.problems.heat_equation(n), heat_ic(n).copy(), None, 0.0, 1.0,
+                                   solver="rkc", arith=arith, tol=tol)
+        acc = rec[rec["accepted"] == 1]
+        assert len(acc) == st["steps_accepted"] > 0
+        assert acc["h"].max() >= 100.0 * 2.0 / sigma and acc["err"].max() <= 1.0
     # max-norm monotone over 50 checkpointed restarts of the same run
     u, prev = heat_ic(n).copy(), 1.0
     for k in range(50):
