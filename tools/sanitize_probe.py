@@ -48,12 +48,13 @@ def main():
                  sink=lambda t, s: snaps.append(t))
     B.outer_loop(pl, b, 0.0, 0.3, 0.1, solver="rkck", arith="fast", gpus=2,
                  sink=lambda t, s: snaps.append(t))
-    # heat with a run-time dimension: padded lane groups (n = 100 in HeatPad<128>,
-    # n = 1000 in HeatPad<1024>), one system per block with the vectors in shared
+    # heat with a run-time dimension: padded lane groups (n = 100 in HeatPad<104>
+    # (RKC) / <128> (RKCK), n = 300 in <320> / <512> (RKCK: stages in shared
+    # memory), n = 1000 in <1024>), one system per block with the vectors in shared
     # memory (n = 1500, and n = 100 forced onto the block kernels) and in the
     # per-block global scratch (n = 4000)
-    for n, t1, force in ((100, 1e-3, 0), (1000, 1e-4, 0), (1500, 1e-5, 0), (100, 1e-3, 1),
-                         (4000, 1e-5, 0)):
+    for n, t1, force in ((100, 1e-3, 0), (300, 1e-4, 0), (1000, 1e-4, 0), (1500, 1e-5, 0),
+                         (100, 1e-3, 1), (4000, 1e-5, 0)):
         hw = B.problems.heat_equation(n)
         wb = B.problems.perturb_initial_conditions(heat_ic(n), 0.01, 3, 20)
         L.bode_set_wide(force)
