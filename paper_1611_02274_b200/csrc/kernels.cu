@@ -43,12 +43,15 @@ static const KernelEntry* kernel_table_rkck(int* count) {
         BODE_BOTH_ARITH_R(HeatPad<32>, 4, 0, false, 1, 128),
         BODE_BOTH_ARITH_R(HeatPad<48>, 8, 0, false, 1, 128),
         BODE_BOTH_ARITH_R(HeatPad<64>, 8, 0, false, 1, 128),
-        // n in (64, 512]: 1.5-4.2x over one system per block (r02cc, r02cd); 512
-        // keeps the stages in shared memory (spill-free), 128 and 256 in
+        // n in (64, 768]: 1.4-4.2x over one system per block (r02cc, r02cd,
+        // r02cg); 512 and 768 keep the stages in shared memory, 128 and 256 in
         // registers (stages in shared memory measured 2-3% slower there)
         BODE_BOTH_ARITH_R(HeatPad<128>, 16, 0, false, 1, 128),
         BODE_BOTH_ARITH_R(HeatPad<256>, 32, 0, false, 1, 128),
         BODE_BOTH_ARITH_R(HeatPad<512>, 32, 0, true, 1, 0),
+        // 768: 1.4x / 2.1x (EXACT / FAST) at n = 600; a 1024 capacity lost to
+        // the block kernel under EXACT (0.80x at n = 1000, r02cg)
+        BODE_BOTH_ARITH_R(HeatPad<768>, 32, 0, true, 1, 0),
     };
     *count = (int)(sizeof(table) / sizeof(table[0]));
     return table;
