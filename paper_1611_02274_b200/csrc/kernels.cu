@@ -12,9 +12,10 @@ long long rkc_table_doubles() { return kRkcTableDoubles; }
 // kernels_rkc.cu: the RKC entries and the one-system-per-block heat kernels
 // (a second translation unit, so the two halves compile in parallel)
 const KernelEntry* kernel_table_rkc(int* count);
-// kernels_pad_a.cu / kernels_pad_b.cu: RKC heatEquation(n) on padded lane groups
+// kernels_pad_{a,b,c}.cu: RKC heatEquation(n) on padded lane groups
 const KernelEntry* kernel_table_pad_a(int* count);
 const KernelEntry* kernel_table_pad_b(int* count);
+const KernelEntry* kernel_table_pad_c(int* count);
 
 static const KernelEntry* kernel_table_rkck(int* count) {
     static const KernelEntry table[] = {
@@ -63,7 +64,8 @@ const KernelEntry* kernel_table(int* count) {
         int n = 0;
         const KernelEntry* a = kernel_table_rkck(&n);
         v.insert(v.end(), a, a + n);
-        for (auto part : {kernel_table_rkc, kernel_table_pad_a, kernel_table_pad_b}) {
+        for (auto part : {kernel_table_rkc, kernel_table_pad_a, kernel_table_pad_b,
+                          kernel_table_pad_c}) {
             const KernelEntry* b = part(&n);
             v.insert(v.end(), b, b + n);
         }

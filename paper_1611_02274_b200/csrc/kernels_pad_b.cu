@@ -1,7 +1,6 @@
 // kernels_pad_b.cu -- RKC heatEquation(n) on padded 32-lane groups for
-// 224 < n <= 1024 (see kernels_pad_a.cu). 8-16 components per lane; 768 and
-// 1024 spill under EXACT but still beat one system per block (2.2x at n =
-// 600, 1.4x at n = 1000, r02al).
+// 224 < n <= 512 (see kernels_pad_a.cu): 8-16 components per lane.
+// kernels_pad_c.cu holds 512 < n <= 1024.
 #include "kernel_entry.cuh"
 
 #ifndef BODE_PAD_R168
@@ -21,8 +20,6 @@ const KernelEntry* kernel_table_pad_b(int* count) {
         make_entry<HeatPad<448>, xd, 32, 1, false, 0>(1, 0),
         make_entry<HeatPad<448>, double, 32, 1, false, BODE_PAD_R168>(1, 1),
         BODE_BOTH_ARITH_R(HeatPad<512>, 32, 1, false, 1, 0),
-        BODE_BOTH_ARITH_R(HeatPad<768>, 32, 1, false, 1, 0),
-        BODE_BOTH_ARITH_R(HeatPad<1024>, 32, 1, false, 1, 0),
     };
     *count = (int)(sizeof(table) / sizeof(table[0]));
     return table;
