@@ -17,6 +17,10 @@ const KernelEntry* kernel_table_pad_c(int* count) {
         BODE_BOTH_ARITH_R(HeatPad<896>, 32, 1, false, 1, 0),
         BODE_BOTH_ARITH_R(HeatPad<960>, 32, 1, false, 1, 0),
         BODE_BOTH_ARITH_R(HeatPad<1024>, 32, 1, false, 1, 0),
+        // FAST only past 1024: 1.6-1.8x over one system per block at n = 1100 /
+        // 1250, while EXACT (heavier spills) measured 1.04x / 0.92x (r02cm)
+        make_entry<HeatPad<1152>, double, 32, 1, false, 0>(1, 1),
+        make_entry<HeatPad<1280>, double, 32, 1, false, 0>(1, 1),
     };
     *count = (int)(sizeof(table) / sizeof(table[0]));
     return table;

@@ -96,7 +96,7 @@ def test_heat_any_n_rkck_exact_bitwise_and_fast(gpu, oracle, n, t1, wide):
         assert np.array_equal(st[k], so[k]), k
 
 
-@pytest.mark.parametrize("n", [37, 200])
+@pytest.mark.parametrize("n", [37, 200, 1100, 1250])  # 1100, 1250: FAST-only capacities
 def test_heat_any_n_rkc_fast_within_reltol(gpu, oracle, n):
     num = 64
     prob = A.make_problem(A.HEAT, n)
